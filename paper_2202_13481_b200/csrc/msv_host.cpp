@@ -1,0 +1,1227 @@
+// Host runtime behind the C ABI (include/msv.h): contexts, immutable input
+// uploads with the reference's validation rules, grid construction (waves,
+// scenario classes), kernel orchestration on the context stream and result
+// assembly. Compiled with -ffp-contract=off: the cdf partial sum and the
+// host-side copies of reference arithmetic must round like the reference.
+#include <math.h>
+#include <string.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <map>
+#include <memory>
+#include <numeric>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "msv_internal.h"
+#include "msv_math.h"
+
+using msv::DevOut;
+using msv::DevPart;
+using msv::DevScen;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, std::string msg) {
+    g_err = std::move(msg);
+    return code;
+}
+
+#define MSV_CUDA_TRY(x)                                                                  \
+    do {                                                                                 \
+        cudaError_t e_ = (x);                                                            \
+        if (e_ != cudaSuccess) return fail(MSV_CUDA, std::string(#x ": ") + cudaGetErrorString(e_)); \
+    } while (0)
+
+struct DevBuf {
+    void* p = nullptr;
+    size_t bytes = 0;
+    DevBuf() = default;
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    ~DevBuf() { release(); }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        bytes = 0;
+    }
+    cudaError_t ensure(size_t n) {
+        if (n <= bytes && p) return cudaSuccess;
+        release();
+        if (n == 0) n = 16;
+        cudaError_t e = cudaMalloc(&p, n);
+        if (e == cudaSuccess) bytes = n;
+        return e;
+    }
+    template <typename T>
+    T* as() const {
+        return static_cast<T*>(p);
+    }
+};
+
+struct Profile {
+    std::vector<int32_t> sizes;
+    int b_max = 0;
+    std::vector<double> lat, util;
+    int cell_off = 0;
+};
+
+struct Dist {
+    std::vector<double> pmf, cdf;
+    size_t dev_off = 0;
+};
+
+struct Plan {
+    int num_gpus = 0, gpcs_per_gpu = 0;
+    std::vector<int32_t> flat;  // partition sizes by id (plan.flatten(), paris.hpp:134-139)
+    int err = 0;                // deferred PartitionPlan::validate() failure
+    std::string err_msg;
+};
+
+struct Routing {
+    std::vector<int32_t> k, first, last;
+};
+
+// glibc's log1p build selected on this host (rng.hpp:20 calls whichever one the
+// ifunc resolver picked). Probe inputs where the two builds round differently.
+int probe_host_log1p() {
+    uint64_t s = 0x9E3779B97F4A7C15ull;
+    int fma_votes = 0, gen_votes = 0;
+    for (int it = 0; it < 2000000 && fma_votes + gen_votes < 16; ++it) {
+        s ^= s << 13;
+        s ^= s >> 7;
+        s ^= s << 17;
+        const double u = (double)(s >> 11) * 0x1.0p-53;
+        const double a = msv_log1p_neg(-u, MSV_LOG1P_FMA);
+        const double g = msv_log1p_neg(-u, MSV_LOG1P_GENERIC);
+        if (msv_dbits(a) == msv_dbits(g)) continue;
+        volatile double xin = -u;
+        const double h = log1p(xin);
+        if (msv_dbits(h) == msv_dbits(a)) ++fma_votes;
+        else if (msv_dbits(h) == msv_dbits(g)) ++gen_votes;
+    }
+    return gen_votes > fma_votes ? MSV_LOG1P_GENERIC : MSV_LOG1P_FMA;
+}
+
+}  // namespace
+
+namespace migserve_capi {
+int set_error(int code, const char* what) { return fail(code, what ? what : ""); }
+}  // namespace migserve_capi
+
+struct msv_ctx {
+    int device = 0;
+    int sms = 148;
+    cudaStream_t stream = nullptr;
+    int log1p = MSV_LOG1P_FMA;
+    int64_t launches = 0;
+    int64_t h2d = 0, d2h = 0;
+    cudaEvent_t ev[8] = {};
+    std::vector<Profile> profiles;
+    std::vector<Dist> dists;
+    std::vector<Plan> plans;
+    std::vector<Routing> routings;
+    // concatenated profile cells / cdfs on the device
+    DevBuf d_lat, d_util, d_cdf;
+    int n_cells = 0;
+    bool tables_dirty = true;
+
+    int sync_tables() {
+        if (!tables_dirty) return MSV_OK;
+        std::vector<double> lat, util, cdf;
+        for (Profile& p : profiles) {
+            p.cell_off = (int)lat.size();
+            lat.insert(lat.end(), p.lat.begin(), p.lat.end());
+            util.insert(util.end(), p.util.begin(), p.util.end());
+        }
+        for (Dist& d : dists) {
+            d.dev_off = cdf.size();
+            cdf.insert(cdf.end(), d.cdf.begin(), d.cdf.end());
+        }
+        n_cells = (int)lat.size();
+        MSV_CUDA_TRY(d_lat.ensure(std::max<size_t>(lat.size(), 1) * 8));
+        MSV_CUDA_TRY(d_util.ensure(std::max<size_t>(util.size(), 1) * 8));
+        MSV_CUDA_TRY(d_cdf.ensure(std::max<size_t>(cdf.size(), 1) * 8));
+        if (!lat.empty()) {
+            MSV_CUDA_TRY(cudaMemcpy(d_lat.p, lat.data(), lat.size() * 8, cudaMemcpyHostToDevice));
+            MSV_CUDA_TRY(cudaMemcpy(d_util.p, util.data(), util.size() * 8, cudaMemcpyHostToDevice));
+        }
+        if (!cdf.empty()) MSV_CUDA_TRY(cudaMemcpy(d_cdf.p, cdf.data(), cdf.size() * 8, cudaMemcpyHostToDevice));
+        tables_dirty = false;
+        return MSV_OK;
+    }
+};
+
+namespace {
+
+struct SetDevice {
+    int prev = -1;
+    explicit SetDevice(int dev) {
+        cudaGetDevice(&prev);
+        if (prev != dev) cudaSetDevice(dev);
+    }
+    ~SetDevice() {
+        int cur = -1;
+        cudaGetDevice(&cur);
+        if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+    }
+};
+
+// Scenario class: W lanes per scenario, S partition slots per lane, scheduler.
+struct ClassKey {
+    int W, S, sched;
+    bool operator<(const ClassKey& o) const {
+        return std::tie(W, S, sched) < std::tie(o.W, o.S, o.sched);
+    }
+};
+
+ClassKey class_of(int P, int sched) {
+    ClassKey c{32, 1, sched};
+    if (P <= 4) c.W = 4;
+    else if (P <= 8) c.W = 8;
+    else if (P <= 16) c.W = 16;
+    else if (P <= 32) c.W = 32;
+    else if (P <= 64) c.S = 2;
+    else c.S = 4;
+    return c;
+}
+
+std::string fmt_num(double v) {
+    char buf[64];
+    snprintf(buf, sizeof buf, "%g", v);
+    return buf;
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// Grid: everything one launch needs, resident on the device.
+// ---------------------------------------------------------------------------
+struct msv_grid {
+    msv_ctx* ctx = nullptr;
+    bool generated = true;
+    bool records = false;
+    int64_t n = 0;
+    std::vector<msv_scenario> scen;
+    std::vector<double> tail_p;
+    std::vector<int64_t> cap, toff;   // per-scenario trace capacity and offset
+    std::vector<int32_t> P, usage_off;
+    int64_t usage_total = 0;
+    struct Wave {
+        int64_t s0 = 0, s1 = 0;  // scenarios [s0, s1)
+        int64_t q0 = 0, q1 = 0;  // trace slots [q0, q1)
+        std::vector<std::pair<ClassKey, std::vector<int32_t>>> classes;
+        std::vector<int64_t> work_off;  // offset of each class's work list in d_work
+    };
+    std::vector<Wave> waves;
+    int64_t max_wave_q = 0;
+    DevBuf d_scen, d_out, d_tjobs, d_tailjobs, d_tails, d_p, d_usage, d_nq, d_tovf, d_parts, d_masks,
+        d_work, d_counter;
+    DevBuf d_arr, d_bat, d_next, d_samples, d_rec, d_glat, d_gutil;
+    int n_cells = 0;
+    std::vector<DevScen> h_scen;  // pointers into the wave buffers
+    cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+    float t_total = 0, t_trace = 0, t_sim = 0, t_tail = 0;
+    int64_t queries = -1;
+    std::vector<int64_t> host_n;  // replay: trace lengths
+
+    ~msv_grid() {
+        for (cudaEvent_t& e : ev)
+            if (e) cudaEventDestroy(e);
+    }
+};
+
+namespace {
+
+// Reference checks of run()/sample_trace() arguments, in the reference's order:
+// sample_trace (workload.hpp:100-101), then run (engine.hpp:118-124, sched.hpp:44-47,
+// paris.hpp:141-156), then the lookups the engine would hit (profile.hpp:123-132).
+int validate_scenario(const msv_ctx* ctx, const msv_scenario& s, bool generated, int32_t* P_out) {
+    if (s.profile < 0 || s.profile >= (int)ctx->profiles.size())
+        return fail(MSV_PARAM, "scenario: unknown profile handle " + std::to_string(s.profile));
+    if (s.plan < 0 || s.plan >= (int)ctx->plans.size())
+        return fail(MSV_PARAM, "scenario: unknown plan handle " + std::to_string(s.plan));
+    if (generated) {
+        if (s.dist < 0 || s.dist >= (int)ctx->dists.size())
+            return fail(MSV_PARAM, "scenario: unknown dist handle " + std::to_string(s.dist));
+        if (!(s.rate_qps > 0.0)) return fail(MSV_PARAM, "sample_trace: rate must be > 0");
+        if (s.duration_ms < 0.0) return fail(MSV_PARAM, "sample_trace: duration must be >= 0");
+    }
+    if (s.scheduler != MSV_FIFS && s.scheduler != MSV_ELSA)
+        return fail(MSV_VALIDATION, "unknown scheduler " + std::to_string(s.scheduler));
+    const Plan& plan = ctx->plans[s.plan];
+    if (plan.err) return fail(plan.err, plan.err_msg);
+    if (!(s.sla_ms > 0.0)) return fail(MSV_PARAM, "sla: target must be > 0");
+    if (s.alpha < 0.0 || s.beta < 0.0) return fail(MSV_PARAM, "sla: alpha/beta must be >= 0");
+    if (plan.flat.empty()) return fail(MSV_PARAM, "run: plan has no partition instances");
+    if (s.warmup_fraction < 0.0 || s.warmup_fraction >= 1.0)
+        return fail(MSV_PARAM, "run: warmup_fraction must be in [0,1)");
+    if (s.routing >= 0) {
+        if (s.routing >= (int)ctx->routings.size())
+            return fail(MSV_PARAM, "scenario: unknown routing handle " + std::to_string(s.routing));
+        if (ctx->routings[s.routing].k.empty())
+            return fail(MSV_PARAM, "run: segment_routing enabled without segments");
+        if (ctx->profiles[s.profile].b_max > 64)
+            return fail(MSV_PARAM, "segment routing on the device supports b_max <= 64");
+    }
+    if ((int)plan.flat.size() > 128)
+        return fail(MSV_PARAM, "run: the device engine supports at most 128 partitions per plan");
+    // Plan sizes missing from the profile are not an up-front error: like the
+    // reference, the engine raises LookupError only if a lookup reaches them.
+    *P_out = (int32_t)plan.flat.size();
+    return MSV_OK;
+}
+
+// by_ascending_size order (sched.hpp:96-104) of the plan's partitions.
+std::vector<DevPart> plan_parts(const Plan& plan, const Profile& prof, int cell_off) {
+    std::vector<DevPart> parts;
+    for (int32_t id = 0; id < (int32_t)plan.flat.size(); ++id) {
+        const int32_t k = plan.flat[id];
+        const auto it = std::lower_bound(prof.sizes.begin(), prof.sizes.end(), k);
+        const int32_t row = (it == prof.sizes.end() || *it != k)
+                                ? -1
+                                : cell_off + (int32_t)(it - prof.sizes.begin()) * prof.b_max;
+        parts.push_back(DevPart{id, k, row, 0});
+    }
+    std::stable_sort(parts.begin(), parts.end(), [](const DevPart& a, const DevPart& b) {
+        if (a.k != b.k) return a.k < b.k;
+        return a.pid < b.pid;
+    });
+    return parts;
+}
+
+// Per-partition candidate masks of segment routing (engine.hpp:197-203).
+std::vector<uint64_t> route_masks(const std::vector<DevPart>& parts, const Routing& r, int b_max) {
+    std::vector<uint64_t> m;
+    for (const DevPart& p : parts) {
+        uint64_t bits = 0;
+        for (int b = 1; b <= b_max && b <= 64; ++b)
+            for (size_t j = 0; j < r.k.size(); ++j)
+                if (r.k[j] == p.k && b >= r.first[j] && b <= r.last[j]) {
+                    bits |= 1ull << (b - 1);
+                    break;
+                }
+        m.push_back(bits);
+    }
+    return m;
+}
+
+int64_t trace_capacity(double rate_qps, double duration_ms) {
+    const double mean = rate_qps * duration_ms / 1000.0;
+    if (!(mean < 4e9)) return -1;
+    return (int64_t)ceil(mean + 10.0 * sqrt(mean) + 160.0);
+}
+
+size_t free_device_bytes() {
+    size_t fr = 0, tot = 0;
+    cudaMemGetInfo(&fr, &tot);
+    return fr;
+}
+
+// Build a grid. generated: traces from K1; otherwise host traces (offsets/arrival/batch).
+int grid_build(msv_ctx* ctx, const msv_scenario* sc, int64_t n, const double* tail_p, int n_tails,
+               const int64_t* offsets, const double* arrival, const int32_t* batch, bool records,
+               msv_grid** out, const int64_t* cap_override = nullptr) {
+    if (n < 0) return fail(MSV_PARAM, "grid: negative scenario count");
+    if (n_tails < 0 || n_tails > 4) return fail(MSV_PARAM, "grid: between 0 and 4 tail percentiles");
+    for (int j = 0; j < n_tails; ++j)
+        if (!(tail_p[j] > 0.0) || !(tail_p[j] < 1.0))
+            return fail(MSV_PARAM, "tail_latency: percentile must be in (0,1)");
+    int rc = ctx->sync_tables();
+    if (rc) return rc;
+    std::unique_ptr<msv_grid> g(new msv_grid);
+    g->ctx = ctx;
+    g->generated = offsets == nullptr;
+    g->records = records;
+    g->n = n;
+    g->scen.assign(sc, sc + n);
+    g->tail_p.assign(tail_p, tail_p + n_tails);
+    g->cap.resize(n);
+    g->toff.resize(n);
+    g->P.resize(n);
+    g->usage_off.resize(n);
+    for (int64_t i = 0; i < n; ++i) {
+        int32_t P = 0;
+        rc = validate_scenario(ctx, sc[i], g->generated, &P);
+        if (rc) {
+            g_err = "scenario " + std::to_string(i) + ": " + g_err;
+            return rc;
+        }
+        g->P[i] = P;
+        g->usage_off[i] = (int32_t)g->usage_total;
+        g->usage_total += P;
+        if (g->generated) {
+            g->cap[i] = cap_override ? cap_override[i] : trace_capacity(sc[i].rate_qps, sc[i].duration_ms);
+            if (g->cap[i] < 0) return fail(MSV_PARAM, "sample_trace: expected trace too long");
+        } else {
+            g->cap[i] = offsets[i + 1] - offsets[i];
+            if (g->cap[i] < 0) return fail(MSV_PARAM, "replay: offsets must be nondecreasing");
+            if (g->cap[i] >= (int64_t)0xFFFFFFFFll) return fail(MSV_PARAM, "replay: trace too long");
+            const int b_max = ctx->profiles[sc[i].profile].b_max;
+            for (int64_t q = offsets[i]; q < offsets[i + 1]; ++q) {
+                if (batch[q] < 1 || batch[q] > b_max)
+                    return fail(MSV_LOOKUP, "scenario " + std::to_string(i) + ": profile: batch " +
+                                                std::to_string(batch[q]) + " outside grid 1.." +
+                                                std::to_string(b_max));
+                if (q > offsets[i] && arrival[q] < arrival[q - 1])
+                    return fail(MSV_VALIDATION, "scenario " + std::to_string(i) +
+                                                    ": replay traces must be sorted by arrival_ms");
+            }
+        }
+    }
+    // Waves: bound the per-launch trace working set (arrival 8 + batch 4 + link 4 +
+    // sample 8 [+ record 24] bytes per query slot).
+    const size_t per_q = 24 + (records ? sizeof(msv_record) : 0);
+    size_t budget = free_device_bytes() / 2;
+    if (budget > ((size_t)48 << 30)) budget = (size_t)48 << 30;
+    const int64_t max_q = std::max<int64_t>((int64_t)(budget / per_q), 1 << 20);
+    // Long scenarios first inside each wave (work stealing balances the rest).
+    std::vector<int64_t> order(n);
+    std::iota(order.begin(), order.end(), 0);
+    {
+        int64_t s0 = 0;
+        while (s0 < n) {
+            msv_grid::Wave w;
+            w.s0 = s0;
+            int64_t q = 0;
+            int64_t s1 = s0;
+            while (s1 < n && (s1 == s0 || q + g->cap[s1] <= max_q)) q += g->cap[s1++];
+            w.s1 = s1;
+            g->waves.push_back(std::move(w));
+            s0 = s1;
+        }
+    }
+    int64_t qoff_global = 0;
+    for (msv_grid::Wave& w : g->waves) {
+        w.q0 = qoff_global;
+        int64_t q = 0;
+        for (int64_t i = w.s0; i < w.s1; ++i) {
+            g->toff[i] = q;  // offset inside the wave buffers
+            q += g->cap[i];
+        }
+        w.q1 = w.q0 + q;
+        qoff_global += q;
+        g->max_wave_q = std::max(g->max_wave_q, q);
+        std::map<ClassKey, std::vector<int32_t>> cls;
+        for (int64_t i = w.s0; i < w.s1; ++i) cls[class_of(g->P[i], sc[i].scheduler)].push_back((int32_t)i);
+        for (auto& kv : cls) {
+            std::stable_sort(kv.second.begin(), kv.second.end(),
+                             [&](int32_t a, int32_t b) { return g->cap[a] > g->cap[b]; });
+            w.classes.emplace_back(kv.first, std::move(kv.second));
+        }
+    }
+    // Device buffers.
+    const size_t wq = (size_t)std::max<int64_t>(g->max_wave_q, 1);
+    MSV_CUDA_TRY(g->d_arr.ensure(wq * 8));
+    MSV_CUDA_TRY(g->d_bat.ensure(wq * 4));
+    MSV_CUDA_TRY(g->d_next.ensure(wq * 4));
+    MSV_CUDA_TRY(g->d_samples.ensure(wq * 8));
+    if (records) MSV_CUDA_TRY(g->d_rec.ensure(wq * sizeof(msv_record)));
+    MSV_CUDA_TRY(g->d_scen.ensure(std::max<int64_t>(n, 1) * sizeof(DevScen)));
+    MSV_CUDA_TRY(g->d_out.ensure(std::max<int64_t>(n, 1) * sizeof(DevOut)));
+    MSV_CUDA_TRY(g->d_tjobs.ensure(std::max<int64_t>(n, 1) * sizeof(msv::TraceJob)));
+    MSV_CUDA_TRY(g->d_tailjobs.ensure(std::max<int64_t>(n, 1) * sizeof(msv::TailJob)));
+    MSV_CUDA_TRY(g->d_tails.ensure(std::max<int64_t>(n, 1) * 4 * sizeof(double)));
+    MSV_CUDA_TRY(g->d_p.ensure(4 * sizeof(double)));
+    MSV_CUDA_TRY(g->d_usage.ensure(std::max<int64_t>(g->usage_total, 1) * sizeof(msv_usage)));
+    MSV_CUDA_TRY(g->d_nq.ensure(std::max<int64_t>(n, 1) * 8));
+    MSV_CUDA_TRY(g->d_tovf.ensure(std::max<int64_t>(n, 1) * 4));
+    MSV_CUDA_TRY(g->d_counter.ensure(64 * sizeof(int32_t)));
+    if (n_tails) MSV_CUDA_TRY(cudaMemcpy(g->d_p.p, tail_p, n_tails * sizeof(double), cudaMemcpyHostToDevice));
+
+    // Compact profile table of this grid (staged in shared memory by the kernel).
+    std::map<int, int> grid_cell_off;
+    std::vector<double> glat, gutil;
+    for (int64_t i = 0; i < n; ++i) {
+        if (grid_cell_off.count(sc[i].profile)) continue;
+        const Profile& pr = ctx->profiles[sc[i].profile];
+        grid_cell_off[sc[i].profile] = (int)glat.size();
+        glat.insert(glat.end(), pr.lat.begin(), pr.lat.end());
+        gutil.insert(gutil.end(), pr.util.begin(), pr.util.end());
+    }
+    if ((int)glat.size() > msv::kMaxSmemCells)
+        return fail(MSV_PARAM, "grid: profiles of one call exceed the device table capacity (" +
+                                   std::to_string(msv::kMaxSmemCells) + " cells)");
+    g->n_cells = (int)glat.size();
+    MSV_CUDA_TRY(g->d_glat.ensure(std::max<size_t>(glat.size(), 1) * 8));
+    MSV_CUDA_TRY(g->d_gutil.ensure(std::max<size_t>(gutil.size(), 1) * 8));
+    if (!glat.empty()) {
+        MSV_CUDA_TRY(cudaMemcpy(g->d_glat.p, glat.data(), glat.size() * 8, cudaMemcpyHostToDevice));
+        MSV_CUDA_TRY(cudaMemcpy(g->d_gutil.p, gutil.data(), gutil.size() * 8, cudaMemcpyHostToDevice));
+    }
+    // Partition tables per (plan, profile) and routing masks per (plan, profile, routing).
+    std::map<std::pair<int, int>, size_t> part_off;
+    std::map<std::tuple<int, int, int>, size_t> mask_off;
+    std::vector<DevPart> parts_h;
+    std::vector<uint64_t> masks_h;
+    std::vector<size_t> sc_part(n), sc_mask(n, (size_t)-1);
+    for (int64_t i = 0; i < n; ++i) {
+        auto key = std::make_pair(sc[i].plan, sc[i].profile);
+        auto it = part_off.find(key);
+        if (it == part_off.end()) {
+            std::vector<DevPart> pp =
+                plan_parts(ctx->plans[sc[i].plan], ctx->profiles[sc[i].profile], grid_cell_off[sc[i].profile]);
+            it = part_off.emplace(key, parts_h.size()).first;
+            parts_h.insert(parts_h.end(), pp.begin(), pp.end());
+        }
+        sc_part[i] = it->second;
+        if (sc[i].routing >= 0) {
+            auto mk = std::make_tuple(sc[i].plan, sc[i].profile, sc[i].routing);
+            auto mt = mask_off.find(mk);
+            if (mt == mask_off.end()) {
+                std::vector<DevPart> pp(parts_h.begin() + it->second, parts_h.begin() + it->second + g->P[i]);
+                std::vector<uint64_t> mm =
+                    route_masks(pp, ctx->routings[sc[i].routing], ctx->profiles[sc[i].profile].b_max);
+                mt = mask_off.emplace(mk, masks_h.size()).first;
+                masks_h.insert(masks_h.end(), mm.begin(), mm.end());
+            }
+            sc_mask[i] = mt->second;
+        }
+    }
+    MSV_CUDA_TRY(g->d_parts.ensure(std::max<size_t>(parts_h.size(), 1) * sizeof(DevPart)));
+    MSV_CUDA_TRY(g->d_masks.ensure(std::max<size_t>(masks_h.size(), 1) * 8));
+    if (!parts_h.empty())
+        MSV_CUDA_TRY(cudaMemcpy(g->d_parts.p, parts_h.data(), parts_h.size() * sizeof(DevPart), cudaMemcpyHostToDevice));
+    if (!masks_h.empty())
+        MSV_CUDA_TRY(cudaMemcpy(g->d_masks.p, masks_h.data(), masks_h.size() * 8, cudaMemcpyHostToDevice));
+
+    // Per-scenario device descriptors.
+    g->h_scen.resize(n);
+    std::vector<msv::TraceJob> tj(n);
+    std::vector<msv::TailJob> lj(n);
+    for (int64_t i = 0; i < n; ++i) {
+        const msv_scenario& s = sc[i];
+        const Profile& prof = ctx->profiles[s.profile];
+        DevScen& d = g->h_scen[i];
+        const int64_t o = g->toff[i];
+        d.arrival = g->d_arr.as<double>() + o;
+        d.batch = g->d_bat.as<int32_t>() + o;
+        d.n = g->d_nq.as<int64_t>() + i;
+        d.duration_ms = s.duration_ms;
+        d.warmup_ms = s.warmup_fraction * s.duration_ms;  // engine.hpp:238
+        d.sla = s.sla_ms;
+        d.alpha = s.alpha;
+        d.beta = s.beta;
+        d.parts = g->d_parts.as<DevPart>() + sc_part[i];
+        d.route_mask = (sc_mask[i] == (size_t)-1) ? nullptr : g->d_masks.as<uint64_t>() + sc_mask[i];
+        d.next = g->d_next.as<uint32_t>() + o;
+        d.samples = g->d_samples.as<double>() + o;
+        d.records = records ? g->d_rec.as<msv_record>() + o : nullptr;
+        d.P = g->P[i];
+        d.b_max = prof.b_max;
+        d.sched = s.scheduler;
+        d.flags = s.flags;
+        d.usage_off = g->usage_off[i];
+        d.pad = 0;
+        msv::TraceJob& t = tj[i];
+        t.seed = s.seed;
+        t.rate_per_ms = s.rate_qps / 1000.0;  // workload.hpp:103
+        t.duration_ms = s.duration_ms;
+        t.cdf = g->generated ? ctx->d_cdf.as<double>() + ctx->dists[s.dist].dev_off : nullptr;
+        t.b_max = g->generated ? (int32_t)ctx->dists[s.dist].cdf.size() : 0;
+        t.pad = 0;
+        t.arrival = g->d_arr.as<double>() + o;
+        t.batch = g->d_bat.as<int32_t>() + o;
+        t.cap = g->cap[i];
+        t.n_out = g->d_nq.as<int64_t>() + i;
+        t.overflow = g->d_tovf.as<int32_t>() + i;
+        msv::TailJob& l = lj[i];
+        l.samples = d.samples;
+        l.src = g->d_out.as<DevOut>() + i;
+        l.out = g->d_tails.as<double>() + 4 * i;
+    }
+    ctx->h2d += (int64_t)(n * (sizeof(DevScen) + sizeof(msv::TraceJob) + sizeof(msv::TailJob)) +
+                          parts_h.size() * sizeof(DevPart) + masks_h.size() * 8 + glat.size() * 16 +
+                          n_tails * sizeof(double));
+    if (n) {
+        MSV_CUDA_TRY(cudaMemcpy(g->d_scen.p, g->h_scen.data(), n * sizeof(DevScen), cudaMemcpyHostToDevice));
+        MSV_CUDA_TRY(cudaMemcpy(g->d_tjobs.p, tj.data(), n * sizeof(msv::TraceJob), cudaMemcpyHostToDevice));
+        MSV_CUDA_TRY(cudaMemcpy(g->d_tailjobs.p, lj.data(), n * sizeof(msv::TailJob), cudaMemcpyHostToDevice));
+        MSV_CUDA_TRY(cudaMemset(g->d_tovf.p, 0, n * 4));
+    }
+    // Work lists of every (wave, class).
+    std::vector<int32_t> work_h;
+    for (msv_grid::Wave& w : g->waves)
+        for (auto& c : w.classes) {
+            w.work_off.push_back((int64_t)work_h.size());
+            work_h.insert(work_h.end(), c.second.begin(), c.second.end());
+        }
+    MSV_CUDA_TRY(g->d_work.ensure(std::max<size_t>(work_h.size(), 1) * 4));
+    if (!work_h.empty())
+        MSV_CUDA_TRY(cudaMemcpy(g->d_work.p, work_h.data(), work_h.size() * 4, cudaMemcpyHostToDevice));
+    ctx->h2d += (int64_t)(work_h.size() * 4);
+    if (!g->generated) {
+        // Host traces stay resident: replay grids are a single wave.
+        if (g->waves.size() > 1) return fail(MSV_PARAM, "replay: traces exceed device memory budget");
+        g->host_n.resize(n);
+        for (int64_t i = 0; i < n; ++i) g->host_n[i] = g->cap[i];
+        const int64_t q0 = offsets[0];
+        const int64_t total = n ? offsets[n] - q0 : 0;
+        if (total) {
+            MSV_CUDA_TRY(cudaMemcpy(g->d_arr.p, arrival + q0, total * 8, cudaMemcpyHostToDevice));
+            MSV_CUDA_TRY(cudaMemcpy(g->d_bat.p, batch + q0, total * 4, cudaMemcpyHostToDevice));
+        }
+        if (n) MSV_CUDA_TRY(cudaMemcpy(g->d_nq.p, g->host_n.data(), n * 8, cudaMemcpyHostToDevice));
+    }
+    for (cudaEvent_t& e : g->ev) MSV_CUDA_TRY(cudaEventCreate(&e));
+    *out = g.release();
+    return MSV_OK;
+}
+
+int grid_launch(msv_grid* g) {
+    msv_ctx* ctx = g->ctx;
+    cudaStream_t st = ctx->stream;
+    float tr = 0, si = 0, ta = 0;
+    MSV_CUDA_TRY(cudaEventRecord(g->ev[0], st));
+    for (size_t wi = 0; wi < g->waves.size(); ++wi) {
+        const msv_grid::Wave& w = g->waves[wi];
+        const int64_t ns = w.s1 - w.s0;
+        cudaEvent_t e1 = g->ev[1], e2 = g->ev[2], e3 = g->ev[3];
+        if (g->generated) {
+            MSV_CUDA_TRY(msv::launch_trace_gen(g->d_tjobs.as<msv::TraceJob>() + w.s0, (int)ns, ctx->log1p, st));
+            ctx->launches += 1;
+        }
+        MSV_CUDA_TRY(cudaEventRecord(e1, st));
+        MSV_CUDA_TRY(cudaMemsetAsync(g->d_counter.p, 0, 64 * sizeof(int32_t), st));
+        for (size_t c = 0; c < w.classes.size(); ++c) {
+            const ClassKey& k = w.classes[c].first;
+            const int32_t nwork = (int32_t)w.classes[c].second.size();
+            msv::SimParams p;
+            p.scen = g->d_scen.as<DevScen>();
+            p.out = g->d_out.as<DevOut>();
+            p.usage = g->d_usage.as<msv_usage>();
+            p.work = g->d_work.as<int32_t>() + w.work_off[c];
+            p.n_work = nwork;
+            p.counter = g->d_counter.as<int32_t>() + (c % 64);
+            p.lat = g->d_glat.as<double>();
+            p.util = g->d_gutil.as<double>();
+            p.n_cells = g->n_cells;
+            p.pad = 0;
+            const int occ = msv::sim_max_blocks_per_sm(k.W, k.S, k.sched, g->records, g->n_cells);
+            if (occ <= 0) return fail(MSV_CUDA, "sim kernel: no occupancy for class");
+            const int segs_per_block = msv::kSimWarpsPerBlock * (32 / k.W);
+            const int need = (nwork + segs_per_block - 1) / segs_per_block;
+            const int blocks = std::max(1, std::min(need, occ * ctx->sms));
+            MSV_CUDA_TRY(msv::launch_sim(k.W, k.S, k.sched, g->records, p, blocks, st));
+            ctx->launches += 1;
+        }
+        MSV_CUDA_TRY(cudaEventRecord(e2, st));
+        if (!g->tail_p.empty()) {
+            MSV_CUDA_TRY(msv::launch_tail(g->d_tailjobs.as<msv::TailJob>() + w.s0, (int)ns, g->d_p.as<double>(),
+                                          (int)g->tail_p.size(), st));
+            ctx->launches += 1;
+        }
+        MSV_CUDA_TRY(cudaEventRecord(e3, st));
+        if (g->waves.size() > 1 || wi + 1 == g->waves.size()) {
+            // per-wave stage timing (events are reused, so accumulate after each wave)
+            if (g->waves.size() > 1) {
+                MSV_CUDA_TRY(cudaEventSynchronize(e3));
+                float a = 0, b = 0, c2 = 0;
+                cudaEventElapsedTime(&a, g->ev[0], e1);
+                cudaEventElapsedTime(&b, e1, e2);
+                cudaEventElapsedTime(&c2, e2, e3);
+                tr += a;
+                si += b;
+                ta += c2;
+                MSV_CUDA_TRY(cudaEventRecord(g->ev[0], st));
+            }
+        }
+    }
+    if (g->waves.size() > 1) {
+        g->t_trace = tr;
+        g->t_sim = si;
+        g->t_tail = ta;
+        g->t_total = tr + si + ta;
+    } else {
+        g->t_total = -1;  // resolved lazily in msv_grid_timing
+    }
+    return MSV_OK;
+}
+
+int grid_results(msv_grid* g, msv_result* res, msv_usage* usage, msv_record* records,
+                 std::vector<int64_t>* retry_trace) {
+    msv_ctx* ctx = g->ctx;
+    MSV_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    const int64_t n = g->n;
+    std::vector<DevOut> outs(n);
+    std::vector<double> tails(n * 4);
+    std::vector<int64_t> nq(n);
+    std::vector<int32_t> tovf(n);
+    if (n) {
+        MSV_CUDA_TRY(cudaMemcpy(outs.data(), g->d_out.p, n * sizeof(DevOut), cudaMemcpyDeviceToHost));
+        MSV_CUDA_TRY(cudaMemcpy(tails.data(), g->d_tails.p, n * 4 * sizeof(double), cudaMemcpyDeviceToHost));
+        MSV_CUDA_TRY(cudaMemcpy(nq.data(), g->d_nq.p, n * 8, cudaMemcpyDeviceToHost));
+        MSV_CUDA_TRY(cudaMemcpy(tovf.data(), g->d_tovf.p, n * 4, cudaMemcpyDeviceToHost));
+        ctx->d2h += n * (int64_t)(sizeof(DevOut) + 4 * sizeof(double) + 8 + 4);
+    }
+    if (usage && g->usage_total)
+        MSV_CUDA_TRY(cudaMemcpy(usage, g->d_usage.p, g->usage_total * sizeof(msv_usage), cudaMemcpyDeviceToHost));
+    if (records && g->records && g->waves.size() == 1 && g->max_wave_q)
+        MSV_CUDA_TRY(cudaMemcpy(records, g->d_rec.p, g->max_wave_q * sizeof(msv_record), cudaMemcpyDeviceToHost));
+    int first_err = MSV_OK;
+    int64_t first_i = -1;
+    for (int64_t i = 0; i < n; ++i) {
+        msv_result& r = res[i];
+        const DevOut& o = outs[i];
+        memset(&r, 0, sizeof r);
+        r.total = nq[i];
+        r.violations = o.violations;
+        r.measured = o.measured;
+        r.measured_violations = o.measured_violations;
+        for (int j = 0; j < 4; ++j)
+            r.tail[j] = j < (int)g->tail_p.size() ? tails[4 * i + j] : __builtin_nan("");
+        r.horizon_ms = o.horizon_ms;
+        r.warmup_ms = g->scen[i].warmup_fraction * g->scen[i].duration_ms;
+        r.max_wait_estimate_diff = o.max_wait_diff;
+        r.duration_ms = g->scen[i].duration_ms;
+        r.placement_hash = o.hash;
+        r.status = o.status;
+        r.n_partitions = g->P[i];
+        if (tovf[i]) {
+            r.status = msv::kStatusRetryTrace;
+            if (retry_trace) retry_trace->push_back(i);
+        }
+        if (r.status != MSV_OK && r.status < 100 && first_err == MSV_OK) {
+            first_err = r.status;
+            first_i = i;
+        }
+    }
+    if (first_err != MSV_OK)
+        return fail(first_err, "scenario " + std::to_string(first_i) + ": profile: batch outside the profile grid");
+    return MSV_OK;
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// C ABI
+// ---------------------------------------------------------------------------
+extern "C" {
+
+const char* msv_last_error(void) { return g_err.c_str(); }
+
+int msv_abi_version(void) { return MSV_ABI_VERSION; }
+
+int msv_create(int device, msv_ctx** out) {
+    if (!out) return fail(MSV_PARAM, "msv_create: null out");
+    *out = nullptr;
+    int count = 0;
+    cudaError_t e = cudaGetDeviceCount(&count);
+    if (e != cudaSuccess || count == 0)
+        return fail(MSV_CUDA, std::string("msv_create: no CUDA device: ") + cudaGetErrorString(e));
+    if (device < 0 || device >= count) return fail(MSV_PARAM, "msv_create: bad device ordinal");
+    SetDevice sd(device);
+    std::unique_ptr<msv_ctx> ctx(new msv_ctx);
+    ctx->device = device;
+    MSV_CUDA_TRY(cudaSetDevice(device));
+    MSV_CUDA_TRY(cudaDeviceGetAttribute(&ctx->sms, cudaDevAttrMultiProcessorCount, device));
+    int major = 0, minor = 0;
+    cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, device);
+    cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, device);
+    if (major != 10 || minor != 0)
+        return fail(MSV_CUDA, "msv_create: libmsv is built for sm_100a (B200); device is sm_" +
+                                  std::to_string(major) + std::to_string(minor));
+    MSV_CUDA_TRY(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+    ctx->log1p = probe_host_log1p();
+    *out = ctx.release();
+    return MSV_OK;
+}
+
+int msv_destroy(msv_ctx* ctx) {
+    if (!ctx) return MSV_OK;
+    SetDevice sd(ctx->device);
+    cudaStreamSynchronize(ctx->stream);
+    for (cudaEvent_t e : ctx->ev)
+        if (e) cudaEventDestroy(e);
+    cudaStreamDestroy(ctx->stream);
+    delete ctx;
+    return MSV_OK;
+}
+
+int msv_set_log1p_variant(msv_ctx* ctx, int variant) {
+    if (!ctx) return fail(MSV_PARAM, "null context");
+    if (variant == MSV_LOG1P_AUTO) variant = probe_host_log1p();
+    if (variant != MSV_LOG1P_GENERIC && variant != MSV_LOG1P_FMA)
+        return fail(MSV_PARAM, "msv_set_log1p_variant: unknown variant");
+    ctx->log1p = variant;
+    return MSV_OK;
+}
+
+int msv_get_log1p_variant(msv_ctx* ctx, int* variant) {
+    if (!ctx || !variant) return fail(MSV_PARAM, "null argument");
+    *variant = ctx->log1p;
+    return MSV_OK;
+}
+
+// ProfileTable::validate (profile.hpp:134-169).
+int msv_upload_profile(msv_ctx* ctx, int n_sizes, const int32_t* sizes, int b_max, const double* latency_ms,
+                       const double* utilization, int32_t* handle) {
+    if (!ctx || !handle) return fail(MSV_PARAM, "null argument");
+    if (n_sizes <= 0) return fail(MSV_PARAM, "profile: empty size set");
+    if (b_max < 1) return fail(MSV_PARAM, "profile: b_max must be >= 1");
+    Profile p;
+    p.sizes.assign(sizes, sizes + n_sizes);
+    p.b_max = b_max;
+    for (int i = 1; i < n_sizes; ++i)
+        if (!(p.sizes[i - 1] < p.sizes[i])) return fail(MSV_VALIDATION, "profile: sizes must be strictly ascending");
+    if (p.sizes.front() < 1) return fail(MSV_VALIDATION, "profile: partition sizes must be positive");
+    const size_t cells = (size_t)n_sizes * b_max;
+    p.lat.assign(latency_ms, latency_ms + cells);
+    p.util.assign(utilization, utilization + cells);
+    for (size_t i = 0; i < cells; ++i) {
+        if (!(p.lat[i] > 0.0)) return fail(MSV_VALIDATION, "profile: latency must be positive");
+        if (p.util[i] < 0.0 || p.util[i] > 1.0) return fail(MSV_VALIDATION, "profile: utilization outside [0,1]");
+    }
+    const double tol = 1e-9;
+    for (int i = 0; i < n_sizes; ++i)
+        for (int b = 2; b <= b_max; ++b) {
+            const size_t c = (size_t)i * b_max + (b - 1);
+            if (p.util[c] < p.util[c - 1] - tol)
+                return fail(MSV_VALIDATION, "profile: utilization must be nondecreasing in batch");
+            if (p.lat[c] < p.lat[c - 1] * (1.0 - tol))
+                return fail(MSV_VALIDATION, "profile: latency must be nondecreasing in batch");
+        }
+    for (int i = 1; i < n_sizes; ++i)
+        for (int b = 1; b <= b_max; ++b) {
+            const size_t c = (size_t)i * b_max + (b - 1);
+            if (p.lat[c] > p.lat[c - b_max] * (1.0 + tol))
+                return fail(MSV_VALIDATION, "profile: latency must be nonincreasing in partition size");
+        }
+    ctx->profiles.push_back(std::move(p));
+    ctx->tables_dirty = true;
+    *handle = (int32_t)ctx->profiles.size() - 1;
+    return MSV_OK;
+}
+
+// BatchDistribution(weights) (workload.hpp:25-38).
+int msv_upload_dist(msv_ctx* ctx, int b_max, const double* weights, int32_t* handle) {
+    if (!ctx || !handle) return fail(MSV_PARAM, "null argument");
+    if (b_max <= 0) return fail(MSV_PARAM, "batch distribution: empty support");
+    Dist d;
+    d.pmf.assign(weights, weights + b_max);
+    double total = 0.0;
+    for (double w : d.pmf) {
+        if (w < 0.0 || !std::isfinite(w)) return fail(MSV_PARAM, "batch distribution: weights must be finite and >= 0");
+        total += w;
+    }
+    if (!(total > 0.0)) return fail(MSV_PARAM, "batch distribution: all weights are zero");
+    for (double& w : d.pmf) w /= total;
+    d.cdf.resize(d.pmf.size());
+    double acc = 0.0;
+    for (size_t i = 0; i < d.pmf.size(); ++i) {
+        acc = (i == 0) ? d.pmf[0] : acc + d.pmf[i];  // std::partial_sum
+        d.cdf[i] = acc;
+    }
+    d.cdf.back() = 1.0;
+    ctx->dists.push_back(std::move(d));
+    ctx->tables_dirty = true;
+    *handle = (int32_t)ctx->dists.size() - 1;
+    return MSV_OK;
+}
+
+int msv_upload_cdf(msv_ctx* ctx, int b_max, const double* cdf, int32_t* handle) {
+    if (!ctx || !handle || !cdf) return fail(MSV_PARAM, "null argument");
+    if (b_max <= 0) return fail(MSV_PARAM, "batch distribution: empty support");
+    Dist d;
+    d.cdf.assign(cdf, cdf + b_max);
+    for (int i = 0; i < b_max; ++i) {
+        if (!(d.cdf[i] >= 0.0) || d.cdf[i] > 1.0 || (i && d.cdf[i] < d.cdf[i - 1]))
+            return fail(MSV_PARAM, "batch distribution: cdf must be nondecreasing in [0,1]");
+    }
+    if (d.cdf.back() != 1.0) return fail(MSV_PARAM, "batch distribution: cdf must end at 1.0");
+    d.pmf.resize(b_max);
+    for (int i = 0; i < b_max; ++i) d.pmf[i] = i ? d.cdf[i] - d.cdf[i - 1] : d.cdf[0];
+    ctx->dists.push_back(std::move(d));
+    ctx->tables_dirty = true;
+    *handle = (int32_t)ctx->dists.size() - 1;
+    return MSV_OK;
+}
+
+// PartitionPlan + validate() (paris.hpp:133-156); validation errors surface at run.
+int msv_upload_plan(msv_ctx* ctx, int num_gpus, int gpcs_per_gpu, const int32_t* n_per_gpu,
+                    const int32_t* sizes_flat, int32_t* handle) {
+    if (!ctx || !handle) return fail(MSV_PARAM, "null argument");
+    Plan p;
+    p.num_gpus = num_gpus;
+    p.gpcs_per_gpu = gpcs_per_gpu;
+    if (num_gpus < 1) {
+        p.err = MSV_VALIDATION;
+        p.err_msg = "plan: num_gpus must be >= 1";
+    } else if (gpcs_per_gpu < 1) {
+        p.err = MSV_VALIDATION;
+        p.err_msg = "plan: gpcs_per_gpu must be >= 1";
+    }
+    size_t off = 0;
+    for (int g = 0; g < std::max(num_gpus, 0); ++g) {
+        int used = 0;
+        for (int j = 0; j < n_per_gpu[g]; ++j) {
+            const int32_t k = sizes_flat[off + j];
+            if (k < 1 && !p.err) {
+                p.err = MSV_VALIDATION;
+                p.err_msg = "plan: partition size must be positive";
+            }
+            used += k;
+            p.flat.push_back(k);
+        }
+        off += n_per_gpu[g];
+        if (used > gpcs_per_gpu && !p.err) {
+            p.err = MSV_VALIDATION;
+            p.err_msg = "plan: GPU over capacity (" + std::to_string(used) + " > " + std::to_string(gpcs_per_gpu) + ")";
+        }
+    }
+    ctx->plans.push_back(std::move(p));
+    *handle = (int32_t)ctx->plans.size() - 1;
+    return MSV_OK;
+}
+
+int msv_upload_routing(msv_ctx* ctx, int n_segments, const int32_t* k, const int32_t* first,
+                       const int32_t* last, int32_t* handle) {
+    if (!ctx || !handle) return fail(MSV_PARAM, "null argument");
+    if (n_segments < 0) return fail(MSV_PARAM, "routing: negative segment count");
+    Routing r;
+    r.k.assign(k, k + n_segments);
+    r.first.assign(first, first + n_segments);
+    r.last.assign(last, last + n_segments);
+    ctx->routings.push_back(std::move(r));
+    *handle = (int32_t)ctx->routings.size() - 1;
+    return MSV_OK;
+}
+
+int msv_grid_create(msv_ctx* ctx, const msv_scenario* scenarios, int64_t n, const double* tail_p, int n_tails,
+                    msv_grid** out) {
+    if (!ctx || !out || (n > 0 && !scenarios)) return fail(MSV_PARAM, "null argument");
+    SetDevice sd(ctx->device);
+    return grid_build(ctx, scenarios, n, tail_p, n_tails, nullptr, nullptr, nullptr, false, out);
+}
+
+int msv_grid_launch(msv_grid* grid) {
+    if (!grid) return fail(MSV_PARAM, "null grid");
+    SetDevice sd(grid->ctx->device);
+    return grid_launch(grid);
+}
+
+int msv_grid_results(msv_grid* grid, msv_result* results, msv_usage* usage) {
+    if (!grid || (grid->n > 0 && !results)) return fail(MSV_PARAM, "null argument");
+    SetDevice sd(grid->ctx->device);
+    return grid_results(grid, results, usage, nullptr, nullptr);
+}
+
+int msv_grid_destroy(msv_grid* grid) {
+    if (!grid) return MSV_OK;
+    SetDevice sd(grid->ctx->device);
+    cudaStreamSynchronize(grid->ctx->stream);
+    delete grid;
+    return MSV_OK;
+}
+
+int msv_grid_timing(msv_grid* g, float* total_ms, float* trace_ms, float* sim_ms, float* tail_ms) {
+    if (!g) return fail(MSV_PARAM, "null grid");
+    SetDevice sd(g->ctx->device);
+    if (g->t_total < 0) {
+        MSV_CUDA_TRY(cudaEventSynchronize(g->ev[3]));
+        cudaEventElapsedTime(&g->t_trace, g->ev[0], g->ev[1]);
+        cudaEventElapsedTime(&g->t_sim, g->ev[1], g->ev[2]);
+        cudaEventElapsedTime(&g->t_tail, g->ev[2], g->ev[3]);
+        cudaEventElapsedTime(&g->t_total, g->ev[0], g->ev[3]);
+    }
+    if (total_ms) *total_ms = g->t_total;
+    if (trace_ms) *trace_ms = g->t_trace;
+    if (sim_ms) *sim_ms = g->t_sim;
+    if (tail_ms) *tail_ms = g->t_tail;
+    return MSV_OK;
+}
+
+int64_t msv_grid_queries(msv_grid* g) {
+    if (!g) return -1;
+    SetDevice sd(g->ctx->device);
+    if (cudaStreamSynchronize(g->ctx->stream) != cudaSuccess) return -1;
+    std::vector<int64_t> nq(g->n);
+    if (g->n && cudaMemcpy(nq.data(), g->d_nq.p, g->n * 8, cudaMemcpyDeviceToHost) != cudaSuccess) return -1;
+    int64_t s = 0;
+    for (int64_t v : nq) s += v;
+    return s;
+}
+
+int msv_synchronize(msv_ctx* ctx) {
+    if (!ctx) return fail(MSV_PARAM, "null context");
+    SetDevice sd(ctx->device);
+    MSV_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    return MSV_OK;
+}
+
+int64_t msv_kernel_launches(msv_ctx* ctx) { return ctx ? ctx->launches : -1; }
+
+int msv_event_record(msv_ctx* ctx, int slot) {
+    if (!ctx || slot < 0 || slot >= 8) return fail(MSV_PARAM, "msv_event_record: bad slot");
+    SetDevice sd(ctx->device);
+    if (!ctx->ev[slot]) MSV_CUDA_TRY(cudaEventCreate(&ctx->ev[slot]));
+    MSV_CUDA_TRY(cudaEventRecord(ctx->ev[slot], ctx->stream));
+    return MSV_OK;
+}
+
+int msv_event_elapsed(msv_ctx* ctx, int a, int b, float* ms) {
+    if (!ctx || !ms || a < 0 || a >= 8 || b < 0 || b >= 8 || !ctx->ev[a] || !ctx->ev[b])
+        return fail(MSV_PARAM, "msv_event_elapsed: bad slot");
+    SetDevice sd(ctx->device);
+    MSV_CUDA_TRY(cudaEventSynchronize(ctx->ev[b]));
+    MSV_CUDA_TRY(cudaEventElapsedTime(ms, ctx->ev[a], ctx->ev[b]));
+    return MSV_OK;
+}
+
+int msv_transfer_bytes(msv_ctx* ctx, int64_t* h2d, int64_t* d2h) {
+    if (!ctx) return fail(MSV_PARAM, "null context");
+    if (h2d) *h2d = ctx->h2d;
+    if (d2h) *d2h = ctx->d2h;
+    return MSV_OK;
+}
+
+int msv_run_grid(msv_ctx* ctx, const msv_scenario* scenarios, int64_t n, const double* tail_p, int n_tails,
+                 msv_result* results, msv_usage* usage) {
+    if (!ctx || (n > 0 && (!scenarios || !results))) return fail(MSV_PARAM, "null argument");
+    SetDevice sd(ctx->device);
+    msv_grid* g = nullptr;
+    int rc = grid_build(ctx, scenarios, n, tail_p, n_tails, nullptr, nullptr, nullptr, false, &g);
+    if (rc) return rc;
+    std::unique_ptr<msv_grid> guard(g);
+    rc = grid_launch(g);
+    if (rc) return rc;
+    std::vector<int64_t> retry;
+    rc = grid_results(g, results, usage, nullptr, &retry);
+    if (rc) return rc;
+    // Traces longer than the Poisson-tail capacity (a >10-sigma Poisson count):
+    // rerun those scenarios alone with the capacity quadrupled until they fit.
+    std::vector<int64_t> caps_prev;
+    for (int64_t i : retry) caps_prev.push_back(g->cap[i]);
+    for (int attempt = 0; !retry.empty(); ++attempt) {
+        if (attempt >= 6) return fail(MSV_PARAM, "sample_trace: trace exceeded its capacity repeatedly");
+        std::vector<msv_scenario> sub;
+        std::vector<int64_t> caps;
+        int64_t usage_n = 0;
+        for (size_t j = 0; j < retry.size(); ++j) {
+            sub.push_back(scenarios[retry[j]]);
+            caps.push_back(caps_prev[j] * 4);
+        }
+        msv_grid* g2 = nullptr;
+        rc = grid_build(ctx, sub.data(), (int64_t)sub.size(), tail_p, n_tails, nullptr, nullptr, nullptr, false, &g2,
+                        caps.data());
+        if (rc) return rc;
+        std::unique_ptr<msv_grid> guard2(g2);
+        rc = grid_launch(g2);
+        if (rc) return rc;
+        usage_n = g2->usage_total;
+        std::vector<msv_result> sub_res(sub.size());
+        std::vector<msv_usage> sub_use(std::max<int64_t>(usage_n, 1));
+        std::vector<int64_t> again;
+        rc = grid_results(g2, sub_res.data(), sub_use.data(), nullptr, &again);
+        if (rc) return rc;
+        std::vector<int64_t> next_retry, next_caps;
+        size_t again_pos = 0;
+        for (size_t j = 0; j < sub.size(); ++j) {
+            const int64_t i = retry[j];
+            if (again_pos < again.size() && again[again_pos] == (int64_t)j) {
+                ++again_pos;
+                next_retry.push_back(i);
+                next_caps.push_back(caps[j]);
+                continue;
+            }
+            results[i] = sub_res[j];
+            if (usage)
+                for (int32_t q = 0; q < g2->P[j]; ++q) usage[g->usage_off[i] + q] = sub_use[g2->usage_off[j] + q];
+        }
+        retry.swap(next_retry);
+        caps_prev.swap(next_caps);
+    }
+    return MSV_OK;
+}
+
+int msv_run_replay(msv_ctx* ctx, const msv_scenario* scenarios, int64_t n, const int64_t* offsets,
+                   const double* arrival_ms, const int32_t* batch, const double* tail_p, int n_tails,
+                   msv_result* results, msv_usage* usage, msv_record* records) {
+    if (!ctx || (n > 0 && (!scenarios || !results || !offsets))) return fail(MSV_PARAM, "null argument");
+    SetDevice sd(ctx->device);
+    msv_grid* g = nullptr;
+    int rc = grid_build(ctx, scenarios, n, tail_p, n_tails, offsets, arrival_ms, batch, records != nullptr, &g);
+    if (rc) return rc;
+    std::unique_ptr<msv_grid> guard(g);
+    rc = grid_launch(g);
+    if (rc) return rc;
+    return grid_results(g, results, usage, records, nullptr);
+}
+
+int msv_sample_trace(msv_ctx* ctx, int32_t dist, double rate_qps, double duration_ms, uint64_t seed, int64_t cap,
+                     double* arrival_ms, int32_t* batch, int64_t* n_out) {
+    if (!ctx || !n_out) return fail(MSV_PARAM, "null argument");
+    if (!(rate_qps > 0.0)) return fail(MSV_PARAM, "sample_trace: rate must be > 0");
+    if (duration_ms < 0.0) return fail(MSV_PARAM, "sample_trace: duration must be >= 0");
+    if (dist < 0 || dist >= (int)ctx->dists.size()) return fail(MSV_PARAM, "sample_trace: unknown dist handle");
+    if (cap < 0) return fail(MSV_PARAM, "sample_trace: negative capacity");
+    SetDevice sd(ctx->device);
+    int rc = ctx->sync_tables();
+    if (rc) return rc;
+    DevBuf d_arr, d_bat, d_job, d_n, d_ovf;
+    const int64_t c = std::max<int64_t>(cap, 1);
+    MSV_CUDA_TRY(d_arr.ensure(c * 8));
+    MSV_CUDA_TRY(d_bat.ensure(c * 4));
+    MSV_CUDA_TRY(d_job.ensure(sizeof(msv::TraceJob)));
+    MSV_CUDA_TRY(d_n.ensure(8));
+    MSV_CUDA_TRY(d_ovf.ensure(4));
+    msv::TraceJob j;
+    j.seed = seed;
+    j.rate_per_ms = rate_qps / 1000.0;
+    j.duration_ms = duration_ms;
+    j.cdf = ctx->d_cdf.as<double>() + ctx->dists[dist].dev_off;
+    j.b_max = (int32_t)ctx->dists[dist].cdf.size();
+    j.pad = 0;
+    j.arrival = d_arr.as<double>();
+    j.batch = d_bat.as<int32_t>();
+    j.cap = cap;
+    j.n_out = d_n.as<int64_t>();
+    j.overflow = d_ovf.as<int32_t>();
+    MSV_CUDA_TRY(cudaMemcpyAsync(d_job.p, &j, sizeof j, cudaMemcpyHostToDevice, ctx->stream));
+    MSV_CUDA_TRY(msv::launch_trace_gen(d_job.as<msv::TraceJob>(), 1, ctx->log1p, ctx->stream));
+    ctx->launches += 1;
+    int64_t nn = 0;
+    int32_t ovf = 0;
+    MSV_CUDA_TRY(cudaMemcpyAsync(&nn, d_n.p, 8, cudaMemcpyDeviceToHost, ctx->stream));
+    MSV_CUDA_TRY(cudaMemcpyAsync(&ovf, d_ovf.p, 4, cudaMemcpyDeviceToHost, ctx->stream));
+    MSV_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    if (ovf) {
+        *n_out = cap + 1;
+        return fail(MSV_PARAM, "sample_trace: capacity " + std::to_string(cap) + " too small");
+    }
+    *n_out = nn;
+    if (nn) {
+        MSV_CUDA_TRY(cudaMemcpy(arrival_ms, d_arr.p, nn * 8, cudaMemcpyDeviceToHost));
+        MSV_CUDA_TRY(cudaMemcpy(batch, d_bat.p, nn * 4, cudaMemcpyDeviceToHost));
+    }
+    return MSV_OK;
+}
+
+// tail_latency(samples, p) (metrics.hpp:22-29) on the device.
+int msv_tail_latency(msv_ctx* ctx, const double* samples, int64_t n, const double* p, int n_p, double* out) {
+    if (!ctx || !out || (n > 0 && !samples)) return fail(MSV_PARAM, "null argument");
+    if (n <= 0) return fail(MSV_PARAM, "tail_latency: no samples");
+    if (n_p < 1 || n_p > 4) return fail(MSV_PARAM, "tail_latency: between 1 and 4 percentiles");
+    for (int j = 0; j < n_p; ++j)
+        if (!(p[j] > 0.0) || !(p[j] < 1.0)) return fail(MSV_PARAM, "tail_latency: percentile must be in (0,1)");
+    SetDevice sd(ctx->device);
+    DevBuf d_s, d_out, d_job, d_p, d_res;
+    MSV_CUDA_TRY(d_s.ensure(n * 8));
+    MSV_CUDA_TRY(d_out.ensure(sizeof(DevOut)));
+    MSV_CUDA_TRY(d_job.ensure(sizeof(msv::TailJob)));
+    MSV_CUDA_TRY(d_p.ensure(n_p * 8));
+    MSV_CUDA_TRY(d_res.ensure(4 * 8));
+    const double* src = samples;
+    DevOut o;
+    memset(&o, 0, sizeof o);
+    o.n_samples = n;
+    o.lat_min_bits = ~0ull;  // min > max: the kernel derives the key range itself
+    o.lat_max_bits = 0;
+    msv::TailJob j;
+    j.samples = d_s.as<double>();
+    j.src = d_out.as<DevOut>();
+    j.out = d_res.as<double>();
+    MSV_CUDA_TRY(cudaMemcpyAsync(d_s.p, src, n * 8, cudaMemcpyHostToDevice, ctx->stream));
+    MSV_CUDA_TRY(cudaMemcpyAsync(d_out.p, &o, sizeof o, cudaMemcpyHostToDevice, ctx->stream));
+    MSV_CUDA_TRY(cudaMemcpyAsync(d_job.p, &j, sizeof j, cudaMemcpyHostToDevice, ctx->stream));
+    MSV_CUDA_TRY(cudaMemcpyAsync(d_p.p, p, n_p * 8, cudaMemcpyHostToDevice, ctx->stream));
+    MSV_CUDA_TRY(msv::launch_tail(d_job.as<msv::TailJob>(), 1, d_p.as<double>(), n_p, ctx->stream));
+    ctx->launches += 1;
+    MSV_CUDA_TRY(cudaMemcpyAsync(out, d_res.p, n_p * 8, cudaMemcpyDeviceToHost, ctx->stream));
+    MSV_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    return MSV_OK;
+}
+
+int msv_dispatch_batch(msv_ctx* ctx, int32_t profile, int scheduler, int64_t n_trials, const int64_t* part_off,
+                       const int32_t* part_id, const int32_t* part_k, const uint8_t* busy, const double* cur_est,
+                       const double* cur_start, const int64_t* q_off, const int32_t* qbatch,
+                       const int32_t* query_batch, const double* now_ms, const double* sla_ms, const double* alpha,
+                       const double* beta, int32_t* chosen, int32_t* kind, double* t_wait_out) {
+    if (!ctx || !part_off || !chosen || !kind) return fail(MSV_PARAM, "null argument");
+    // fifs_dispatch takes no table (sched.hpp:154): profile -1 is allowed for FIFS
+    // decisions that do not request t_wait.
+    const bool no_table = profile == -1 && scheduler == MSV_FIFS && !t_wait_out;
+    if (!no_table && (profile < 0 || profile >= (int)ctx->profiles.size()))
+        return fail(MSV_PARAM, "unknown profile handle");
+    if (scheduler != MSV_FIFS && scheduler != MSV_ELSA) return fail(MSV_VALIDATION, "unknown scheduler");
+    if (n_trials <= 0) return MSV_OK;
+    SetDevice sd(ctx->device);
+    int rc = ctx->sync_tables();
+    if (rc) return rc;
+    static const Profile kEmpty;
+    const Profile& prof = no_table ? kEmpty : ctx->profiles[profile];
+    const int64_t np = part_off[n_trials] - part_off[0];
+    const int64_t nqb = np ? q_off[part_off[n_trials]] - q_off[part_off[0]] : 0;
+    if (part_off[0] != 0 || (np && q_off[0] != 0))
+        return fail(MSV_PARAM, "dispatch: offsets must start at 0");
+    for (int64_t t = 0; t < n_trials; ++t) {
+        if (part_off[t + 1] <= part_off[t]) return fail(MSV_PARAM, "elsa_dispatch: no partitions");
+        if (part_off[t + 1] - part_off[t] > 128) return fail(MSV_PARAM, "dispatch: at most 128 partitions per trial");
+    }
+    std::vector<int32_t> rows(np);
+    for (int64_t j = 0; j < np; ++j) {
+        auto it = std::lower_bound(prof.sizes.begin(), prof.sizes.end(), part_k[j]);
+        rows[j] = (it == prof.sizes.end() || *it != part_k[j])
+                      ? -1
+                      : prof.cell_off + (int32_t)(it - prof.sizes.begin()) * prof.b_max;
+    }
+    DevBuf b_poff, b_pid, b_pk, b_row, b_busy, b_est, b_start, b_qoff, b_qb, b_qbat, b_now, b_sla, b_al, b_be,
+        b_ch, b_kind, b_tw, b_err;
+    auto up = [&](DevBuf& b, const void* src, size_t bytes) -> int {
+        MSV_CUDA_TRY(b.ensure(bytes ? bytes : 16));
+        if (bytes) MSV_CUDA_TRY(cudaMemcpyAsync(b.p, src, bytes, cudaMemcpyHostToDevice, ctx->stream));
+        return MSV_OK;
+    };
+    if ((rc = up(b_poff, part_off, (n_trials + 1) * 8)) || (rc = up(b_pid, part_id, np * 4)) ||
+        (rc = up(b_pk, part_k, np * 4)) || (rc = up(b_row, rows.data(), np * 4)) || (rc = up(b_busy, busy, np)) ||
+        (rc = up(b_est, cur_est, np * 8)) || (rc = up(b_start, cur_start, np * 8)) ||
+        (rc = up(b_qoff, q_off, (np + 1) * 8)) || (rc = up(b_qb, qbatch, nqb * 4)) ||
+        (rc = up(b_qbat, query_batch, n_trials * 4)) || (rc = up(b_now, now_ms, n_trials * 8)) ||
+        (rc = up(b_sla, sla_ms, n_trials * 8)) || (rc = up(b_al, alpha, n_trials * 8)) ||
+        (rc = up(b_be, beta, n_trials * 8)))
+        return rc;
+    MSV_CUDA_TRY(b_ch.ensure(n_trials * 4));
+    MSV_CUDA_TRY(b_kind.ensure(n_trials * 4));
+    MSV_CUDA_TRY(b_err.ensure(n_trials * 4));
+    if (t_wait_out) MSV_CUDA_TRY(b_tw.ensure(np * 8));
+    msv::DispatchParams p;
+    p.n_trials = n_trials;
+    p.part_off = b_poff.as<int64_t>();
+    p.part_id = b_pid.as<int32_t>();
+    p.part_k = b_pk.as<int32_t>();
+    p.part_row = b_row.as<int32_t>();
+    p.busy = b_busy.as<uint8_t>();
+    p.cur_est = b_est.as<double>();
+    p.cur_start = b_start.as<double>();
+    p.q_off = b_qoff.as<int64_t>();
+    p.qbatch = b_qb.as<int32_t>();
+    p.query_batch = b_qbat.as<int32_t>();
+    p.now_ms = b_now.as<double>();
+    p.sla_ms = b_sla.as<double>();
+    p.alpha = b_al.as<double>();
+    p.beta = b_be.as<double>();
+    p.lat = ctx->d_lat.as<double>();
+    p.b_max = prof.b_max;
+    p.scheduler = scheduler;
+    p.chosen = b_ch.as<int32_t>();
+    p.kind = b_kind.as<int32_t>();
+    p.t_wait_out = t_wait_out ? b_tw.as<double>() : nullptr;
+    p.error = b_err.as<int32_t>();
+    MSV_CUDA_TRY(msv::launch_dispatch(p, ctx->stream));
+    ctx->launches += 1;
+    std::vector<int32_t> err(n_trials);
+    MSV_CUDA_TRY(cudaMemcpyAsync(chosen, b_ch.p, n_trials * 4, cudaMemcpyDeviceToHost, ctx->stream));
+    MSV_CUDA_TRY(cudaMemcpyAsync(kind, b_kind.p, n_trials * 4, cudaMemcpyDeviceToHost, ctx->stream));
+    MSV_CUDA_TRY(cudaMemcpyAsync(err.data(), b_err.p, n_trials * 4, cudaMemcpyDeviceToHost, ctx->stream));
+    if (t_wait_out) MSV_CUDA_TRY(cudaMemcpyAsync(t_wait_out, b_tw.p, np * 8, cudaMemcpyDeviceToHost, ctx->stream));
+    MSV_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    for (int64_t t = 0; t < n_trials; ++t)
+        if (err[t]) return fail(err[t], "trial " + std::to_string(t) + ": profile lookup outside the grid");
+    return MSV_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,144 @@
+// Internal structures shared by the CUDA kernels (msv_kernels.cu) and the host
+// runtime (msv_host.cpp). Not part of the public ABI (include/msv.h).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/msv.h"
+
+namespace msv {
+
+// Shared-memory ring capacity of each partition's FIFO (entries). Deeper queues
+// continue as a singly linked list threaded through the scenario's query ids
+// (DevScen::next), so queue depth is bounded only by the trace length.
+constexpr int kQCap = 8;
+// Profile cells (latency + utilisation, all uploaded profiles) staged in shared
+// memory by the simulation kernel.
+constexpr int kMaxSmemCells = 1024;
+constexpr int kSimWarpsPerBlock = 8;
+constexpr int kTraceWarpsPerBlock = 4;
+constexpr int kTailThreads = 256;
+constexpr int kTailSmemCap = 2048;  // values gathered for the final in-smem select
+// Internal status: generated trace exceeded its capacity, host re-runs with a larger one.
+constexpr int kStatusRetryTrace = 101;
+
+// One partition as the simulation sees it, in by_ascending_size order
+// (sched.hpp:96-104): the warp lane of order index o = s*W + lane.
+struct DevPart {
+    int32_t pid;   // partition id = index in plan.flatten() (paris.hpp:134-139)
+    int32_t k;     // partition size in GPCs
+    int32_t row;   // offset of latency(k, 1) in the concatenated profile cells
+    int32_t pad;
+};
+
+// Per-scenario inputs of the simulation kernel.
+struct DevScen {
+    const double* arrival;      // trace arrivals (device)
+    const int32_t* batch;       // trace batches (device)
+    const int64_t* n;           // queries in the trace (written by K1 or the host)
+    double duration_ms;
+    double warmup_ms;
+    double sla, alpha, beta;
+    const DevPart* parts;       // P entries in (k, id) ascending order
+    const uint64_t* route_mask; // P masks (bit b-1: segment of k covers batch b) or null
+    uint32_t* next;             // per-query link of the overflow queues (capacity n)
+    double* samples;            // measured latencies out (capacity n)
+    msv_record* records;        // per-query records out, or null
+    int32_t P;
+    int32_t b_max;              // profile b_max
+    int32_t sched;
+    int32_t flags;
+    int32_t usage_off;          // first msv_usage slot of this scenario (or -1)
+    int32_t pad;
+};
+
+// Per-scenario outputs of the simulation kernel (input of the tail kernel).
+struct DevOut {
+    int64_t violations;
+    int64_t measured;
+    int64_t measured_violations;
+    int64_t n_samples;
+    double horizon_ms;
+    double max_wait_diff;
+    uint64_t hash;
+    uint64_t lat_min_bits;
+    uint64_t lat_max_bits;
+    int32_t status;
+    int32_t pad;
+};
+
+struct SimParams {
+    const DevScen* scen;
+    DevOut* out;
+    msv_usage* usage;
+    const int32_t* work;  // scenario indices of this class, longest first
+    int32_t n_work;
+    int32_t* counter;     // work-stealing counter (device)
+    const double* lat;    // all profile latency cells
+    const double* util;   // all profile utilisation cells
+    int32_t n_cells;
+    int32_t pad;
+};
+
+// Trace generation job (sample_trace, workload.hpp:97-113).
+struct TraceJob {
+    uint64_t seed;
+    double rate_per_ms;   // rate_qps / 1000.0 (workload.hpp:103)
+    double duration_ms;
+    const double* cdf;    // BatchDistribution cdf (device)
+    int32_t b_max;
+    int32_t pad;
+    double* arrival;      // out
+    int32_t* batch;       // out
+    int64_t cap;
+    int64_t* n_out;       // out: queries generated (min(n, cap))
+    int32_t* overflow;    // out: 1 when the trace did not fit in cap
+};
+
+struct TailJob {
+    const double* samples;
+    const DevOut* src;  // n_samples / lat_min_bits / lat_max_bits of the scenario
+    double* out;        // n_p tails
+};
+
+// Single-decision dispatch trials (msv_dispatch_batch).
+struct DispatchParams {
+    int64_t n_trials;
+    const int64_t* part_off;
+    const int32_t* part_id;
+    const int32_t* part_k;
+    const int32_t* part_row;
+    const uint8_t* busy;
+    const double* cur_est;
+    const double* cur_start;
+    const int64_t* q_off;
+    const int32_t* qbatch;
+    const int32_t* query_batch;
+    const double* now_ms;
+    const double* sla_ms;
+    const double* alpha;
+    const double* beta;
+    const double* lat;
+    int32_t b_max;        // shared profile's b_max
+    int32_t scheduler;
+    int32_t* chosen;
+    int32_t* kind;
+    double* t_wait_out;
+    int32_t* error;  // LookupError flag per trial
+};
+
+// Kernel launchers (msv_kernels.cu). Return cudaGetLastError().
+cudaError_t launch_trace_gen(const TraceJob* d_jobs, int n_jobs, int log1p_variant,
+                             cudaStream_t stream);
+// Persistent simulation kernel for P <= W*S (W lanes per scenario, S slots per lane).
+// sched is the scenario class's scheduler (all scenarios of one launch share it).
+cudaError_t launch_sim(int W, int S, int sched, bool records, const SimParams& p, int blocks,
+                       cudaStream_t stream);
+size_t sim_smem_bytes(int S, int n_cells);
+int sim_max_blocks_per_sm(int W, int S, int sched, bool records, int n_cells);
+cudaError_t launch_tail(const TailJob* d_jobs, int n_jobs, const double* d_p, int n_p,
+                        cudaStream_t stream);
+cudaError_t launch_dispatch(const DispatchParams& p, cudaStream_t stream);
+
+}  // namespace msv

@@ -1,0 +1,531 @@
+"""Python face of the engine: the reference's data types (ProfileTable,
+BatchDistribution, PartitionPlan, SlaConfig) as light holders, and `Engine`, one
+device context (include/msv.h) with the hot-path calls:
+
+    Engine.run_grid      sample_trace -> run -> tail_latency per scenario (device)
+    Engine.run           run() on host traces, per-query records   (engine.hpp:115)
+    Engine.sample_trace  sample_trace on the device                (workload.hpp:97)
+    Engine.tail_latency  nearest-rank tail on the device           (metrics.hpp:22)
+    Engine.dispatch      elsa_dispatch / fifs_dispatch / t_wait    (sched.hpp:77-174)
+    Engine.grid          device-resident grid for timing loops
+
+Host-side constructors (synth_profile, lognormal_batch_pdf, paris_plan) call the C++
+host headers through libmsv.so, so Python and C++ users get the same bits.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+from typing import Iterable, Sequence
+
+import numpy as np
+
+from . import _native as N
+from ._native import check
+
+
+def _arr(a, dtype):
+    return np.ascontiguousarray(np.asarray(a, dtype=dtype))
+
+
+def _ptr(a: np.ndarray, ctype):
+    return a.ctypes.data_as(C.POINTER(ctype))
+
+
+# ---------------------------------------------------------------------------
+# reference data types
+# ---------------------------------------------------------------------------
+@dataclass
+class SyntheticProfileParams:
+    """profile.hpp:43-48 (defaults identical)."""
+    work_per_sample: float = 10.0
+    fixed_overhead: float = 5.0
+    parallelism_per_sample: float = 0.15
+    util_cap: float = 0.95
+
+
+@dataclass
+class ProfileTable:
+    """Dense [size_idx][batch-1] latency / utilisation grid (profile.hpp:52-132)."""
+    sizes: np.ndarray
+    b_max: int
+    latency: np.ndarray      # (n_sizes, b_max) float64
+    utilization: np.ndarray  # (n_sizes, b_max) float64
+    model: str = "synthetic"
+
+    def _cell(self, k: int, batch: int) -> tuple[int, int]:
+        idx = int(np.searchsorted(self.sizes, k))
+        if idx >= len(self.sizes) or int(self.sizes[idx]) != k:
+            raise N.LookupError_(f"profile: unknown partition size k={k}")
+        if batch < 1 or batch > self.b_max:
+            raise N.LookupError_(f"profile: batch {batch} outside grid 1..{self.b_max}")
+        return idx, batch - 1
+
+    def latency_ms(self, k: int, batch: int) -> float:
+        return float(self.latency[self._cell(k, batch)])
+
+    def util(self, k: int, batch: int) -> float:
+        return float(self.utilization[self._cell(k, batch)])
+
+    def max_size(self) -> int:
+        return int(self.sizes[-1])
+
+
+def synth_profile(params: SyntheticProfileParams, sizes: Sequence[int], b_max: int, model: str = "synthetic"
+                  ) -> ProfileTable:
+    """synth_profile (profile.hpp:183-215), computed by the C++ host header."""
+    s = _arr(sizes, np.int32)
+    out_sizes = np.zeros(max(len(s), 1), np.int32)
+    lat = np.zeros(max(len(s), 1) * max(b_max, 1), np.float64)
+    util = np.zeros_like(lat)
+    n = C.c_int32(0)
+    check(N.lib().msv_synth_profile(params.work_per_sample, params.fixed_overhead, params.parallelism_per_sample,
+                                    params.util_cap, len(s), _ptr(s, C.c_int32), b_max, C.byref(n),
+                                    _ptr(out_sizes, C.c_int32), _ptr(lat, C.c_double), _ptr(util, C.c_double)),
+          "synth_profile")
+    k = n.value
+    return ProfileTable(out_sizes[:k].copy(), b_max, lat[:k * b_max].reshape(k, b_max).copy(),
+                        util[:k * b_max].reshape(k, b_max).copy(), model)
+
+
+@dataclass
+class BatchDistribution:
+    """BatchDistribution(weights) (workload.hpp:22-53); `weights` are kept raw so the
+    device rebuilds pmf/cdf with the reference's exact arithmetic."""
+    weights: np.ndarray
+
+    @property
+    def b_max(self) -> int:
+        return len(self.weights)
+
+    def tables(self) -> tuple[np.ndarray, np.ndarray]:
+        w = [float(x) for x in self.weights]
+        total = 0.0
+        for x in w:
+            total += x
+        pmf = np.array([x / total for x in w])
+        cdf = np.empty_like(pmf)
+        acc = 0.0
+        for i, p in enumerate(pmf):
+            acc = p if i == 0 else acc + p
+            cdf[i] = acc
+        cdf[-1] = 1.0
+        return pmf, cdf
+
+
+def lognormal_batch_pdf(mu: float, sigma: float, b_max: int) -> BatchDistribution:
+    """lognormal_batch_pdf (workload.hpp:81-93); returned as its exact normalised pmf."""
+    pmf = np.zeros(max(b_max, 1))
+    cdf = np.zeros_like(pmf)
+    check(N.lib().msv_lognormal_pdf(mu, sigma, b_max, _ptr(pmf, C.c_double), _ptr(cdf, C.c_double)),
+          "lognormal_batch_pdf")
+    return BatchDistribution(pmf)
+
+
+@dataclass
+class PartitionPlan:
+    """PartitionPlan (paris.hpp:133-156): sizes per GPU; ids = GPU-major order."""
+    num_gpus: int
+    gpcs_per_gpu: int
+    gpus: list[list[int]]
+
+    def flatten(self) -> list[int]:
+        return [k for g in self.gpus for k in g]
+
+    def total_instances(self) -> int:
+        return sum(len(g) for g in self.gpus)
+
+    def instance_counts(self) -> list[tuple[int, int]]:
+        c: dict[int, int] = {}
+        for k in self.flatten():
+            c[k] = c.get(k, 0) + 1
+        return sorted(c.items())
+
+    def used_gpcs(self) -> int:
+        return sum(self.flatten())
+
+    def key(self) -> tuple:
+        return (self.num_gpus, self.gpcs_per_gpu, tuple(tuple(g) for g in self.gpus))
+
+
+def paris_plan(table: ProfileTable, dist: BatchDistribution, total_gpcs: int, num_gpus: int, gpcs_per_gpu: int,
+               knee_threshold: float = 0.8) -> PartitionPlan:
+    """paris_plan (paris.hpp:329-345) through the C++ host header."""
+    n_per = np.zeros(num_gpus, np.int32)
+    flat = np.zeros(num_gpus * gpcs_per_gpu, np.int32)
+    sizes = _arr(table.sizes, np.int32)
+    lat = _arr(table.latency, np.float64)
+    util = _arr(table.utilization, np.float64)
+    w = _arr(dist.weights, np.float64)
+    if len(w) != table.b_max:
+        raise N.ValidationError("paris_plan: distribution support must match profile b_max")
+    check(N.lib().msv_paris_plan(len(sizes), _ptr(sizes, C.c_int32), table.b_max, _ptr(lat, C.c_double),
+                                 _ptr(util, C.c_double), _ptr(w, C.c_double), total_gpcs, num_gpus, gpcs_per_gpu,
+                                 knee_threshold, _ptr(n_per, C.c_int32), _ptr(flat, C.c_int32)), "paris_plan")
+    gpus, off = [], 0
+    for g in range(num_gpus):
+        gpus.append([int(x) for x in flat[off:off + n_per[g]]])
+        off += int(n_per[g])
+    return PartitionPlan(num_gpus, gpcs_per_gpu, gpus)
+
+
+def homogeneous_plan(k: int, total_gpcs: int, num_gpus: int, gpcs_per_gpu: int) -> PartitionPlan:
+    """homogeneous_plan (paris.hpp:275-290)."""
+    if k < 1:
+        raise N.ParamError("homogeneous_plan: k must be >= 1")
+    if num_gpus < 1:
+        raise N.ParamError("homogeneous_plan: num_gpus must be >= 1")
+    if k > gpcs_per_gpu:
+        raise N.InfeasibleError("homogeneous_plan: k exceeds gpcs_per_gpu")
+    n = min(num_gpus * (gpcs_per_gpu // k), total_gpcs // k)
+    gpus: list[list[int]] = [[] for _ in range(num_gpus)]
+    for i in range(n):
+        gpus[i % num_gpus].append(k)
+    return PartitionPlan(num_gpus, gpcs_per_gpu, gpus)
+
+
+@dataclass
+class SlaConfig:
+    sla_target_ms: float
+    alpha: float = 1.0
+    beta: float = 1.0
+
+
+def derive_sla_target(table: ProfileTable, b_max: int, multiplier: float) -> float:
+    """derive_sla_target (metrics.hpp:34-37)."""
+    if not multiplier > 0.0:
+        raise N.ParamError("derive_sla_target: multiplier must be > 0")
+    return multiplier * table.latency_ms(table.max_size(), b_max)
+
+
+@dataclass
+class GridSpec:
+    """One scenario of a grid (msv_scenario) in Python terms."""
+    plan: PartitionPlan
+    table: ProfileTable
+    dist: BatchDistribution
+    sla: SlaConfig
+    rate_qps: float
+    duration_ms: float
+    seed: int
+    scheduler: str = "elsa"
+    warmup_fraction: float = 0.1
+    routing: list[tuple[int, int, int]] | None = None  # (k, first, last) segments
+    check_wait: bool = False
+
+
+# Placeholder distribution of replay scenarios (the trace is the caller's).
+_REPLAY_DIST = BatchDistribution(np.ones(1))
+
+
+# ---------------------------------------------------------------------------
+# device context
+# ---------------------------------------------------------------------------
+class Engine:
+    """One msv_ctx: a CUDA device, its memory and stream."""
+
+    def __init__(self, device: int = 0, log1p_variant: int | None = None):
+        self._lib = N.lib()
+        h = C.c_void_p()
+        check(self._lib.msv_create(device, C.byref(h)), "msv_create")
+        self._h = h
+        self.device = device
+        if log1p_variant is not None:
+            check(self._lib.msv_set_log1p_variant(self._h, log1p_variant), "msv_set_log1p_variant")
+        self._profiles: dict[int, int] = {}
+        self._dists: dict[int, int] = {}
+        self._plans: dict[tuple, int] = {}
+        self._routings: dict[tuple, int] = {}
+        self._keep: list = []
+
+    def close(self) -> None:
+        if self._h:
+            self._lib.msv_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def log1p_variant(self) -> int:
+        v = C.c_int(-1)
+        check(self._lib.msv_get_log1p_variant(self._h, C.byref(v)))
+        return v.value
+
+    def kernel_launches(self) -> int:
+        return int(self._lib.msv_kernel_launches(self._h))
+
+    # ---- uploads (cached by object identity / value) ----
+    def profile(self, t: ProfileTable) -> int:
+        key = id(t)
+        if key not in self._profiles:
+            sizes = _arr(t.sizes, np.int32)
+            lat = _arr(t.latency, np.float64)
+            util = _arr(t.utilization, np.float64)
+            h = C.c_int32(-1)
+            check(self._lib.msv_upload_profile(self._h, len(sizes), _ptr(sizes, C.c_int32), t.b_max,
+                                               _ptr(lat, C.c_double), _ptr(util, C.c_double), C.byref(h)),
+                  "msv_upload_profile")
+            self._profiles[key] = h.value
+            self._keep.append(t)
+        return self._profiles[key]
+
+    def dist(self, d: BatchDistribution) -> int:
+        key = id(d)
+        if key not in self._dists:
+            w = _arr(d.weights, np.float64)
+            h = C.c_int32(-1)
+            check(self._lib.msv_upload_dist(self._h, len(w), _ptr(w, C.c_double), C.byref(h)), "msv_upload_dist")
+            self._dists[key] = h.value
+            self._keep.append(d)
+        return self._dists[key]
+
+    def plan(self, p: PartitionPlan) -> int:
+        key = p.key()
+        if key not in self._plans:
+            n_per = _arr([len(g) for g in p.gpus] or [0], np.int32)
+            flat = _arr(p.flatten() or [0], np.int32)
+            h = C.c_int32(-1)
+            check(self._lib.msv_upload_plan(self._h, p.num_gpus, p.gpcs_per_gpu, _ptr(n_per, C.c_int32),
+                                            _ptr(flat, C.c_int32), C.byref(h)), "msv_upload_plan")
+            self._plans[key] = h.value
+        return self._plans[key]
+
+    def routing(self, segs: Sequence[tuple[int, int, int]]) -> int:
+        key = tuple(tuple(s) for s in segs)
+        if key not in self._routings:
+            k = _arr([s[0] for s in segs] or [0], np.int32)
+            f = _arr([s[1] for s in segs] or [0], np.int32)
+            la = _arr([s[2] for s in segs] or [0], np.int32)
+            h = C.c_int32(-1)
+            check(self._lib.msv_upload_routing(self._h, len(segs), _ptr(k, C.c_int32), _ptr(f, C.c_int32),
+                                               _ptr(la, C.c_int32), C.byref(h)), "msv_upload_routing")
+            self._routings[key] = h.value
+        return self._routings[key]
+
+    def scenarios(self, specs: Iterable[GridSpec]) -> C.Array:
+        specs = list(specs)
+        arr = (N.Scenario * max(len(specs), 1))()
+        for i, s in enumerate(specs):
+            sc = arr[i]
+            sc.profile = self.profile(s.table)
+            sc.dist = self.dist(s.dist)
+            sc.plan = self.plan(s.plan)
+            sc.scheduler = N.MSV_ELSA if s.scheduler == "elsa" else N.MSV_FIFS
+            sc.routing = self.routing(s.routing) if s.routing is not None else -1
+            sc.flags = N.MSV_FLAG_CHECK_WAIT if s.check_wait else 0
+            sc.sla_ms, sc.alpha, sc.beta = s.sla.sla_target_ms, s.sla.alpha, s.sla.beta
+            sc.rate_qps, sc.duration_ms = s.rate_qps, s.duration_ms
+            sc.warmup_fraction, sc.seed = s.warmup_fraction, s.seed
+        return arr
+
+    # ---- hot path ----
+    def run_grid(self, specs: Sequence[GridSpec], tail_p: Sequence[float] = (0.95, 0.99), usage: bool = False
+                 ) -> dict:
+        sc = self.scenarios(specs)
+        n = len(specs)
+        ps = _arr(list(tail_p) or [0.5], np.float64)
+        res = (N.Result * max(n, 1))()
+        n_use = sum(s.plan.total_instances() for s in specs)
+        use = (N.Usage * max(n_use, 1))() if usage else None
+        check(self._lib.msv_run_grid(self._h, sc, n, _ptr(ps, C.c_double), len(tail_p), res, use), "run_grid")
+        return results_to_numpy(res, n, len(tail_p), use, n_use)
+
+    def run(self, plan: PartitionPlan, scheduler: str, arrival, batch, duration_ms: float, table: ProfileTable,
+            sla: SlaConfig, warmup_fraction: float = 0.1, routing=None, check_wait: bool = False,
+            tail_p: Sequence[float] = ()) -> dict:
+        """run() (engine.hpp:115-253) on one host trace, with per-query records."""
+        return self.run_many([(plan, scheduler, arrival, batch, duration_ms, table, sla, warmup_fraction, routing,
+                               check_wait)], tail_p)[0]
+
+    def run_many(self, items, tail_p: Sequence[float] = ()) -> list[dict]:
+        specs, arrs, bats = [], [], []
+        for plan, scheduler, arrival, batch, duration_ms, table, sla, warm, routing, cw in items:
+            specs.append(GridSpec(plan, table, _REPLAY_DIST, sla, 1.0, duration_ms, 0, scheduler, warm, routing,
+                                  cw))
+            arrs.append(_arr(arrival, np.float64))
+            bats.append(_arr(batch, np.int32))
+        sc = self.scenarios(specs)
+        n = len(specs)
+        offs = np.zeros(n + 1, np.int64)
+        for i, a in enumerate(arrs):
+            offs[i + 1] = offs[i] + len(a)
+        arrival = np.concatenate(arrs) if offs[-1] else np.zeros(1)
+        batch = np.concatenate(bats).astype(np.int32) if offs[-1] else np.zeros(1, np.int32)
+        ps = _arr(list(tail_p) or [0.5], np.float64)
+        res = (N.Result * max(n, 1))()
+        n_use = sum(s.plan.total_instances() for s in specs)
+        use = (N.Usage * max(n_use, 1))()
+        rec = (N.Record * max(int(offs[-1]), 1))()
+        check(self._lib.msv_run_replay(self._h, sc, n, _ptr(offs, C.c_int64), _ptr(arrival, C.c_double),
+                                       _ptr(batch, C.c_int32), _ptr(ps, C.c_double), len(tail_p), res, use, rec),
+              "run")
+        agg = results_to_numpy(res, n, len(tail_p), use, n_use)
+        recs = np.ctypeslib.as_array(rec)[: int(offs[-1])] if offs[-1] else np.zeros(0, rec._type_)
+        out, uo = [], 0
+        for i, s in enumerate(specs):
+            P = s.plan.total_instances()
+            r = {k: (v[i] if isinstance(v, np.ndarray) and k != "usage" else v) for k, v in agg.items() if k != "usage"}
+            rr = recs[offs[i]:offs[i + 1]]
+            r["partition"] = np.array(rr["partition"], np.int32)
+            r["start_ms"] = np.array(rr["start_ms"])
+            r["finish_ms"] = np.array(rr["finish_ms"])
+            r["kind"] = np.array(rr["kind"], np.int32)
+            r["busy_ms"] = agg["usage"]["busy_ms"][uo:uo + P]
+            r["weighted_busy_ms"] = agg["usage"]["weighted_busy_ms"][uo:uo + P]
+            r["queries"] = agg["usage"]["queries"][uo:uo + P]
+            uo += P
+            out.append(r)
+        return out
+
+    def sample_trace(self, dist: BatchDistribution, rate_qps: float, duration_ms: float, seed: int
+                     ) -> tuple[np.ndarray, np.ndarray]:
+        h = self.dist(dist)
+        mean = rate_qps * duration_ms / 1000.0 if rate_qps > 0 else 0.0
+        cap = int(np.ceil(mean + 10 * np.sqrt(max(mean, 0.0)) + 160))
+        while True:
+            arr = np.zeros(max(cap, 1))
+            bat = np.zeros(max(cap, 1), np.int32)
+            n = C.c_int64(0)
+            rc = self._lib.msv_sample_trace(self._h, h, rate_qps, duration_ms, seed, cap, _ptr(arr, C.c_double),
+                                            _ptr(bat, C.c_int32), C.byref(n))
+            if rc == N.MSV_PARAM and n.value > cap:
+                cap *= 4
+                continue
+            check(rc, "sample_trace")
+            return arr[: n.value].copy(), bat[: n.value].copy()
+
+    def tail_latency(self, samples, p: float | Sequence[float] = 0.95):
+        s = _arr(samples, np.float64)
+        ps = _arr([p] if np.isscalar(p) else list(p), np.float64)
+        out = np.zeros(len(ps))
+        check(self._lib.msv_tail_latency(self._h, _ptr(s, C.c_double), len(s), _ptr(ps, C.c_double), len(ps),
+                                         _ptr(out, C.c_double)), "tail_latency")
+        return float(out[0]) if np.isscalar(p) else out
+
+    def dispatch(self, table: ProfileTable | None, scheduler: str, trials: Sequence[dict], want_t_wait: bool = False):
+        """Batched elsa_dispatch / fifs_dispatch. Each trial: dict(parts=[(id, k, busy, cur_est, cur_start,
+        [queued batches])...], batch, now, sla, alpha, beta)."""
+        part_off, ids, ks, busy, est, start, q_off, qb = [0], [], [], [], [], [], [0], []
+        qbatch, now, sla, al, be = [], [], [], [], []
+        for t in trials:
+            for (pid, k, b, e, s, queue) in t["parts"]:
+                ids.append(pid)
+                ks.append(k)
+                busy.append(1 if b else 0)
+                est.append(e)
+                start.append(s)
+                qb.extend(queue)
+                q_off.append(len(qb))
+            part_off.append(len(ids))
+            qbatch.append(t["batch"])
+            now.append(t.get("now", 0.0))
+            sla.append(t.get("sla", 1.0))
+            al.append(t.get("alpha", 1.0))
+            be.append(t.get("beta", 1.0))
+        a = {k: _arr(v or [0], dt) for k, v, dt in [
+            ("part_off", part_off, np.int64), ("id", ids, np.int32), ("k", ks, np.int32), ("busy", busy, np.uint8),
+            ("est", est, np.float64), ("start", start, np.float64), ("q_off", q_off, np.int64),
+            ("qb", qb, np.int32), ("qbatch", qbatch, np.int32), ("now", now, np.float64), ("sla", sla, np.float64),
+            ("al", al, np.float64), ("be", be, np.float64)]}
+        n = len(trials)
+        chosen = np.zeros(max(n, 1), np.int32)
+        kind = np.zeros(max(n, 1), np.int32)
+        tw = np.zeros(max(len(ids), 1))
+        prof = self.profile(table) if table is not None else -1
+        check(self._lib.msv_dispatch_batch(
+            self._h, prof, N.MSV_ELSA if scheduler == "elsa" else N.MSV_FIFS, n, _ptr(a["part_off"], C.c_int64),
+            _ptr(a["id"], C.c_int32), _ptr(a["k"], C.c_int32), _ptr(a["busy"], C.c_uint8),
+            _ptr(a["est"], C.c_double), _ptr(a["start"], C.c_double), _ptr(a["q_off"], C.c_int64),
+            _ptr(a["qb"], C.c_int32), _ptr(a["qbatch"], C.c_int32), _ptr(a["now"], C.c_double),
+            _ptr(a["sla"], C.c_double), _ptr(a["al"], C.c_double), _ptr(a["be"], C.c_double),
+            _ptr(chosen, C.c_int32), _ptr(kind, C.c_int32), _ptr(tw, C.c_double) if want_t_wait else None),
+            "dispatch")
+        if want_t_wait:
+            return chosen[:n], kind[:n], tw[: len(ids)]
+        return chosen[:n], kind[:n]
+
+    def grid(self, specs: Sequence[GridSpec], tail_p: Sequence[float] = (0.95, 0.99)) -> "DeviceGrid":
+        return DeviceGrid(self, specs, tail_p)
+
+    def synchronize(self) -> None:
+        check(self._lib.msv_synchronize(self._h))
+
+    def event_record(self, slot: int) -> None:
+        check(self._lib.msv_event_record(self._h, slot), "msv_event_record")
+
+    def event_elapsed_ms(self, a: int, b: int) -> float:
+        ms = C.c_float()
+        check(self._lib.msv_event_elapsed(self._h, a, b, C.byref(ms)), "msv_event_elapsed")
+        return float(ms.value)
+
+    def transfer_bytes(self) -> tuple[int, int]:
+        h, d = C.c_int64(), C.c_int64()
+        check(self._lib.msv_transfer_bytes(self._h, C.byref(h), C.byref(d)))
+        return int(h.value), int(d.value)
+
+
+class DeviceGrid:
+    """msv_grid: scenarios, traces and outputs resident on the device; launch() runs
+    trace generation + simulation + tail selection with no host traffic."""
+
+    def __init__(self, eng: Engine, specs: Sequence[GridSpec], tail_p: Sequence[float]):
+        self.eng = eng
+        self.specs = list(specs)
+        self.tail_p = list(tail_p)
+        sc = eng.scenarios(self.specs)
+        ps = _arr(self.tail_p or [0.5], np.float64)
+        g = C.c_void_p()
+        check(eng._lib.msv_grid_create(eng._h, sc, len(self.specs), _ptr(ps, C.c_double), len(self.tail_p),
+                                       C.byref(g)), "msv_grid_create")
+        self._g = g
+        self.n_usage = sum(s.plan.total_instances() for s in self.specs)
+
+    def launch(self) -> None:
+        check(self.eng._lib.msv_grid_launch(self._g), "msv_grid_launch")
+
+    def timing(self) -> dict:
+        t = [C.c_float() for _ in range(4)]
+        check(self.eng._lib.msv_grid_timing(self._g, *[C.byref(x) for x in t]), "msv_grid_timing")
+        return dict(zip(("total_ms", "trace_ms", "sim_ms", "tail_ms"), (x.value for x in t)))
+
+    def queries(self) -> int:
+        return int(self.eng._lib.msv_grid_queries(self._g))
+
+    def results(self, usage: bool = False) -> dict:
+        n = len(self.specs)
+        res = (N.Result * max(n, 1))()
+        use = (N.Usage * max(self.n_usage, 1))() if usage else None
+        check(self.eng._lib.msv_grid_results(self._g, res, use), "msv_grid_results")
+        return results_to_numpy(res, n, len(self.tail_p), use, self.n_usage)
+
+    def close(self) -> None:
+        if self._g:
+            self.eng._lib.msv_grid_destroy(self._g)
+            self._g = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def results_to_numpy(res, n: int, n_tails: int, use=None, n_use: int = 0) -> dict:
+    a = np.ctypeslib.as_array(res)[:n] if n else np.zeros(0, np.dtype(N.Result))
+    out = {
+        "total": np.array(a["total"]), "violations": np.array(a["violations"]), "measured": np.array(a["measured"]),
+        "measured_violations": np.array(a["measured_violations"]),
+        "tail": np.array(a["tail"])[:, :n_tails] if n else np.zeros((0, n_tails)),
+        "horizon_ms": np.array(a["horizon_ms"]), "warmup_ms": np.array(a["warmup_ms"]),
+        "max_wait_estimate_diff": np.array(a["max_wait_estimate_diff"]),
+        "placement_hash": np.array(a["placement_hash"], dtype=np.uint64), "status": np.array(a["status"]),
+    }
+    if use is not None:
+        u = np.ctypeslib.as_array(use)[:n_use]
+        out["usage"] = {"busy_ms": np.array(u["busy_ms"]), "weighted_busy_ms": np.array(u["weighted_busy_ms"]),
+                        "queries": np.array(u["queries"])}
+    return out
