@@ -85,10 +85,12 @@ static inline uint64_t ora_bits(double x) {
     return v.u;
 }
 static inline uint64_t ora_query_digest(uint64_t id, int32_t partition, double start, double finish) {
-    uint64_t h = ora_mix64(id ^ ((uint64_t)(uint32_t)partition << 40));
-    h = ora_mix64(h ^ ora_bits(start));
-    h = ora_mix64(h ^ ora_bits(finish));
-    return h;
+    uint64_t x = ora_bits(start) + ora_bits(finish) * 0x9E3779B97F4A7C15ull +
+                 ((id << 8) | (uint64_t)(uint8_t)partition) * 0xC2B2AE3D27D4EB4Full;
+    x ^= x >> 31;
+    x *= 0xBF58476D1CE4E5B9ull;
+    x ^= x >> 29;
+    return x;
 }
 
 /* ---- entry points (same names in both oracles, prefix ora_) ---- */

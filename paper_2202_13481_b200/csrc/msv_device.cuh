@@ -1,0 +1,90 @@
+// Device helpers shared by the kernels. Every .cu of the engine is compiled with
+// -fmad=false: decision and accumulation expressions must round exactly like the
+// reference's x86-64 SSE2 build (no contraction).
+#pragma once
+
+#include <math.h>
+
+#include "msv_internal.h"
+#include "msv_math.h"
+
+namespace msv {
+
+constexpr unsigned kFull = 0xffffffffu;
+constexpr uint64_t kSignBit = 1ull << 63;
+
+// Order-preserving map of IEEE doubles onto uint64 (total order of finite values).
+__device__ __forceinline__ uint64_t order_key(uint64_t b) { return (b & kSignBit) ? ~b : (b | kSignBit); }
+__device__ __forceinline__ uint64_t order_unkey(uint64_t k) { return (k & kSignBit) ? (k & ~kSignBit) : ~k; }
+
+// Minimum over the W-lane segment of a warp; every lane of the warp must call it.
+template <int W>
+__device__ __forceinline__ uint32_t seg_min_u32(uint32_t v) {
+    if constexpr (W == 32) {
+        return __reduce_min_sync(kFull, v);
+    } else {
+#pragma unroll
+        for (int off = W / 2; off > 0; off >>= 1) {
+            const uint32_t o = __shfl_xor_sync(kFull, v, off);
+            v = o < v ? o : v;
+        }
+        return v;
+    }
+}
+
+// Minimum of non-negative IEEE bit patterns (or ~0 sentinels) over a segment.
+template <int W>
+__device__ __forceinline__ uint64_t seg_min_u64(uint64_t v) {
+    if constexpr (W == 32) {
+        const uint32_t hi = (uint32_t)(v >> 32);
+        const uint32_t mh = __reduce_min_sync(kFull, hi);
+        const uint32_t lo = (hi == mh) ? (uint32_t)v : 0xffffffffu;
+        const uint32_t ml = __reduce_min_sync(kFull, lo);
+        return ((uint64_t)mh << 32) | ml;
+    } else {
+#pragma unroll
+        for (int off = W / 2; off > 0; off >>= 1) {
+            const uint64_t o = __shfl_xor_sync(kFull, v, off);
+            v = o < v ? o : v;
+        }
+        return v;
+    }
+}
+
+// Segment-masked reductions for segment-uniform branches (only that segment's lanes).
+template <int W>
+__device__ __forceinline__ uint64_t seg_sum_u64(uint64_t v, unsigned mask) {
+#pragma unroll
+    for (int off = W / 2; off > 0; off >>= 1) v += __shfl_xor_sync(mask, v, off);
+    return v;
+}
+template <int W>
+__device__ __forceinline__ uint64_t seg_max_u64(uint64_t v, unsigned mask) {
+#pragma unroll
+    for (int off = W / 2; off > 0; off >>= 1) {
+        const uint64_t o = __shfl_xor_sync(mask, v, off);
+        v = o > v ? o : v;
+    }
+    return v;
+}
+template <int W>
+__device__ __forceinline__ uint64_t seg_minm_u64(uint64_t v, unsigned mask) {
+#pragma unroll
+    for (int off = W / 2; off > 0; off >>= 1) {
+        const uint64_t o = __shfl_xor_sync(mask, v, off);
+        v = o < v ? o : v;
+    }
+    return v;
+}
+// std::max on doubles as the reference writes it: (a < b) ? b : a.
+template <int W>
+__device__ __forceinline__ double seg_max_f64(double v, unsigned mask) {
+#pragma unroll
+    for (int off = W / 2; off > 0; off >>= 1) {
+        const double o = __shfl_xor_sync(mask, v, off);
+        v = (v < o) ? o : v;
+    }
+    return v;
+}
+
+}  // namespace msv

@@ -210,6 +210,7 @@ struct msv_grid {
     std::vector<double> tail_p;
     std::vector<int64_t> cap, toff;   // per-scenario trace capacity and offset
     std::vector<int32_t> P, usage_off;
+    std::vector<uint8_t> bad;  // plan has a size the profile lacks
     int64_t usage_total = 0;
     struct Wave {
         int64_t s0 = 0, s1 = 0;  // scenarios [s0, s1)
@@ -459,6 +460,7 @@ int grid_build(msv_ctx* ctx, const msv_scenario* sc, int64_t n, const double* ta
     std::vector<DevPart> parts_h;
     std::vector<uint64_t> masks_h;
     std::vector<size_t> sc_part(n), sc_mask(n, (size_t)-1);
+    g->bad.assign(n, 0);
     for (int64_t i = 0; i < n; ++i) {
         auto key = std::make_pair(sc[i].plan, sc[i].profile);
         auto it = part_off.find(key);
@@ -469,6 +471,8 @@ int grid_build(msv_ctx* ctx, const msv_scenario* sc, int64_t n, const double* ta
             parts_h.insert(parts_h.end(), pp.begin(), pp.end());
         }
         sc_part[i] = it->second;
+        for (int32_t j = 0; j < g->P[i]; ++j)
+            if (parts_h[it->second + j].row < 0) g->bad[i] = 1;
         if (sc[i].routing >= 0) {
             auto mk = std::make_tuple(sc[i].plan, sc[i].profile, sc[i].routing);
             auto mt = mask_off.find(mk);
@@ -600,7 +604,12 @@ int grid_launch(msv_grid* g) {
             p.lat = g->d_glat.as<double>();
             p.util = g->d_gutil.as<double>();
             p.n_cells = g->n_cells;
-            p.pad = 0;
+            p.any_routing = p.any_bad = p.any_check_wait = 0;
+            for (int32_t si : w.classes[c].second) {
+                if (g->scen[si].routing >= 0) p.any_routing = 1;
+                if (g->bad[si]) p.any_bad = 1;
+                if (g->scen[si].flags & MSV_FLAG_CHECK_WAIT) p.any_check_wait = 1;
+            }
             const int occ = msv::sim_max_blocks_per_sm(k.W, k.S, k.sched, g->records, g->n_cells);
             if (occ <= 0) return fail(MSV_CUDA, "sim kernel: no occupancy for class");
             const int segs_per_block = msv::kSimWarpsPerBlock * (32 / k.W);

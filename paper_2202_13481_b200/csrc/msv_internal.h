@@ -16,7 +16,7 @@ constexpr int kQCap = 8;
 // Profile cells (latency + utilisation, all uploaded profiles) staged in shared
 // memory by the simulation kernel.
 constexpr int kMaxSmemCells = 1024;
-constexpr int kSimWarpsPerBlock = 8;
+constexpr int kSimWarpsPerBlock = 4;
 constexpr int kTraceWarpsPerBlock = 4;
 constexpr int kTailThreads = 256;
 constexpr int kTailSmemCap = 2048;  // values gathered for the final in-smem select
@@ -78,7 +78,11 @@ struct SimParams {
     const double* lat;    // all profile latency cells
     const double* util;   // all profile utilisation cells
     int32_t n_cells;
-    int32_t pad;
+    // Launch-wide feature flags: when 0, the kernel skips the corresponding per-arrival
+    // warp votes entirely.
+    int32_t any_routing;     // some scenario uses segment routing
+    int32_t any_bad;         // some plan has a size the profile lacks
+    int32_t any_check_wait;  // some scenario sets MSV_FLAG_CHECK_WAIT
 };
 
 // Trace generation job (sample_trace, workload.hpp:97-113).
@@ -135,7 +139,7 @@ cudaError_t launch_trace_gen(const TraceJob* d_jobs, int n_jobs, int log1p_varia
 // sched is the scenario class's scheduler (all scenarios of one launch share it).
 cudaError_t launch_sim(int W, int S, int sched, bool records, const SimParams& p, int blocks,
                        cudaStream_t stream);
-size_t sim_smem_bytes(int S, int n_cells);
+size_t sim_smem_bytes(int W, int S, int n_cells);
 int sim_max_blocks_per_sm(int W, int S, int sched, bool records, int n_cells);
 cudaError_t launch_tail(const TailJob* d_jobs, int n_jobs, const double* d_p, int n_p,
                         cudaStream_t stream);

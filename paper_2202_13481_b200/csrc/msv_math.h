@@ -194,8 +194,10 @@ MSV_HD uint64_t msv_mix64(uint64_t z) {
 }
 
 MSV_HD uint64_t msv_query_digest(uint64_t id, int32_t partition, double start, double finish) {
-    uint64_t h = msv_mix64(id ^ ((uint64_t)(uint32_t)partition << 40));
-    h = msv_mix64(h ^ msv_dbits(start));
-    h = msv_mix64(h ^ msv_dbits(finish));
-    return h;
+    uint64_t x = msv_dbits(start) + msv_dbits(finish) * 0x9E3779B97F4A7C15ull +
+                 ((id << 8) | (uint64_t)(uint8_t)partition) * 0xC2B2AE3D27D4EB4Full;
+    x ^= x >> 31;
+    x *= 0xBF58476D1CE4E5B9ull;
+    x ^= x >> 29;
+    return x;
 }

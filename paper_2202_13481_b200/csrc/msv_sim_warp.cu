@@ -1,0 +1,406 @@
+// K2 for plans of 17..128 partitions: sim_warp_kernel — one scenario per warp.
+//
+// Same semantics as msv_sim.cu (see its header for the per-arrival protocol) with
+// the warp-uniform structure this class allows: scenario -> 32-arrival window ->
+// arrival loops with no per-arrival bookkeeping; the window's first measured
+// arrival is one ballot; Step B's 64-bit argmin is two REDUX.MIN; the horizon is
+// the last completion each lane retained. Lane slot s of lane l owns by_ascending_size
+// order index s*32 + l (sched.hpp:96-104).
+#include "msv_device.cuh"
+
+namespace msv {
+
+namespace {
+
+constexpr uint64_t kQid = (1ull << 40) - 1;
+
+template <int S>
+struct WarpCfg {
+    static constexpr int qcap = S == 1 ? 8 : (S == 2 ? 4 : 2);  // shared ring entries per slot
+    static constexpr int min_blocks = S == 1 ? 5 : (S == 2 ? 4 : 2);
+};
+
+template <int S, int SCHED, bool REC>
+__global__ void __launch_bounds__(kSimWarpsPerBlock * 32, WarpCfg<S>::min_blocks)
+    sim_warp_kernel(const SimParams p) {
+    constexpr int QC = WarpCfg<S>::qcap;
+    extern __shared__ __align__(16) unsigned char smem[];
+    double* s_lat = reinterpret_cast<double*>(smem);
+    double* s_util = s_lat + p.n_cells;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const size_t tab_bytes = ((size_t)2 * p.n_cells * sizeof(double) + 15) & ~(size_t)15;
+    double* q_est = reinterpret_cast<double*>(smem + tab_bytes) + (size_t)warp * (3 * S * QC * 32);
+    double* q_arr = q_est + S * QC * 32;
+    uint64_t* q_meta = reinterpret_cast<uint64_t*>(q_arr + S * QC * 32);
+    for (int c = threadIdx.x; c < p.n_cells; c += blockDim.x) {
+        s_lat[c] = p.lat[c];
+        s_util[c] = p.util[c];
+    }
+    __syncthreads();
+
+    for (;;) {
+        int w = 0;
+        if (lane == 0) w = atomicAdd(p.counter, 1);
+        w = __shfl_sync(kFull, w, 0);
+        if (w >= p.n_work) break;
+        const int sidx = p.work[w];
+        const DevScen& d = p.scen[sidx];
+        const int n = (int)*d.n;
+        const double* __restrict__ g_arr = d.arrival;
+        const int32_t* __restrict__ g_bat = d.batch;
+        uint32_t* g_next = d.next;
+        double* samples = d.samples;
+        msv_record* rec = d.records;
+        const double sla = d.sla, warmup = d.warmup_ms, alpha = d.alpha, beta = d.beta;
+        const bool unit_ab = alpha == 1.0 && beta == 1.0;  // 1*x == x: identical bits
+        const bool check_wait = p.any_check_wait && (d.flags & MSV_FLAG_CHECK_WAIT);
+        const int bmax = d.b_max;
+        const bool routed = d.route_mask != nullptr;
+
+        // ---- lane slots ----
+        bool act[S], busy[S];
+        int32_t row[S], pid[S], kk[S], qh[S], qn[S];
+        uint32_t gh[S], gt[S], gn[S], nq[S];
+        double c_start[S], c_est[S], c_comp[S], c_arr[S], fold[S], bms[S], wbms[S];
+        uint64_t c_meta[S], rmask[S];
+#pragma unroll
+        for (int s = 0; s < S; ++s) {
+            const int o = s * 32 + lane;
+            act[s] = o < d.P;
+            row[s] = -1;
+            pid[s] = kk[s] = 0;
+            rmask[s] = 0;
+            if (act[s]) {
+                const DevPart dp = d.parts[o];
+                pid[s] = dp.pid;
+                kk[s] = dp.k;
+                row[s] = dp.row;
+                if (routed) rmask[s] = d.route_mask[o];
+            }
+            busy[s] = false;
+            qh[s] = qn[s] = 0;
+            gh[s] = gt[s] = gn[s] = nq[s] = 0;
+            c_start[s] = c_est[s] = c_comp[s] = c_arr[s] = 0.0;
+            fold[s] = 0.0;  // < 0: must be recomputed
+            bms[s] = wbms[s] = 0.0;
+            c_meta[s] = 0;
+        }
+        uint32_t viol = 0, mviol = 0;
+        uint64_t hash = 0;
+        double wdiff = 0.0;
+        int m0 = -1, status = 0;
+
+        // Retire every completion of this lane with time <= t, in chain order.
+        auto drain = [&](double t) {
+#pragma unroll
+            for (int s = 0; s < S; ++s) {
+                while (busy[s] && c_comp[s] <= t) {  // engine.hpp:167-187
+                    const double now = c_comp[s];
+                    const double lat = now - c_arr[s];
+                    const bool met = lat <= sla;
+                    const double ran = now - c_start[s];
+                    const uint64_t q = c_meta[s] & kQid;
+                    const int cb = (int)(c_meta[s] >> 40);
+                    bms[s] = bms[s] + ran;
+                    wbms[s] = wbms[s] + ran * s_util[row[s] + cb - 1];
+                    nq[s] += 1;
+                    viol += met ? 0u : 1u;
+                    if (c_arr[s] >= warmup) {
+                        mviol += met ? 0u : 1u;
+                        samples[(uint32_t)q - (uint32_t)m0] = lat;
+                    }
+                    hash += msv_query_digest(q, pid[s], c_start[s], now);
+                    if (REC) {
+                        rec[q].start_ms = c_start[s];
+                        rec[q].finish_ms = now;
+                    }
+                    if (qn[s] > 0) {  // start the queue head now (engine.hpp:181-185)
+                        const int e = (s * QC + qh[s]) * 32 + lane;
+                        const double est = q_est[e];
+                        c_arr[s] = q_arr[e];
+                        c_meta[s] = q_meta[e];
+                        qh[s] = (qh[s] + 1) & (QC - 1);
+                        qn[s] -= 1;
+                        if (gn[s] > 0) {  // refill the ring from the overflow list
+                            const uint32_t g = gh[s];
+                            gh[s] = g_next[g];
+                            gn[s] -= 1;
+                            const int32_t gb = g_bat[g];
+                            const int e2 = (s * QC + ((qh[s] + qn[s]) & (QC - 1))) * 32 + lane;
+                            q_est[e2] = s_lat[row[s] + gb - 1];
+                            q_arr[e2] = g_arr[g];
+                            q_meta[e2] = (uint64_t)g | ((uint64_t)gb << 40);
+                            qn[s] += 1;
+                        }
+                        c_start[s] = now;
+                        c_est[s] = est;
+                        c_comp[s] = now + est;
+                        fold[s] = qn[s] == 0 ? 0.0 : -1.0;
+                    } else {
+                        busy[s] = false;
+                        fold[s] = 0.0;
+                    }
+                }
+            }
+        };
+
+        double nx_t = lane < n ? g_arr[lane] : 0.0;
+        int nx_b = lane < n ? g_bat[lane] : 0;
+        for (int base = 0; base < n && status == 0; base += 32) {
+            const double win_t = nx_t;
+            const int win_b = nx_b;
+            if (base + 32 + lane < n) {
+                nx_t = g_arr[base + 32 + lane];
+                nx_b = g_bat[base + 32 + lane];
+            }
+            if (m0 < 0) {  // first arrival >= warmup (arrivals are sorted; engine.hpp:262)
+                const unsigned mb = __ballot_sync(kFull, base + lane < n && win_t >= warmup);
+                if (mb) m0 = base + __ffs(mb) - 1;
+            }
+            const int cnt = min(32, n - base);
+            for (int j = 0; j < cnt; ++j) {
+                const double t = __shfl_sync(kFull, win_t, j);
+                const int b = __shfl_sync(kFull, win_b, j);
+                const int i = base + j;
+                drain(t);
+                if (b < 1 || b > bmax) {  // LookupError at this query (profile.hpp:127-129)
+                    status = MSV_LOOKUP;
+                    break;
+                }
+                // ---- candidates, Eq. 1 waits ----
+                bool cand[S];
+                double est_n[S], wv[S];
+#pragma unroll
+                for (int s = 0; s < S; ++s) {
+                    cand[s] = act[s];
+                    est_n[s] = row[s] >= 0 ? s_lat[row[s] + b - 1] : 0.0;
+                    wv[s] = 0.0;
+                }
+                if (p.any_routing && routed) {  // engine.hpp:197-206 (warp-uniform)
+                    unsigned anyc = 0;
+#pragma unroll
+                    for (int s = 0; s < S; ++s) {
+                        cand[s] = act[s] && (((rmask[s] >> (b - 1)) & 1ull) != 0);
+                        anyc |= __ballot_sync(kFull, cand[s]);
+                    }
+                    if (anyc == 0) {
+#pragma unroll
+                        for (int s = 0; s < S; ++s) cand[s] = act[s];
+                    }
+                }
+                int bad_o = 1 << 30;  // order index of the first candidate whose size is missing
+                if (p.any_bad) {
+#pragma unroll
+                    for (int s = S - 1; s >= 0; --s) {
+                        const unsigned bb = __ballot_sync(kFull, cand[s] && row[s] < 0);
+                        if (bb) bad_o = s * 32 + __ffs(bb) - 1;
+                    }
+                }
+                if (SCHED == MSV_ELSA || check_wait) {
+#pragma unroll
+                    for (int s = 0; s < S; ++s) {
+                        if (!cand[s] || row[s] < 0) continue;
+                        if (fold[s] < 0.0) {  // exact left fold of the FIFO (sched.hpp:78-79)
+                            double acc = 0.0;
+                            for (int k = 0; k < qn[s]; ++k) acc = acc + q_est[(s * QC + ((qh[s] + k) & (QC - 1))) * 32 + lane];
+                            uint32_t g = gh[s];
+                            for (uint32_t k = 0; k < gn[s]; ++k) {
+                                acc = acc + s_lat[row[s] + g_bat[g] - 1];
+                                g = g_next[g];
+                            }
+                            fold[s] = acc;
+                        }
+                        double wt = fold[s];
+                        if (busy[s]) {  // sched.hpp:80-83
+                            const double x = c_est[s] - (t - c_start[s]);
+                            wt = wt + ((0.0 < x) ? x : 0.0);
+                        }
+                        wv[s] = wt;
+                        if (check_wait) {  // engine.hpp:208-217
+                            double gw = fold[s];
+                            if (busy[s]) {
+                                const double y = c_comp[s] - t;
+                                gw = gw + ((0.0 < y) ? y : 0.0);
+                            }
+                            const double dd = fabs(gw - wt);
+                            wdiff = (wdiff < dd) ? dd : wdiff;
+                        }
+                    }
+                }
+                // ---- decision ----
+                int ch = -1;  // chosen order index
+                int kind;
+                if constexpr (SCHED == MSV_ELSA) {
+                    // Step A (sched.hpp:125-130): first in order with sla > alpha*(w + beta*est).
+#pragma unroll
+                    for (int s = S - 1; s >= 0; --s) {
+                        const bool ok = cand[s] && row[s] >= 0;
+                        const bool pred =
+                            ok && (unit_ab ? (sla > wv[s] + est_n[s]) : (sla > alpha * (wv[s] + beta * est_n[s])));
+                        const unsigned bA = __ballot_sync(kFull, pred);
+                        if (bA) ch = s * 32 + __ffs(bA) - 1;
+                    }
+                    kind = MSV_SLACK_SATISFYING;
+                    if (ch < 0) {  // Step B (sched.hpp:132-142): argmin w + est, earliest on ties
+                        uint64_t fb[S];
+                        uint64_t vmin = ~0ull;
+#pragma unroll
+                        for (int s = 0; s < S; ++s) {
+                            fb[s] = (cand[s] && row[s] >= 0) ? msv_dbits(wv[s] + est_n[s]) : ~0ull;
+                            vmin = fb[s] < vmin ? fb[s] : vmin;
+                        }
+                        vmin = seg_min_u64<32>(vmin);
+#pragma unroll
+                        for (int s = S - 1; s >= 0; --s) {
+                            const unsigned bB = __ballot_sync(kFull, fb[s] == vmin && vmin != ~0ull);
+                            if (bB) ch = s * 32 + __ffs(bB) - 1;
+                        }
+                        kind = MSV_FASTEST_FALLBACK;
+                    }
+                    // a size missing from the profile is a LookupError once the scan reaches it
+                    if (bad_o != (1 << 30) && (kind == MSV_FASTEST_FALLBACK || bad_o < ch)) {
+                        status = MSV_LOOKUP;
+                        break;
+                    }
+                } else {
+                    // FIFS (sched.hpp:154-170): idle -> max k, min id; else min queue length, min id.
+                    uint32_t mi = ~0u;
+#pragma unroll
+                    for (int s = 0; s < S; ++s) {
+                        const uint32_t key =
+                            (cand[s] && !busy[s]) ? (((0x7FFFu - (uint32_t)kk[s]) << 16) | (uint32_t)pid[s]) : ~0u;
+                        mi = key < mi ? key : mi;
+                    }
+                    mi = __reduce_min_sync(kFull, mi);
+                    uint32_t key2[S];
+                    if (mi != ~0u) {
+                        kind = MSV_IDLE_LARGEST;
+                        // the key encodes (k, id): its owner is the lane slot with that pid
+#pragma unroll
+                        for (int s = 0; s < S; ++s) key2[s] = (cand[s] && !busy[s]) ? (((0x7FFFu - (uint32_t)kk[s]) << 16) | (uint32_t)pid[s]) : ~0u;
+                    } else {
+                        kind = MSV_SHORTEST_QUEUE;
+                        uint32_t mq = ~0u;
+#pragma unroll
+                        for (int s = 0; s < S; ++s) {
+                            const uint32_t len = (uint32_t)qn[s] + gn[s];
+                            key2[s] = cand[s] ? (((len < 0xFFFFFFu ? len : 0xFFFFFFu) << 8) | (uint32_t)pid[s]) : ~0u;
+                            mq = key2[s] < mq ? key2[s] : mq;
+                        }
+                        mi = __reduce_min_sync(kFull, mq);
+                    }
+#pragma unroll
+                    for (int s = S - 1; s >= 0; --s) {
+                        const unsigned bs = __ballot_sync(kFull, key2[s] == mi);
+                        if (bs) ch = s * 32 + __ffs(bs) - 1;
+                    }
+                    if (p.any_bad) {  // the chosen partition's latency lookup fails (engine.hpp:226)
+                        bool mine = false;
+#pragma unroll
+                        for (int s = 0; s < S; ++s) mine |= (s * 32 + lane == ch) && row[s] < 0;
+                        if (__any_sync(kFull, mine)) {
+                            status = MSV_LOOKUP;
+                            break;
+                        }
+                    }
+                }
+                // ---- start or enqueue on the chosen partition (engine.hpp:225-230) ----
+#pragma unroll
+                for (int s = 0; s < S; ++s) {
+                    if (s * 32 + lane == ch) {
+                        const double est = est_n[s];
+                        if (!busy[s]) {
+                            busy[s] = true;
+                            c_start[s] = t;
+                            c_est[s] = est;
+                            c_comp[s] = t + est;
+                            c_arr[s] = t;
+                            c_meta[s] = (uint64_t)i | ((uint64_t)b << 40);
+                        } else {
+                            if (gn[s] == 0 && qn[s] < QC) {
+                                const int e = (s * QC + ((qh[s] + qn[s]) & (QC - 1))) * 32 + lane;
+                                q_est[e] = est;
+                                q_arr[e] = t;
+                                q_meta[e] = (uint64_t)i | ((uint64_t)b << 40);
+                                qn[s] += 1;
+                            } else {
+                                if (gn[s] == 0) gh[s] = (uint32_t)i;
+                                else g_next[gt[s]] = (uint32_t)i;
+                                gt[s] = (uint32_t)i;
+                                gn[s] += 1;
+                            }
+                            if (fold[s] >= 0.0) fold[s] = fold[s] + est;
+                        }
+                        if (REC) {
+                            rec[i].partition = pid[s];
+                            rec[i].kind = kind;
+                        }
+                    }
+                }
+            }
+        }
+        drain(INFINITY);  // after the last arrival: drain everything, no horizon cut-off
+
+        // ---- publish (engine.hpp:233-252) ----
+        double lf = 0.0;  // last completion = each lane's final c_comp (completions per lane ascend)
+#pragma unroll
+        for (int s = 0; s < S; ++s)
+            if (nq[s] > 0) lf = (lf < c_comp[s]) ? c_comp[s] : lf;
+        const uint64_t v0 = seg_sum_u64<32>((uint64_t)viol, kFull);
+        const uint64_t v2 = seg_sum_u64<32>((uint64_t)mviol, kFull);
+        const uint64_t hsum = seg_sum_u64<32>(hash, kFull);
+        lf = seg_max_f64<32>(lf, kFull);
+        const double wd = seg_max_f64<32>(wdiff, kFull);
+        if (lane == 0) {
+            DevOut o;
+            o.violations = (int64_t)v0;
+            o.measured = m0 >= 0 ? n - m0 : 0;
+            o.measured_violations = (int64_t)v2;
+            o.n_samples = o.measured;
+            o.horizon_ms = (d.duration_ms < lf) ? lf : d.duration_ms;  // engine.hpp:237
+            o.max_wait_diff = wd;
+            o.hash = hsum;
+            o.lat_min_bits = ~0ull;  // K3 derives the key range
+            o.lat_max_bits = 0;
+            o.status = status;
+            o.pad = 0;
+            p.out[sidx] = o;
+        }
+        if (d.usage_off >= 0) {
+#pragma unroll
+            for (int s = 0; s < S; ++s) {
+                if (act[s]) {
+                    msv_usage u;
+                    u.busy_ms = bms[s];
+                    u.weighted_busy_ms = wbms[s];
+                    u.queries = nq[s];
+                    p.usage[d.usage_off + pid[s]] = u;
+                }
+            }
+        }
+    }
+}
+
+}  // namespace
+
+void* sim_warp_fn(int S, int sched, bool rec) {
+#define MSV_PICKW(s)                                                                                           \
+    if (S == s) {                                                                                              \
+        if (sched == MSV_ELSA)                                                                                 \
+            return rec ? (void*)&sim_warp_kernel<s, MSV_ELSA, true> : (void*)&sim_warp_kernel<s, MSV_ELSA, false>; \
+        return rec ? (void*)&sim_warp_kernel<s, MSV_FIFS, true> : (void*)&sim_warp_kernel<s, MSV_FIFS, false>;     \
+    }
+    MSV_PICKW(1)
+    MSV_PICKW(2)
+    MSV_PICKW(4)
+#undef MSV_PICKW
+    return nullptr;
+}
+
+size_t sim_warp_smem_bytes(int S, int n_cells) {
+    const int qc = S == 1 ? 8 : (S == 2 ? 4 : 2);
+    const size_t tab = ((size_t)2 * n_cells * sizeof(double) + 15) & ~(size_t)15;
+    return tab + (size_t)kSimWarpsPerBlock * 3 * S * qc * 32 * sizeof(double);
+}
+
+}  // namespace msv
