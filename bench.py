@@ -39,7 +39,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--seeds", type=int, default=128, help="seeds per load level per rank")
+    ap.add_argument("--seeds", type=int, default=1024, help="seeds per load level per rank")
     ap.add_argument("--queries", type=float, default=1e5, help="expected queries per scenario")
     ap.add_argument("--cpu-seconds", type=float, default=15.0, help="CPU baseline sample budget")
     ap.add_argument("--no-cpu-baseline", action="store_true")

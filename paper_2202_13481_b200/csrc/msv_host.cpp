@@ -8,6 +8,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <map>
 #include <memory>
 #include <numeric>
@@ -113,8 +114,16 @@ namespace migserve_capi {
 int set_error(int code, const char* what) { return fail(code, what ? what : ""); }
 }  // namespace migserve_capi
 
+// Device buffers of one grid launch sequence.
+struct GridBufs {
+    DevBuf d_scen, d_out, d_tjobs, d_tailjobs, d_tails, d_p, d_usage, d_nq, d_tovf, d_parts, d_masks, d_work,
+        d_counter;
+    DevBuf d_arr, d_bat, d_next, d_samples, d_rec, d_glat, d_gutil;
+};
+
 struct msv_ctx {
     int device = 0;
+    GridBufs scratch;  // reused by one-shot grids (msv_run_grid / msv_run_replay)
     int sms = 148;
     cudaStream_t stream = nullptr;
     int log1p = MSV_LOG1P_FMA;
@@ -220,9 +229,8 @@ struct msv_grid {
     };
     std::vector<Wave> waves;
     int64_t max_wave_q = 0;
-    DevBuf d_scen, d_out, d_tjobs, d_tailjobs, d_tails, d_p, d_usage, d_nq, d_tovf, d_parts, d_masks,
-        d_work, d_counter;
-    DevBuf d_arr, d_bat, d_next, d_samples, d_rec, d_glat, d_gutil;
+    GridBufs own;            // buffers of a persistent grid (msv_grid_create)
+    GridBufs* B = &own;      // -> own, or the context's scratch set for one-shot calls
     int n_cells = 0;
     std::vector<DevScen> h_scen;  // pointers into the wave buffers
     cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
@@ -326,7 +334,7 @@ size_t free_device_bytes() {
 // Build a grid. generated: traces from K1; otherwise host traces (offsets/arrival/batch).
 int grid_build(msv_ctx* ctx, const msv_scenario* sc, int64_t n, const double* tail_p, int n_tails,
                const int64_t* offsets, const double* arrival, const int32_t* batch, bool records,
-               msv_grid** out, const int64_t* cap_override = nullptr) {
+               msv_grid** out, const int64_t* cap_override = nullptr, bool scratch = false) {
     if (n < 0) return fail(MSV_PARAM, "grid: negative scenario count");
     if (n_tails < 0 || n_tails > 4) return fail(MSV_PARAM, "grid: between 0 and 4 tail percentiles");
     for (int j = 0; j < n_tails; ++j)
@@ -336,6 +344,7 @@ int grid_build(msv_ctx* ctx, const msv_scenario* sc, int64_t n, const double* ta
     if (rc) return rc;
     std::unique_ptr<msv_grid> g(new msv_grid);
     g->ctx = ctx;
+    if (scratch) g->B = &ctx->scratch;
     g->generated = offsets == nullptr;
     g->records = records;
     g->n = n;
@@ -417,22 +426,22 @@ int grid_build(msv_ctx* ctx, const msv_scenario* sc, int64_t n, const double* ta
     }
     // Device buffers.
     const size_t wq = (size_t)std::max<int64_t>(g->max_wave_q, 1);
-    MSV_CUDA_TRY(g->d_arr.ensure(wq * 8));
-    MSV_CUDA_TRY(g->d_bat.ensure(wq * 4));
-    MSV_CUDA_TRY(g->d_next.ensure(wq * 4));
-    MSV_CUDA_TRY(g->d_samples.ensure(wq * 8));
-    if (records) MSV_CUDA_TRY(g->d_rec.ensure(wq * sizeof(msv_record)));
-    MSV_CUDA_TRY(g->d_scen.ensure(std::max<int64_t>(n, 1) * sizeof(DevScen)));
-    MSV_CUDA_TRY(g->d_out.ensure(std::max<int64_t>(n, 1) * sizeof(DevOut)));
-    MSV_CUDA_TRY(g->d_tjobs.ensure(std::max<int64_t>(n, 1) * sizeof(msv::TraceJob)));
-    MSV_CUDA_TRY(g->d_tailjobs.ensure(std::max<int64_t>(n, 1) * sizeof(msv::TailJob)));
-    MSV_CUDA_TRY(g->d_tails.ensure(std::max<int64_t>(n, 1) * 4 * sizeof(double)));
-    MSV_CUDA_TRY(g->d_p.ensure(4 * sizeof(double)));
-    MSV_CUDA_TRY(g->d_usage.ensure(std::max<int64_t>(g->usage_total, 1) * sizeof(msv_usage)));
-    MSV_CUDA_TRY(g->d_nq.ensure(std::max<int64_t>(n, 1) * 8));
-    MSV_CUDA_TRY(g->d_tovf.ensure(std::max<int64_t>(n, 1) * 4));
-    MSV_CUDA_TRY(g->d_counter.ensure(64 * sizeof(int32_t)));
-    if (n_tails) MSV_CUDA_TRY(cudaMemcpy(g->d_p.p, tail_p, n_tails * sizeof(double), cudaMemcpyHostToDevice));
+    MSV_CUDA_TRY(g->B->d_arr.ensure(wq * 8));
+    MSV_CUDA_TRY(g->B->d_bat.ensure(wq * 4));
+    MSV_CUDA_TRY(g->B->d_next.ensure(wq * 4));
+    MSV_CUDA_TRY(g->B->d_samples.ensure(wq * 8));
+    if (records) MSV_CUDA_TRY(g->B->d_rec.ensure(wq * sizeof(msv_record)));
+    MSV_CUDA_TRY(g->B->d_scen.ensure(std::max<int64_t>(n, 1) * sizeof(DevScen)));
+    MSV_CUDA_TRY(g->B->d_out.ensure(std::max<int64_t>(n, 1) * sizeof(DevOut)));
+    MSV_CUDA_TRY(g->B->d_tjobs.ensure(std::max<int64_t>(n, 1) * sizeof(msv::TraceJob)));
+    MSV_CUDA_TRY(g->B->d_tailjobs.ensure(std::max<int64_t>(n, 1) * sizeof(msv::TailJob)));
+    MSV_CUDA_TRY(g->B->d_tails.ensure(std::max<int64_t>(n, 1) * 4 * sizeof(double)));
+    MSV_CUDA_TRY(g->B->d_p.ensure(4 * sizeof(double)));
+    MSV_CUDA_TRY(g->B->d_usage.ensure(std::max<int64_t>(g->usage_total, 1) * sizeof(msv_usage)));
+    MSV_CUDA_TRY(g->B->d_nq.ensure(std::max<int64_t>(n, 1) * 8));
+    MSV_CUDA_TRY(g->B->d_tovf.ensure(std::max<int64_t>(n, 1) * 4));
+    MSV_CUDA_TRY(g->B->d_counter.ensure(64 * sizeof(int32_t)));
+    if (n_tails) MSV_CUDA_TRY(cudaMemcpy(g->B->d_p.p, tail_p, n_tails * sizeof(double), cudaMemcpyHostToDevice));
 
     // Compact profile table of this grid (staged in shared memory by the kernel).
     std::map<int, int> grid_cell_off;
@@ -448,11 +457,11 @@ int grid_build(msv_ctx* ctx, const msv_scenario* sc, int64_t n, const double* ta
         return fail(MSV_PARAM, "grid: profiles of one call exceed the device table capacity (" +
                                    std::to_string(msv::kMaxSmemCells) + " cells)");
     g->n_cells = (int)glat.size();
-    MSV_CUDA_TRY(g->d_glat.ensure(std::max<size_t>(glat.size(), 1) * 8));
-    MSV_CUDA_TRY(g->d_gutil.ensure(std::max<size_t>(gutil.size(), 1) * 8));
+    MSV_CUDA_TRY(g->B->d_glat.ensure(std::max<size_t>(glat.size(), 1) * 8));
+    MSV_CUDA_TRY(g->B->d_gutil.ensure(std::max<size_t>(gutil.size(), 1) * 8));
     if (!glat.empty()) {
-        MSV_CUDA_TRY(cudaMemcpy(g->d_glat.p, glat.data(), glat.size() * 8, cudaMemcpyHostToDevice));
-        MSV_CUDA_TRY(cudaMemcpy(g->d_gutil.p, gutil.data(), gutil.size() * 8, cudaMemcpyHostToDevice));
+        MSV_CUDA_TRY(cudaMemcpy(g->B->d_glat.p, glat.data(), glat.size() * 8, cudaMemcpyHostToDevice));
+        MSV_CUDA_TRY(cudaMemcpy(g->B->d_gutil.p, gutil.data(), gutil.size() * 8, cudaMemcpyHostToDevice));
     }
     // Partition tables per (plan, profile) and routing masks per (plan, profile, routing).
     std::map<std::pair<int, int>, size_t> part_off;
@@ -486,12 +495,12 @@ int grid_build(msv_ctx* ctx, const msv_scenario* sc, int64_t n, const double* ta
             sc_mask[i] = mt->second;
         }
     }
-    MSV_CUDA_TRY(g->d_parts.ensure(std::max<size_t>(parts_h.size(), 1) * sizeof(DevPart)));
-    MSV_CUDA_TRY(g->d_masks.ensure(std::max<size_t>(masks_h.size(), 1) * 8));
+    MSV_CUDA_TRY(g->B->d_parts.ensure(std::max<size_t>(parts_h.size(), 1) * sizeof(DevPart)));
+    MSV_CUDA_TRY(g->B->d_masks.ensure(std::max<size_t>(masks_h.size(), 1) * 8));
     if (!parts_h.empty())
-        MSV_CUDA_TRY(cudaMemcpy(g->d_parts.p, parts_h.data(), parts_h.size() * sizeof(DevPart), cudaMemcpyHostToDevice));
+        MSV_CUDA_TRY(cudaMemcpy(g->B->d_parts.p, parts_h.data(), parts_h.size() * sizeof(DevPart), cudaMemcpyHostToDevice));
     if (!masks_h.empty())
-        MSV_CUDA_TRY(cudaMemcpy(g->d_masks.p, masks_h.data(), masks_h.size() * 8, cudaMemcpyHostToDevice));
+        MSV_CUDA_TRY(cudaMemcpy(g->B->d_masks.p, masks_h.data(), masks_h.size() * 8, cudaMemcpyHostToDevice));
 
     // Per-scenario device descriptors.
     g->h_scen.resize(n);
@@ -502,19 +511,19 @@ int grid_build(msv_ctx* ctx, const msv_scenario* sc, int64_t n, const double* ta
         const Profile& prof = ctx->profiles[s.profile];
         DevScen& d = g->h_scen[i];
         const int64_t o = g->toff[i];
-        d.arrival = g->d_arr.as<double>() + o;
-        d.batch = g->d_bat.as<int32_t>() + o;
-        d.n = g->d_nq.as<int64_t>() + i;
+        d.arrival = g->B->d_arr.as<double>() + o;
+        d.batch = g->B->d_bat.as<int32_t>() + o;
+        d.n = g->B->d_nq.as<int64_t>() + i;
         d.duration_ms = s.duration_ms;
         d.warmup_ms = s.warmup_fraction * s.duration_ms;  // engine.hpp:238
         d.sla = s.sla_ms;
         d.alpha = s.alpha;
         d.beta = s.beta;
-        d.parts = g->d_parts.as<DevPart>() + sc_part[i];
-        d.route_mask = (sc_mask[i] == (size_t)-1) ? nullptr : g->d_masks.as<uint64_t>() + sc_mask[i];
-        d.next = g->d_next.as<uint32_t>() + o;
-        d.samples = g->d_samples.as<double>() + o;
-        d.records = records ? g->d_rec.as<msv_record>() + o : nullptr;
+        d.parts = g->B->d_parts.as<DevPart>() + sc_part[i];
+        d.route_mask = (sc_mask[i] == (size_t)-1) ? nullptr : g->B->d_masks.as<uint64_t>() + sc_mask[i];
+        d.next = g->B->d_next.as<uint32_t>() + o;
+        d.samples = g->B->d_samples.as<double>() + o;
+        d.records = records ? g->B->d_rec.as<msv_record>() + o : nullptr;
         d.P = g->P[i];
         d.b_max = prof.b_max;
         d.sched = s.scheduler;
@@ -528,24 +537,24 @@ int grid_build(msv_ctx* ctx, const msv_scenario* sc, int64_t n, const double* ta
         t.cdf = g->generated ? ctx->d_cdf.as<double>() + ctx->dists[s.dist].dev_off : nullptr;
         t.b_max = g->generated ? (int32_t)ctx->dists[s.dist].cdf.size() : 0;
         t.pad = 0;
-        t.arrival = g->d_arr.as<double>() + o;
-        t.batch = g->d_bat.as<int32_t>() + o;
+        t.arrival = g->B->d_arr.as<double>() + o;
+        t.batch = g->B->d_bat.as<int32_t>() + o;
         t.cap = g->cap[i];
-        t.n_out = g->d_nq.as<int64_t>() + i;
-        t.overflow = g->d_tovf.as<int32_t>() + i;
+        t.n_out = g->B->d_nq.as<int64_t>() + i;
+        t.overflow = g->B->d_tovf.as<int32_t>() + i;
         msv::TailJob& l = lj[i];
         l.samples = d.samples;
-        l.src = g->d_out.as<DevOut>() + i;
-        l.out = g->d_tails.as<double>() + 4 * i;
+        l.src = g->B->d_out.as<DevOut>() + i;
+        l.out = g->B->d_tails.as<double>() + 4 * i;
     }
     ctx->h2d += (int64_t)(n * (sizeof(DevScen) + sizeof(msv::TraceJob) + sizeof(msv::TailJob)) +
                           parts_h.size() * sizeof(DevPart) + masks_h.size() * 8 + glat.size() * 16 +
                           n_tails * sizeof(double));
     if (n) {
-        MSV_CUDA_TRY(cudaMemcpy(g->d_scen.p, g->h_scen.data(), n * sizeof(DevScen), cudaMemcpyHostToDevice));
-        MSV_CUDA_TRY(cudaMemcpy(g->d_tjobs.p, tj.data(), n * sizeof(msv::TraceJob), cudaMemcpyHostToDevice));
-        MSV_CUDA_TRY(cudaMemcpy(g->d_tailjobs.p, lj.data(), n * sizeof(msv::TailJob), cudaMemcpyHostToDevice));
-        MSV_CUDA_TRY(cudaMemset(g->d_tovf.p, 0, n * 4));
+        MSV_CUDA_TRY(cudaMemcpy(g->B->d_scen.p, g->h_scen.data(), n * sizeof(DevScen), cudaMemcpyHostToDevice));
+        MSV_CUDA_TRY(cudaMemcpy(g->B->d_tjobs.p, tj.data(), n * sizeof(msv::TraceJob), cudaMemcpyHostToDevice));
+        MSV_CUDA_TRY(cudaMemcpy(g->B->d_tailjobs.p, lj.data(), n * sizeof(msv::TailJob), cudaMemcpyHostToDevice));
+        MSV_CUDA_TRY(cudaMemset(g->B->d_tovf.p, 0, n * 4));
     }
     // Work lists of every (wave, class).
     std::vector<int32_t> work_h;
@@ -554,9 +563,9 @@ int grid_build(msv_ctx* ctx, const msv_scenario* sc, int64_t n, const double* ta
             w.work_off.push_back((int64_t)work_h.size());
             work_h.insert(work_h.end(), c.second.begin(), c.second.end());
         }
-    MSV_CUDA_TRY(g->d_work.ensure(std::max<size_t>(work_h.size(), 1) * 4));
+    MSV_CUDA_TRY(g->B->d_work.ensure(std::max<size_t>(work_h.size(), 1) * 4));
     if (!work_h.empty())
-        MSV_CUDA_TRY(cudaMemcpy(g->d_work.p, work_h.data(), work_h.size() * 4, cudaMemcpyHostToDevice));
+        MSV_CUDA_TRY(cudaMemcpy(g->B->d_work.p, work_h.data(), work_h.size() * 4, cudaMemcpyHostToDevice));
     ctx->h2d += (int64_t)(work_h.size() * 4);
     if (!g->generated) {
         // Host traces stay resident: replay grids are a single wave.
@@ -566,14 +575,22 @@ int grid_build(msv_ctx* ctx, const msv_scenario* sc, int64_t n, const double* ta
         const int64_t q0 = offsets[0];
         const int64_t total = n ? offsets[n] - q0 : 0;
         if (total) {
-            MSV_CUDA_TRY(cudaMemcpy(g->d_arr.p, arrival + q0, total * 8, cudaMemcpyHostToDevice));
-            MSV_CUDA_TRY(cudaMemcpy(g->d_bat.p, batch + q0, total * 4, cudaMemcpyHostToDevice));
+            MSV_CUDA_TRY(cudaMemcpy(g->B->d_arr.p, arrival + q0, total * 8, cudaMemcpyHostToDevice));
+            MSV_CUDA_TRY(cudaMemcpy(g->B->d_bat.p, batch + q0, total * 4, cudaMemcpyHostToDevice));
         }
-        if (n) MSV_CUDA_TRY(cudaMemcpy(g->d_nq.p, g->host_n.data(), n * 8, cudaMemcpyHostToDevice));
+        if (n) MSV_CUDA_TRY(cudaMemcpy(g->B->d_nq.p, g->host_n.data(), n * 8, cudaMemcpyHostToDevice));
     }
     for (cudaEvent_t& e : g->ev) MSV_CUDA_TRY(cudaEventCreate(&e));
     *out = g.release();
     return MSV_OK;
+}
+
+// MSV_DEBUG_SYNC=1: synchronise and report after every kernel (diagnostics only).
+void debug_sync(cudaStream_t st, const char* what) {
+    static const bool on = getenv("MSV_DEBUG_SYNC") != nullptr;
+    if (!on) return;
+    cudaError_t e = cudaStreamSynchronize(st);
+    fprintf(stderr, "[msv] %s done: %s\n", what, cudaGetErrorString(e));
 }
 
 int grid_launch(msv_grid* g) {
@@ -586,23 +603,24 @@ int grid_launch(msv_grid* g) {
         const int64_t ns = w.s1 - w.s0;
         cudaEvent_t e1 = g->ev[1], e2 = g->ev[2], e3 = g->ev[3];
         if (g->generated) {
-            MSV_CUDA_TRY(msv::launch_trace_gen(g->d_tjobs.as<msv::TraceJob>() + w.s0, (int)ns, ctx->log1p, st));
+            MSV_CUDA_TRY(msv::launch_trace_gen(g->B->d_tjobs.as<msv::TraceJob>() + w.s0, (int)ns, ctx->log1p, st));
+            debug_sync(st, "trace_gen");
             ctx->launches += 1;
         }
         MSV_CUDA_TRY(cudaEventRecord(e1, st));
-        MSV_CUDA_TRY(cudaMemsetAsync(g->d_counter.p, 0, 64 * sizeof(int32_t), st));
+        MSV_CUDA_TRY(cudaMemsetAsync(g->B->d_counter.p, 0, 64 * sizeof(int32_t), st));
         for (size_t c = 0; c < w.classes.size(); ++c) {
             const ClassKey& k = w.classes[c].first;
             const int32_t nwork = (int32_t)w.classes[c].second.size();
             msv::SimParams p;
-            p.scen = g->d_scen.as<DevScen>();
-            p.out = g->d_out.as<DevOut>();
-            p.usage = g->d_usage.as<msv_usage>();
-            p.work = g->d_work.as<int32_t>() + w.work_off[c];
+            p.scen = g->B->d_scen.as<DevScen>();
+            p.out = g->B->d_out.as<DevOut>();
+            p.usage = g->B->d_usage.as<msv_usage>();
+            p.work = g->B->d_work.as<int32_t>() + w.work_off[c];
             p.n_work = nwork;
-            p.counter = g->d_counter.as<int32_t>() + (c % 64);
-            p.lat = g->d_glat.as<double>();
-            p.util = g->d_gutil.as<double>();
+            p.counter = g->B->d_counter.as<int32_t>() + (c % 64);
+            p.lat = g->B->d_glat.as<double>();
+            p.util = g->B->d_gutil.as<double>();
             p.n_cells = g->n_cells;
             p.any_routing = p.any_bad = p.any_check_wait = 0;
             for (int32_t si : w.classes[c].second) {
@@ -616,12 +634,14 @@ int grid_launch(msv_grid* g) {
             const int need = (nwork + segs_per_block - 1) / segs_per_block;
             const int blocks = std::max(1, std::min(need, occ * ctx->sms));
             MSV_CUDA_TRY(msv::launch_sim(k.W, k.S, k.sched, g->records, p, blocks, st));
+            debug_sync(st, "sim");
             ctx->launches += 1;
         }
         MSV_CUDA_TRY(cudaEventRecord(e2, st));
         if (!g->tail_p.empty()) {
-            MSV_CUDA_TRY(msv::launch_tail(g->d_tailjobs.as<msv::TailJob>() + w.s0, (int)ns, g->d_p.as<double>(),
+            MSV_CUDA_TRY(msv::launch_tail(g->B->d_tailjobs.as<msv::TailJob>() + w.s0, (int)ns, g->B->d_p.as<double>(),
                                           (int)g->tail_p.size(), st));
+            debug_sync(st, "tail");
             ctx->launches += 1;
         }
         MSV_CUDA_TRY(cudaEventRecord(e3, st));
@@ -661,16 +681,16 @@ int grid_results(msv_grid* g, msv_result* res, msv_usage* usage, msv_record* rec
     std::vector<int64_t> nq(n);
     std::vector<int32_t> tovf(n);
     if (n) {
-        MSV_CUDA_TRY(cudaMemcpy(outs.data(), g->d_out.p, n * sizeof(DevOut), cudaMemcpyDeviceToHost));
-        MSV_CUDA_TRY(cudaMemcpy(tails.data(), g->d_tails.p, n * 4 * sizeof(double), cudaMemcpyDeviceToHost));
-        MSV_CUDA_TRY(cudaMemcpy(nq.data(), g->d_nq.p, n * 8, cudaMemcpyDeviceToHost));
-        MSV_CUDA_TRY(cudaMemcpy(tovf.data(), g->d_tovf.p, n * 4, cudaMemcpyDeviceToHost));
+        MSV_CUDA_TRY(cudaMemcpy(outs.data(), g->B->d_out.p, n * sizeof(DevOut), cudaMemcpyDeviceToHost));
+        MSV_CUDA_TRY(cudaMemcpy(tails.data(), g->B->d_tails.p, n * 4 * sizeof(double), cudaMemcpyDeviceToHost));
+        MSV_CUDA_TRY(cudaMemcpy(nq.data(), g->B->d_nq.p, n * 8, cudaMemcpyDeviceToHost));
+        MSV_CUDA_TRY(cudaMemcpy(tovf.data(), g->B->d_tovf.p, n * 4, cudaMemcpyDeviceToHost));
         ctx->d2h += n * (int64_t)(sizeof(DevOut) + 4 * sizeof(double) + 8 + 4);
     }
     if (usage && g->usage_total)
-        MSV_CUDA_TRY(cudaMemcpy(usage, g->d_usage.p, g->usage_total * sizeof(msv_usage), cudaMemcpyDeviceToHost));
+        MSV_CUDA_TRY(cudaMemcpy(usage, g->B->d_usage.p, g->usage_total * sizeof(msv_usage), cudaMemcpyDeviceToHost));
     if (records && g->records && g->waves.size() == 1 && g->max_wave_q)
-        MSV_CUDA_TRY(cudaMemcpy(records, g->d_rec.p, g->max_wave_q * sizeof(msv_record), cudaMemcpyDeviceToHost));
+        MSV_CUDA_TRY(cudaMemcpy(records, g->B->d_rec.p, g->max_wave_q * sizeof(msv_record), cudaMemcpyDeviceToHost));
     int first_err = MSV_OK;
     int64_t first_i = -1;
     for (int64_t i = 0; i < n; ++i) {
@@ -949,7 +969,7 @@ int64_t msv_grid_queries(msv_grid* g) {
     SetDevice sd(g->ctx->device);
     if (cudaStreamSynchronize(g->ctx->stream) != cudaSuccess) return -1;
     std::vector<int64_t> nq(g->n);
-    if (g->n && cudaMemcpy(nq.data(), g->d_nq.p, g->n * 8, cudaMemcpyDeviceToHost) != cudaSuccess) return -1;
+    if (g->n && cudaMemcpy(nq.data(), g->B->d_nq.p, g->n * 8, cudaMemcpyDeviceToHost) != cudaSuccess) return -1;
     int64_t s = 0;
     for (int64_t v : nq) s += v;
     return s;
@@ -993,7 +1013,7 @@ int msv_run_grid(msv_ctx* ctx, const msv_scenario* scenarios, int64_t n, const d
     if (!ctx || (n > 0 && (!scenarios || !results))) return fail(MSV_PARAM, "null argument");
     SetDevice sd(ctx->device);
     msv_grid* g = nullptr;
-    int rc = grid_build(ctx, scenarios, n, tail_p, n_tails, nullptr, nullptr, nullptr, false, &g);
+    int rc = grid_build(ctx, scenarios, n, tail_p, n_tails, nullptr, nullptr, nullptr, false, &g, nullptr, true);
     if (rc) return rc;
     std::unique_ptr<msv_grid> guard(g);
     rc = grid_launch(g);
@@ -1053,7 +1073,7 @@ int msv_run_replay(msv_ctx* ctx, const msv_scenario* scenarios, int64_t n, const
     if (!ctx || (n > 0 && (!scenarios || !results || !offsets))) return fail(MSV_PARAM, "null argument");
     SetDevice sd(ctx->device);
     msv_grid* g = nullptr;
-    int rc = grid_build(ctx, scenarios, n, tail_p, n_tails, offsets, arrival_ms, batch, records != nullptr, &g);
+    int rc = grid_build(ctx, scenarios, n, tail_p, n_tails, offsets, arrival_ms, batch, records != nullptr, &g, nullptr, true);
     if (rc) return rc;
     std::unique_ptr<msv_grid> guard(g);
     rc = grid_launch(g);

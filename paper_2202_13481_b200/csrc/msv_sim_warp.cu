@@ -29,7 +29,7 @@ __global__ void __launch_bounds__(kSimWarpsPerBlock * 32, WarpCfg<S>::min_blocks
     double* s_util = s_lat + p.n_cells;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const size_t tab_bytes = ((size_t)2 * p.n_cells * sizeof(double) + 15) & ~(size_t)15;
-    double* q_est = reinterpret_cast<double*>(smem + tab_bytes) + (size_t)warp * (3 * S * QC * 32);
+    double* q_est = reinterpret_cast<double*>(smem + tab_bytes + (size_t)warp * (3 * S * QC * 32 * 8 + 2 * S * 32 * 4));
     double* q_arr = q_est + S * QC * 32;
     uint64_t* q_meta = reinterpret_cast<uint64_t*>(q_arr + S * QC * 32);
     for (int c = threadIdx.x; c < p.n_cells; c += blockDim.x) {
@@ -51,41 +51,43 @@ __global__ void __launch_bounds__(kSimWarpsPerBlock * 32, WarpCfg<S>::min_blocks
         uint32_t* g_next = d.next;
         double* samples = d.samples;
         msv_record* rec = d.records;
-        const double sla = d.sla, warmup = d.warmup_ms, alpha = d.alpha, beta = d.beta;
-        const bool unit_ab = alpha == 1.0 && beta == 1.0;  // 1*x == x: identical bits
+        const double sla = d.sla, warmup = d.warmup_ms;
+        const bool unit_ab = d.alpha == 1.0 && d.beta == 1.0;  // 1*x == x: identical bits
         const bool check_wait = p.any_check_wait && (d.flags & MSV_FLAG_CHECK_WAIT);
         const int bmax = d.b_max;
-        const bool routed = d.route_mask != nullptr;
+        const uint64_t* route_mask = d.route_mask;
+        const bool routed = route_mask != nullptr;
+        // overflow-list head / tail of each lane slot (rarely touched: shared memory)
+        uint32_t* g_head = reinterpret_cast<uint32_t*>(q_meta + S * QC * 32);
+        uint32_t* g_tail = g_head + S * 32;
 
         // ---- lane slots ----
         bool act[S], busy[S];
-        int32_t row[S], pid[S], kk[S], qh[S], qn[S];
-        uint32_t gh[S], gt[S], gn[S], nq[S];
+        int32_t row[S], pk[S], qh[S], qn[S];  // pk = partition id | k << 8
+        uint32_t gn[S], nq[S];
         double c_start[S], c_est[S], c_comp[S], c_arr[S], fold[S], bms[S], wbms[S];
-        uint64_t c_meta[S], rmask[S];
+        uint64_t c_meta[S];
 #pragma unroll
         for (int s = 0; s < S; ++s) {
             const int o = s * 32 + lane;
             act[s] = o < d.P;
             row[s] = -1;
-            pid[s] = kk[s] = 0;
-            rmask[s] = 0;
+            pk[s] = 0;
             if (act[s]) {
                 const DevPart dp = d.parts[o];
-                pid[s] = dp.pid;
-                kk[s] = dp.k;
+                pk[s] = dp.pid | (dp.k << 8);
                 row[s] = dp.row;
-                if (routed) rmask[s] = d.route_mask[o];
             }
             busy[s] = false;
             qh[s] = qn[s] = 0;
-            gh[s] = gt[s] = gn[s] = nq[s] = 0;
+            gn[s] = nq[s] = 0;
             c_start[s] = c_est[s] = c_comp[s] = c_arr[s] = 0.0;
             fold[s] = 0.0;  // < 0: must be recomputed
             bms[s] = wbms[s] = 0.0;
             c_meta[s] = 0;
         }
         uint32_t viol = 0, mviol = 0;
+        uint32_t khi_min = ~0u, khi_max = 0;  // coarse key range of the samples, for K3
         uint64_t hash = 0;
         double wdiff = 0.0;
         int m0 = -1, status = 0;
@@ -108,8 +110,11 @@ __global__ void __launch_bounds__(kSimWarpsPerBlock * 32, WarpCfg<S>::min_blocks
                     if (c_arr[s] >= warmup) {
                         mviol += met ? 0u : 1u;
                         samples[(uint32_t)q - (uint32_t)m0] = lat;
+                        const uint32_t kh = (uint32_t)(msv_dbits(lat) >> 32) | 0x80000000u;  // order key, high word
+                        khi_min = kh < khi_min ? kh : khi_min;
+                        khi_max = kh > khi_max ? kh : khi_max;
                     }
-                    hash += msv_query_digest(q, pid[s], c_start[s], now);
+                    hash += msv_query_digest(q, pk[s] & 0xff, c_start[s], now);
                     if (REC) {
                         rec[q].start_ms = c_start[s];
                         rec[q].finish_ms = now;
@@ -122,8 +127,8 @@ __global__ void __launch_bounds__(kSimWarpsPerBlock * 32, WarpCfg<S>::min_blocks
                         qh[s] = (qh[s] + 1) & (QC - 1);
                         qn[s] -= 1;
                         if (gn[s] > 0) {  // refill the ring from the overflow list
-                            const uint32_t g = gh[s];
-                            gh[s] = g_next[g];
+                            const uint32_t g = g_head[s * 32 + lane];
+                            g_head[s * 32 + lane] = g_next[g];
                             gn[s] -= 1;
                             const int32_t gb = g_bat[g];
                             const int e2 = (s * QC + ((qh[s] + qn[s]) & (QC - 1))) * 32 + lane;
@@ -180,7 +185,7 @@ __global__ void __launch_bounds__(kSimWarpsPerBlock * 32, WarpCfg<S>::min_blocks
                     unsigned anyc = 0;
 #pragma unroll
                     for (int s = 0; s < S; ++s) {
-                        cand[s] = act[s] && (((rmask[s] >> (b - 1)) & 1ull) != 0);
+                        cand[s] = act[s] && (((route_mask[s * 32 + lane] >> (b - 1)) & 1ull) != 0);
                         anyc |= __ballot_sync(kFull, cand[s]);
                     }
                     if (anyc == 0) {
@@ -203,7 +208,7 @@ __global__ void __launch_bounds__(kSimWarpsPerBlock * 32, WarpCfg<S>::min_blocks
                         if (fold[s] < 0.0) {  // exact left fold of the FIFO (sched.hpp:78-79)
                             double acc = 0.0;
                             for (int k = 0; k < qn[s]; ++k) acc = acc + q_est[(s * QC + ((qh[s] + k) & (QC - 1))) * 32 + lane];
-                            uint32_t g = gh[s];
+                            uint32_t g = g_head[s * 32 + lane];
                             for (uint32_t k = 0; k < gn[s]; ++k) {
                                 acc = acc + s_lat[row[s] + g_bat[g] - 1];
                                 g = g_next[g];
@@ -236,7 +241,7 @@ __global__ void __launch_bounds__(kSimWarpsPerBlock * 32, WarpCfg<S>::min_blocks
                     for (int s = S - 1; s >= 0; --s) {
                         const bool ok = cand[s] && row[s] >= 0;
                         const bool pred =
-                            ok && (unit_ab ? (sla > wv[s] + est_n[s]) : (sla > alpha * (wv[s] + beta * est_n[s])));
+                            ok && (unit_ab ? (sla > wv[s] + est_n[s]) : (sla > d.alpha * (wv[s] + d.beta * est_n[s])));
                         const unsigned bA = __ballot_sync(kFull, pred);
                         if (bA) ch = s * 32 + __ffs(bA) - 1;
                     }
@@ -268,7 +273,7 @@ __global__ void __launch_bounds__(kSimWarpsPerBlock * 32, WarpCfg<S>::min_blocks
 #pragma unroll
                     for (int s = 0; s < S; ++s) {
                         const uint32_t key =
-                            (cand[s] && !busy[s]) ? (((0x7FFFu - (uint32_t)kk[s]) << 16) | (uint32_t)pid[s]) : ~0u;
+                            (cand[s] && !busy[s]) ? (((0x7FFFu - ((uint32_t)pk[s] >> 8)) << 16) | ((uint32_t)pk[s] & 0xffu)) : ~0u;
                         mi = key < mi ? key : mi;
                     }
                     mi = __reduce_min_sync(kFull, mi);
@@ -277,14 +282,14 @@ __global__ void __launch_bounds__(kSimWarpsPerBlock * 32, WarpCfg<S>::min_blocks
                         kind = MSV_IDLE_LARGEST;
                         // the key encodes (k, id): its owner is the lane slot with that pid
 #pragma unroll
-                        for (int s = 0; s < S; ++s) key2[s] = (cand[s] && !busy[s]) ? (((0x7FFFu - (uint32_t)kk[s]) << 16) | (uint32_t)pid[s]) : ~0u;
+                        for (int s = 0; s < S; ++s) key2[s] = (cand[s] && !busy[s]) ? (((0x7FFFu - ((uint32_t)pk[s] >> 8)) << 16) | ((uint32_t)pk[s] & 0xffu)) : ~0u;
                     } else {
                         kind = MSV_SHORTEST_QUEUE;
                         uint32_t mq = ~0u;
 #pragma unroll
                         for (int s = 0; s < S; ++s) {
                             const uint32_t len = (uint32_t)qn[s] + gn[s];
-                            key2[s] = cand[s] ? (((len < 0xFFFFFFu ? len : 0xFFFFFFu) << 8) | (uint32_t)pid[s]) : ~0u;
+                            key2[s] = cand[s] ? (((len < 0xFFFFFFu ? len : 0xFFFFFFu) << 8) | ((uint32_t)pk[s] & 0xffu)) : ~0u;
                             mq = key2[s] < mq ? key2[s] : mq;
                         }
                         mi = __reduce_min_sync(kFull, mq);
@@ -324,15 +329,15 @@ __global__ void __launch_bounds__(kSimWarpsPerBlock * 32, WarpCfg<S>::min_blocks
                                 q_meta[e] = (uint64_t)i | ((uint64_t)b << 40);
                                 qn[s] += 1;
                             } else {
-                                if (gn[s] == 0) gh[s] = (uint32_t)i;
-                                else g_next[gt[s]] = (uint32_t)i;
-                                gt[s] = (uint32_t)i;
+                                if (gn[s] == 0) g_head[s * 32 + lane] = (uint32_t)i;
+                                else g_next[g_tail[s * 32 + lane]] = (uint32_t)i;
+                                g_tail[s * 32 + lane] = (uint32_t)i;
                                 gn[s] += 1;
                             }
                             if (fold[s] >= 0.0) fold[s] = fold[s] + est;
                         }
                         if (REC) {
-                            rec[i].partition = pid[s];
+                            rec[i].partition = pk[s] & 0xff;
                             rec[i].kind = kind;
                         }
                     }
@@ -351,6 +356,8 @@ __global__ void __launch_bounds__(kSimWarpsPerBlock * 32, WarpCfg<S>::min_blocks
         const uint64_t hsum = seg_sum_u64<32>(hash, kFull);
         lf = seg_max_f64<32>(lf, kFull);
         const double wd = seg_max_f64<32>(wdiff, kFull);
+        khi_min = __reduce_min_sync(kFull, khi_min);
+        khi_max = __reduce_max_sync(kFull, khi_max);
         if (lane == 0) {
             DevOut o;
             o.violations = (int64_t)v0;
@@ -360,8 +367,8 @@ __global__ void __launch_bounds__(kSimWarpsPerBlock * 32, WarpCfg<S>::min_blocks
             o.horizon_ms = (d.duration_ms < lf) ? lf : d.duration_ms;  // engine.hpp:237
             o.max_wait_diff = wd;
             o.hash = hsum;
-            o.lat_min_bits = ~0ull;  // K3 derives the key range
-            o.lat_max_bits = 0;
+            o.lat_min_bits = (uint64_t)khi_min << 32;  // bounds every sample's order key
+            o.lat_max_bits = ((uint64_t)khi_max << 32) | 0xffffffffull;
             o.status = status;
             o.pad = 0;
             p.out[sidx] = o;
@@ -374,7 +381,7 @@ __global__ void __launch_bounds__(kSimWarpsPerBlock * 32, WarpCfg<S>::min_blocks
                     u.busy_ms = bms[s];
                     u.weighted_busy_ms = wbms[s];
                     u.queries = nq[s];
-                    p.usage[d.usage_off + pid[s]] = u;
+                    p.usage[d.usage_off + (pk[s] & 0xff)] = u;
                 }
             }
         }
@@ -400,7 +407,8 @@ void* sim_warp_fn(int S, int sched, bool rec) {
 size_t sim_warp_smem_bytes(int S, int n_cells) {
     const int qc = S == 1 ? 8 : (S == 2 ? 4 : 2);
     const size_t tab = ((size_t)2 * n_cells * sizeof(double) + 15) & ~(size_t)15;
-    return tab + (size_t)kSimWarpsPerBlock * 3 * S * qc * 32 * sizeof(double);
+    // per warp: rings (est, arr, meta) + overflow head/tail per lane slot
+    return tab + (size_t)kSimWarpsPerBlock * (3 * S * qc * 32 * sizeof(double) + 2 * S * 32 * sizeof(uint32_t));
 }
 
 }  // namespace msv
