@@ -1,0 +1,96 @@
+"""Multi-GPU scenario sharding: one process per GPU (torch.distributed), each rank
+simulates a cost-balanced contiguous shard of the scenario list on its own device
+(no data-path collective), then one all-gather of fixed-size per-scenario results
+(NCCL over NVLink on GPUs; gloo in the CPU tests) gives every rank the whole grid,
+from which each rank takes the same deterministic PARIS argmin.
+"""
+from __future__ import annotations
+
+from typing import Callable, Sequence
+
+import numpy as np
+
+from .workloads import shard
+
+# Per-scenario record exchanged between ranks (float64 lanes; integers < 2^53).
+FIELDS = ("total", "violations", "measured", "measured_violations", "p95", "p99", "horizon_ms", "hash_hi",
+          "hash_lo", "status")
+
+
+def pack(res: dict) -> np.ndarray:
+    """Engine.run_grid result dict -> (n, len(FIELDS)) float64 rows."""
+    n = len(res["total"])
+    out = np.zeros((n, len(FIELDS)))
+    out[:, 0] = res["total"]
+    out[:, 1] = res["violations"]
+    out[:, 2] = res["measured"]
+    out[:, 3] = res["measured_violations"]
+    tail = np.asarray(res["tail"])
+    out[:, 4] = tail[:, 0] if tail.shape[1] > 0 else np.nan
+    out[:, 5] = tail[:, 1] if tail.shape[1] > 1 else np.nan
+    out[:, 6] = res["horizon_ms"]
+    h = np.asarray(res["placement_hash"], dtype=np.uint64)
+    out[:, 7] = (h >> np.uint64(32)).astype(np.float64)
+    out[:, 8] = (h & np.uint64(0xFFFFFFFF)).astype(np.float64)
+    out[:, 9] = res["status"]
+    return out
+
+
+def unpack(rows: np.ndarray) -> dict:
+    h = (rows[:, 7].astype(np.uint64) << np.uint64(32)) | rows[:, 8].astype(np.uint64)
+    return {"total": rows[:, 0].astype(np.int64), "violations": rows[:, 1].astype(np.int64),
+            "measured": rows[:, 2].astype(np.int64), "measured_violations": rows[:, 3].astype(np.int64),
+            "tail": rows[:, 4:6].copy(), "horizon_ms": rows[:, 6].copy(), "placement_hash": h,
+            "status": rows[:, 9].astype(np.int32)}
+
+
+def shard_bounds(specs: Sequence, world: int) -> list[tuple[int, int]]:
+    """[lo, hi) of every rank's shard (the same cut `workloads.shard` makes)."""
+    bounds, lo = [], 0
+    for r in range(world):
+        n = len(shard(list(specs), r, world))
+        bounds.append((lo, lo + n))
+        lo += n
+    return bounds
+
+
+def run_sharded(specs: Sequence, run_local: Callable[[list], dict], rank: int, world: int, device=None) -> dict:
+    """Run this rank's shard with `run_local` (e.g. Engine.run_grid) and all-gather every
+    rank's rows in global scenario order."""
+    import torch
+    import torch.distributed as td
+    bounds = shard_bounds(specs, world)
+    lo, hi = bounds[rank]
+    local = pack(run_local(list(specs[lo:hi]))) if hi > lo else np.zeros((0, len(FIELDS)))
+    if world == 1:
+        return unpack(local)
+    width = max(h - l for l, h in bounds)
+    buf = np.full((width, len(FIELDS)), np.nan)
+    buf[: hi - lo] = local
+    t = torch.from_numpy(buf)
+    if device is not None:
+        t = t.to(device)
+    parts = [torch.empty_like(t) for _ in range(world)]
+    td.all_gather(parts, t)
+    rows = np.concatenate([p.cpu().numpy()[: h - l] for p, (l, h) in zip(parts, bounds)])
+    return unpack(rows)
+
+
+def paris_argmin(p99: np.ndarray, n_candidates: int, seeds_per_candidate: int) -> tuple[int, np.ndarray]:
+    """Mean p99 per candidate (seed-major rows in candidate order, NaN-free seeds only,
+    summed in seed order like mean_tail_at_rate, metrics.hpp:61-74) and the argmin;
+    ties break toward the lowest candidate index."""
+    p = np.asarray(p99, float).reshape(n_candidates, seeds_per_candidate)
+    means = np.empty(n_candidates)
+    for c in range(n_candidates):
+        s, used = 0.0, 0
+        for v in p[c]:
+            if v == v:
+                s += float(v)
+                used += 1
+        means[c] = s / used if used else np.inf
+    best = 0
+    for c in range(1, n_candidates):
+        if means[c] < means[best]:
+            best = c
+    return best, means

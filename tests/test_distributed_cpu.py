@@ -1,0 +1,81 @@
+"""Multi-process host logic of the multi-GPU path on CPU: world_size 2 over gloo.
+Each rank runs its shard (here through the CPU oracle port, standing in for the
+device), all-gathers, and must end with the full grid identical to a single-process
+run plus the same PARIS argmin on both ranks."""
+from __future__ import annotations
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch.multiprocessing as mp
+
+
+def _free_port() -> int:
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _specs():
+    from paper_2202_13481_b200 import workloads as W
+    m = W.model("bert_base")
+    cands = W.fleet_candidates(1)[:6]  # six 1-GPU fleets
+    rate = 0.6 * W.capacity_qps(m, W.paris(m, 1))
+    return [W._spec(m, p, rate, 1500, 1 + s) for p in cands for s in range(3)], len(cands)
+
+
+def _worker(rank, world, port, out_q):
+    import torch.distributed as td
+    from paper_2202_13481_b200.distributed import paris_argmin, run_sharded
+    from tests import oracle_py as O
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    td.init_process_group("gloo", rank=rank, world_size=world)
+    specs, n_c = _specs()
+    port_oracle = O.Oracle("port")
+    res = run_sharded(specs, lambda sub: port_oracle.run_grid(sub, (0.95, 0.99), threads=1), rank, world)
+    best, means = paris_argmin(res["tail"][:, 1], n_c, 3)
+    out_q.put((rank, res["placement_hash"].tolist(), res["tail"].tolist(), best))
+    td.barrier()
+    td.destroy_process_group()
+
+
+def test_sharded_gather_matches_single_process():
+    from paper_2202_13481_b200.distributed import paris_argmin
+    from tests import oracle_py as O
+    specs, n_c = _specs()
+    ref = O.Oracle("port").run_grid(specs, (0.95, 0.99), threads=1)
+    ref_best, _ = paris_argmin(ref["tail"][:, 1], n_c, 3)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    got = [q.get(timeout=300) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for rank, hashes, tails, best in got:
+        assert hashes == ref["placement_hash"].tolist()
+        assert np.array_equal(np.array(tails), ref["tail"])
+        assert best == ref_best
+
+
+def test_shard_bounds_cover_in_order():
+    from paper_2202_13481_b200.distributed import shard_bounds
+    specs, _ = _specs()
+    for world in (1, 2, 3, 8):
+        b = shard_bounds(specs, world)
+        assert b[0][0] == 0 and b[-1][1] == len(specs)
+        assert all(b[i][1] == b[i + 1][0] for i in range(world - 1))
+
+
+def test_paris_argmin_ties_and_empty_seeds():
+    from paper_2202_13481_b200.distributed import paris_argmin
+    p99 = np.array([3.0, 3.0, 2.0, np.nan, 2.0, 2.0, 1.5, 2.5, 2.0])
+    best, means = paris_argmin(p99, 3, 3)
+    assert means[1] == 2.0 and means[2] == 2.0 and best == 1
