@@ -74,6 +74,7 @@ struct Profile {
 struct Dist {
     std::vector<double> pmf, cdf;
     size_t dev_off = 0;
+    size_t guide_off = 0;
 };
 
 struct Plan {
@@ -135,13 +136,14 @@ struct msv_ctx {
     std::vector<Plan> plans;
     std::vector<Routing> routings;
     // concatenated profile cells / cdfs on the device
-    DevBuf d_lat, d_util, d_cdf;
+    DevBuf d_lat, d_util, d_cdf, d_guide;
     int n_cells = 0;
     bool tables_dirty = true;
 
     int sync_tables() {
         if (!tables_dirty) return MSV_OK;
         std::vector<double> lat, util, cdf;
+        std::vector<int16_t> guide;
         for (Profile& p : profiles) {
             p.cell_off = (int)lat.size();
             lat.insert(lat.end(), p.lat.begin(), p.lat.end());
@@ -150,6 +152,15 @@ struct msv_ctx {
         for (Dist& d : dists) {
             d.dev_off = cdf.size();
             cdf.insert(cdf.end(), d.cdf.begin(), d.cdf.end());
+            // guide[j] = first i with !(cdf[i] < j/G): lower_bound's answer for u = j/G,
+            // a valid start for every u >= j/G (the cdf is nondecreasing).
+            d.guide_off = guide.size();
+            for (int j = 0; j < msv::kGuide; ++j) {
+                const double uj = (double)j / (double)msv::kGuide;
+                size_t i = 0;
+                while (i < d.cdf.size() && d.cdf[i] < uj) ++i;
+                guide.push_back((int16_t)i);
+            }
         }
         n_cells = (int)lat.size();
         MSV_CUDA_TRY(d_lat.ensure(std::max<size_t>(lat.size(), 1) * 8));
@@ -160,6 +171,9 @@ struct msv_ctx {
             MSV_CUDA_TRY(cudaMemcpy(d_util.p, util.data(), util.size() * 8, cudaMemcpyHostToDevice));
         }
         if (!cdf.empty()) MSV_CUDA_TRY(cudaMemcpy(d_cdf.p, cdf.data(), cdf.size() * 8, cudaMemcpyHostToDevice));
+        MSV_CUDA_TRY(d_guide.ensure(std::max<size_t>(guide.size(), 1) * 2));
+        if (!guide.empty())
+            MSV_CUDA_TRY(cudaMemcpy(d_guide.p, guide.data(), guide.size() * 2, cudaMemcpyHostToDevice));
         tables_dirty = false;
         return MSV_OK;
     }
@@ -535,6 +549,7 @@ int grid_build(msv_ctx* ctx, const msv_scenario* sc, int64_t n, const double* ta
         t.rate_per_ms = s.rate_qps / 1000.0;  // workload.hpp:103
         t.duration_ms = s.duration_ms;
         t.cdf = g->generated ? ctx->d_cdf.as<double>() + ctx->dists[s.dist].dev_off : nullptr;
+        t.guide = g->generated ? ctx->d_guide.as<int16_t>() + ctx->dists[s.dist].guide_off : nullptr;
         t.b_max = g->generated ? (int32_t)ctx->dists[s.dist].cdf.size() : 0;
         t.pad = 0;
         t.arrival = g->B->d_arr.as<double>() + o;
@@ -628,7 +643,8 @@ int grid_launch(msv_grid* g) {
                 if (g->bad[si]) p.any_bad = 1;
                 if (g->scen[si].flags & MSV_FLAG_CHECK_WAIT) p.any_check_wait = 1;
             }
-            const int occ = msv::sim_max_blocks_per_sm(k.W, k.S, k.sched, g->records, g->n_cells);
+            const bool full = g->records || p.any_routing || p.any_bad || p.any_check_wait;
+            const int occ = msv::sim_max_blocks_per_sm(k.W, k.S, k.sched, g->records, full, g->n_cells);
             if (occ <= 0) return fail(MSV_CUDA, "sim kernel: no occupancy for class");
             const int segs_per_block = msv::kSimWarpsPerBlock * (32 / k.W);
             const int need = (nwork + segs_per_block - 1) / segs_per_block;
@@ -1103,6 +1119,7 @@ int msv_sample_trace(msv_ctx* ctx, int32_t dist, double rate_qps, double duratio
     j.rate_per_ms = rate_qps / 1000.0;
     j.duration_ms = duration_ms;
     j.cdf = ctx->d_cdf.as<double>() + ctx->dists[dist].dev_off;
+    j.guide = ctx->d_guide.as<int16_t>() + ctx->dists[dist].guide_off;
     j.b_max = (int32_t)ctx->dists[dist].cdf.size();
     j.pad = 0;
     j.arrival = d_arr.as<double>();

@@ -18,8 +18,10 @@ constexpr int kQCap = 8;
 constexpr int kMaxSmemCells = 1024;
 constexpr int kSimWarpsPerBlock = 4;
 constexpr int kTraceWarpsPerBlock = 4;
-constexpr int kTailThreads = 256;
+constexpr int kTailThreads = 512;
 constexpr int kTailSmemCap = 2048;  // values gathered for the final in-smem select
+// Guide table of BatchDistribution::sample: u in [j/G, (j+1)/G) starts its lower_bound at guide[j].
+constexpr int kGuide = 256;
 // Internal status: generated trace exceeded its capacity, host re-runs with a larger one.
 constexpr int kStatusRetryTrace = 101;
 
@@ -91,6 +93,7 @@ struct TraceJob {
     double rate_per_ms;   // rate_qps / 1000.0 (workload.hpp:103)
     double duration_ms;
     const double* cdf;    // BatchDistribution cdf (device)
+    const int16_t* guide; // kGuide entries: first index with cdf >= j / kGuide
     int32_t b_max;
     int32_t pad;
     double* arrival;      // out
@@ -140,7 +143,7 @@ cudaError_t launch_trace_gen(const TraceJob* d_jobs, int n_jobs, int log1p_varia
 cudaError_t launch_sim(int W, int S, int sched, bool records, const SimParams& p, int blocks,
                        cudaStream_t stream);
 size_t sim_smem_bytes(int W, int S, int n_cells);
-int sim_max_blocks_per_sm(int W, int S, int sched, bool records, int n_cells);
+int sim_max_blocks_per_sm(int W, int S, int sched, bool records, bool full, int n_cells);
 cudaError_t launch_tail(const TailJob* d_jobs, int n_jobs, const double* d_p, int n_p,
                         cudaStream_t stream);
 cudaError_t launch_dispatch(const DispatchParams& p, cudaStream_t stream);

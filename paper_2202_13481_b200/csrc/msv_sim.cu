@@ -508,7 +508,7 @@ void* pick_sim(int W, int S, int sched, bool rec) {
 
 }  // namespace
 
-void* sim_warp_fn(int S, int sched, bool rec);       // msv_sim_warp.cu
+void* sim_warp_fn(int S, int sched, bool rec, bool full);  // msv_sim_warp.cu
 size_t sim_warp_smem_bytes(int S, int n_cells);
 
 size_t sim_smem_bytes(int W, int S, int n_cells) {
@@ -517,12 +517,12 @@ size_t sim_smem_bytes(int W, int S, int n_cells) {
     return tab + (size_t)kSimWarpsPerBlock * 3 * S * kQCap * 32 * sizeof(double);
 }
 
-static void* sim_fn_for(int W, int S, int sched, bool rec) {
-    return W == 32 ? sim_warp_fn(S, sched, rec) : pick_sim(W, S, sched, rec);
+static void* sim_fn_for(int W, int S, int sched, bool rec, bool full) {
+    return W == 32 ? sim_warp_fn(S, sched, rec, full) : pick_sim(W, S, sched, rec);
 }
 
-int sim_max_blocks_per_sm(int W, int S, int sched, bool records, int n_cells) {
-    void* fn = sim_fn_for(W, S, sched, records);
+int sim_max_blocks_per_sm(int W, int S, int sched, bool records, bool full, int n_cells) {
+    void* fn = sim_fn_for(W, S, sched, records, full);
     if (!fn) return 0;
     const size_t smem = sim_smem_bytes(W, S, n_cells);
     if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) return 0;
@@ -533,7 +533,8 @@ int sim_max_blocks_per_sm(int W, int S, int sched, bool records, int n_cells) {
 }
 
 cudaError_t launch_sim(int W, int S, int sched, bool records, const SimParams& p, int blocks, cudaStream_t stream) {
-    void* fn = sim_fn_for(W, S, sched, records);
+    const bool full = records || p.any_routing || p.any_bad || p.any_check_wait;
+    void* fn = sim_fn_for(W, S, sched, records, full);
     if (!fn) return cudaErrorInvalidValue;
     const size_t smem = sim_smem_bytes(W, S, p.n_cells);
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

@@ -1,11 +1,22 @@
 // K2 for plans of 17..128 partitions: sim_warp_kernel — one scenario per warp.
 //
 // Same semantics as msv_sim.cu (see its header for the per-arrival protocol) with
-// the warp-uniform structure this class allows: scenario -> 32-arrival window ->
-// arrival loops with no per-arrival bookkeeping; the window's first measured
-// arrival is one ballot; Step B's 64-bit argmin is two REDUX.MIN; the horizon is
-// the last completion each lane retained. Lane slot s of lane l owns by_ascending_size
-// order index s*32 + l (sched.hpp:96-104).
+// the warp-uniform structure this class allows:
+//   * scenario -> 32-arrival window -> arrival loops, no per-arrival bookkeeping;
+//     each window is staged in shared memory and broadcast by LDS;
+//   * the window's first measured arrival is one ballot;
+//   * Step A = ballot + first set bit; Step B's 64-bit argmin = two REDUX.MIN;
+//     FIFS = REDUX.MIN over (k, id) / (queue length, id) keys;
+//   * the FIFO fold of Eq. 1 is kept exact at all times: extended on append and
+//     recomputed in FIFO order when the head leaves (ELSA), so a dispatch is
+//     branch-free: w = fold + max(0, est - (now - start));
+//   * template flags: UNIT (alpha = beta = 1, per scenario: 1*x == x bit for bit)
+//     and FULL (segment routing / sizes missing from the profile / wait-consistency
+//     check present in the launch; the plain variant carries none of their votes);
+//   * the horizon is the last completion each lane retained.
+// Lane slot s of lane l owns by_ascending_size order index s*32 + l (sched.hpp:96-104).
+#include <type_traits>
+
 #include "msv_device.cuh"
 
 namespace msv {
@@ -20,18 +31,30 @@ struct WarpCfg {
     static constexpr int min_blocks = S == 1 ? 5 : (S == 2 ? 4 : 2);
 };
 
-template <int S, int SCHED, bool REC>
+// Per-warp shared-memory layout (after the block's profile table).
+template <int S>
+struct WarpSmem {
+    static constexpr int QC = WarpCfg<S>::qcap;
+    double q_est[S][QC][32];
+    double q_arr[S][QC][32];
+    uint64_t q_meta[S][QC][32];
+    double win_t[32];
+    int32_t win_b[32];
+    uint32_t g_head[S][32];  // overflow list head / tail per lane slot
+    uint32_t g_tail[S][32];
+};
+
+template <int S, int SCHED, bool REC, bool FULL>
 __global__ void __launch_bounds__(kSimWarpsPerBlock * 32, WarpCfg<S>::min_blocks)
     sim_warp_kernel(const SimParams p) {
     constexpr int QC = WarpCfg<S>::qcap;
+    constexpr bool kFold = (SCHED == MSV_ELSA) || FULL;  // Eq. 1 needed (ELSA, or the check)
     extern __shared__ __align__(16) unsigned char smem[];
     double* s_lat = reinterpret_cast<double*>(smem);
     double* s_util = s_lat + p.n_cells;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const size_t tab_bytes = ((size_t)2 * p.n_cells * sizeof(double) + 15) & ~(size_t)15;
-    double* q_est = reinterpret_cast<double*>(smem + tab_bytes + (size_t)warp * (3 * S * QC * 32 * 8 + 2 * S * 32 * 4));
-    double* q_arr = q_est + S * QC * 32;
-    uint64_t* q_meta = reinterpret_cast<uint64_t*>(q_arr + S * QC * 32);
+    WarpSmem<S>& W = reinterpret_cast<WarpSmem<S>*>(smem + tab_bytes)[warp];
     for (int c = threadIdx.x; c < p.n_cells; c += blockDim.x) {
         s_lat[c] = p.lat[c];
         s_util[c] = p.util[c];
@@ -52,14 +75,9 @@ __global__ void __launch_bounds__(kSimWarpsPerBlock * 32, WarpCfg<S>::min_blocks
         double* samples = d.samples;
         msv_record* rec = d.records;
         const double sla = d.sla, warmup = d.warmup_ms;
-        const bool unit_ab = d.alpha == 1.0 && d.beta == 1.0;  // 1*x == x: identical bits
-        const bool check_wait = p.any_check_wait && (d.flags & MSV_FLAG_CHECK_WAIT);
+        const bool check_wait = FULL && p.any_check_wait && (d.flags & MSV_FLAG_CHECK_WAIT);
         const int bmax = d.b_max;
         const uint64_t* route_mask = d.route_mask;
-        const bool routed = route_mask != nullptr;
-        // overflow-list head / tail of each lane slot (rarely touched: shared memory)
-        uint32_t* g_head = reinterpret_cast<uint32_t*>(q_meta + S * QC * 32);
-        uint32_t* g_tail = g_head + S * 32;
 
         // ---- lane slots ----
         bool act[S], busy[S];
@@ -71,7 +89,7 @@ __global__ void __launch_bounds__(kSimWarpsPerBlock * 32, WarpCfg<S>::min_blocks
         for (int s = 0; s < S; ++s) {
             const int o = s * 32 + lane;
             act[s] = o < d.P;
-            row[s] = -1;
+            row[s] = 0;  // inactive lanes read a valid (ignored) cell
             pk[s] = 0;
             if (act[s]) {
                 const DevPart dp = d.parts[o];
@@ -82,7 +100,7 @@ __global__ void __launch_bounds__(kSimWarpsPerBlock * 32, WarpCfg<S>::min_blocks
             qh[s] = qn[s] = 0;
             gn[s] = nq[s] = 0;
             c_start[s] = c_est[s] = c_comp[s] = c_arr[s] = 0.0;
-            fold[s] = 0.0;  // < 0: must be recomputed
+            fold[s] = 0.0;
             bms[s] = wbms[s] = 0.0;
             c_meta[s] = 0;
         }
@@ -91,6 +109,20 @@ __global__ void __launch_bounds__(kSimWarpsPerBlock * 32, WarpCfg<S>::min_blocks
         uint64_t hash = 0;
         double wdiff = 0.0;
         int m0 = -1, status = 0;
+
+        // Exact left fold of slot s's FIFO (sched.hpp:78-79): ring part, then overflow list.
+        auto refold = [&](int s) {
+            double acc = 0.0;
+            for (int k = 0; k < qn[s]; ++k) acc = acc + W.q_est[s][(qh[s] + k) & (QC - 1)][lane];
+            if (gn[s] > 0) {
+                uint32_t g = W.g_head[s][lane];
+                for (uint32_t k = 0; k < gn[s]; ++k) {
+                    acc = acc + s_lat[row[s] + g_bat[g] - 1];
+                    g = g_next[g];
+                }
+            }
+            return acc;
+        };
 
         // Retire every completion of this lane with time <= t, in chain order.
         auto drain = [&](double t) {
@@ -120,27 +152,27 @@ __global__ void __launch_bounds__(kSimWarpsPerBlock * 32, WarpCfg<S>::min_blocks
                         rec[q].finish_ms = now;
                     }
                     if (qn[s] > 0) {  // start the queue head now (engine.hpp:181-185)
-                        const int e = (s * QC + qh[s]) * 32 + lane;
-                        const double est = q_est[e];
-                        c_arr[s] = q_arr[e];
-                        c_meta[s] = q_meta[e];
-                        qh[s] = (qh[s] + 1) & (QC - 1);
+                        const int h = qh[s];
+                        const double est = W.q_est[s][h][lane];
+                        c_arr[s] = W.q_arr[s][h][lane];
+                        c_meta[s] = W.q_meta[s][h][lane];
+                        qh[s] = (h + 1) & (QC - 1);
                         qn[s] -= 1;
                         if (gn[s] > 0) {  // refill the ring from the overflow list
-                            const uint32_t g = g_head[s * 32 + lane];
-                            g_head[s * 32 + lane] = g_next[g];
+                            const uint32_t g = W.g_head[s][lane];
+                            W.g_head[s][lane] = g_next[g];
                             gn[s] -= 1;
                             const int32_t gb = g_bat[g];
-                            const int e2 = (s * QC + ((qh[s] + qn[s]) & (QC - 1))) * 32 + lane;
-                            q_est[e2] = s_lat[row[s] + gb - 1];
-                            q_arr[e2] = g_arr[g];
-                            q_meta[e2] = (uint64_t)g | ((uint64_t)gb << 40);
+                            const int e2 = (qh[s] + qn[s]) & (QC - 1);
+                            W.q_est[s][e2][lane] = s_lat[row[s] + gb - 1];
+                            W.q_arr[s][e2][lane] = g_arr[g];
+                            W.q_meta[s][e2][lane] = (uint64_t)g | ((uint64_t)gb << 40);
                             qn[s] += 1;
                         }
                         c_start[s] = now;
                         c_est[s] = est;
                         c_comp[s] = now + est;
-                        fold[s] = qn[s] == 0 ? 0.0 : -1.0;
+                        if (kFold) fold[s] = refold(s);
                     } else {
                         busy[s] = false;
                         fold[s] = 0.0;
@@ -149,201 +181,194 @@ __global__ void __launch_bounds__(kSimWarpsPerBlock * 32, WarpCfg<S>::min_blocks
             }
         };
 
-        double nx_t = lane < n ? g_arr[lane] : 0.0;
-        int nx_b = lane < n ? g_bat[lane] : 0;
-        for (int base = 0; base < n && status == 0; base += 32) {
-            const double win_t = nx_t;
-            const int win_b = nx_b;
-            if (base + 32 + lane < n) {
-                nx_t = g_arr[base + 32 + lane];
-                nx_b = g_bat[base + 32 + lane];
-            }
-            if (m0 < 0) {  // first arrival >= warmup (arrivals are sorted; engine.hpp:262)
-                const unsigned mb = __ballot_sync(kFull, base + lane < n && win_t >= warmup);
-                if (mb) m0 = base + __ffs(mb) - 1;
-            }
-            const int cnt = min(32, n - base);
-            for (int j = 0; j < cnt; ++j) {
-                const double t = __shfl_sync(kFull, win_t, j);
-                const int b = __shfl_sync(kFull, win_b, j);
-                const int i = base + j;
-                drain(t);
-                if (b < 1 || b > bmax) {  // LookupError at this query (profile.hpp:127-129)
-                    status = MSV_LOOKUP;
-                    break;
+        // One scenario's arrival stream; UNIT: alpha == beta == 1.
+        auto simulate = [&](auto unit_tag) {
+            constexpr bool UNIT = decltype(unit_tag)::value;
+            const double alpha = d.alpha, beta = d.beta;
+            double nx_t = lane < n ? g_arr[lane] : 0.0;
+            int nx_b = lane < n ? g_bat[lane] : 0;
+            for (int base = 0; base < n; base += 32) {
+                const double cur_t = nx_t;
+                __syncwarp();
+                W.win_t[lane] = cur_t;
+                W.win_b[lane] = nx_b;
+                __syncwarp();
+                if (base + 32 + lane < n) {  // prefetch the next window
+                    nx_t = g_arr[base + 32 + lane];
+                    nx_b = g_bat[base + 32 + lane];
                 }
-                // ---- candidates, Eq. 1 waits ----
-                bool cand[S];
-                double est_n[S], wv[S];
-#pragma unroll
-                for (int s = 0; s < S; ++s) {
-                    cand[s] = act[s];
-                    est_n[s] = row[s] >= 0 ? s_lat[row[s] + b - 1] : 0.0;
-                    wv[s] = 0.0;
+                if (m0 < 0) {  // first arrival >= warmup (arrivals are sorted; engine.hpp:262)
+                    const unsigned mb = __ballot_sync(kFull, base + lane < n && cur_t >= warmup);
+                    if (mb) m0 = base + __ffs(mb) - 1;
                 }
-                if (p.any_routing && routed) {  // engine.hpp:197-206 (warp-uniform)
-                    unsigned anyc = 0;
+                const int cnt = min(32, n - base);
+                for (int j = 0; j < cnt; ++j) {
+                    const double t = W.win_t[j];
+                    const int b = W.win_b[j];
+                    const int i = base + j;
+                    drain(t);
+                    if (b < 1 || b > bmax) {  // LookupError at this query (profile.hpp:127-129)
+                        status = MSV_LOOKUP;
+                        return;
+                    }
+                    // ---- candidates and Eq. 1 waits (sched.hpp:77-85) ----
+                    bool cand[S];
+                    double est_n[S], wv[S];
 #pragma unroll
                     for (int s = 0; s < S; ++s) {
-                        cand[s] = act[s] && (((route_mask[s * 32 + lane] >> (b - 1)) & 1ull) != 0);
-                        anyc |= __ballot_sync(kFull, cand[s]);
+                        cand[s] = act[s];
+                        const double x = c_est[s] - (t - c_start[s]);
+                        wv[s] = fold[s] + ((busy[s] && 0.0 < x) ? x : 0.0);
+                        if (FULL) est_n[s] = row[s] >= 0 ? s_lat[row[s] + b - 1] : 0.0;
+                        else est_n[s] = s_lat[row[s] + b - 1];
                     }
-                    if (anyc == 0) {
+                    int bad_o = 1 << 30;  // order index of the first candidate whose size is missing
+                    if (FULL) {
+                        if (p.any_routing && route_mask != nullptr) {  // engine.hpp:197-206
+                            unsigned anyc = 0;
 #pragma unroll
-                        for (int s = 0; s < S; ++s) cand[s] = act[s];
-                    }
-                }
-                int bad_o = 1 << 30;  // order index of the first candidate whose size is missing
-                if (p.any_bad) {
-#pragma unroll
-                    for (int s = S - 1; s >= 0; --s) {
-                        const unsigned bb = __ballot_sync(kFull, cand[s] && row[s] < 0);
-                        if (bb) bad_o = s * 32 + __ffs(bb) - 1;
-                    }
-                }
-                if (SCHED == MSV_ELSA || check_wait) {
-#pragma unroll
-                    for (int s = 0; s < S; ++s) {
-                        if (!cand[s] || row[s] < 0) continue;
-                        if (fold[s] < 0.0) {  // exact left fold of the FIFO (sched.hpp:78-79)
-                            double acc = 0.0;
-                            for (int k = 0; k < qn[s]; ++k) acc = acc + q_est[(s * QC + ((qh[s] + k) & (QC - 1))) * 32 + lane];
-                            uint32_t g = g_head[s * 32 + lane];
-                            for (uint32_t k = 0; k < gn[s]; ++k) {
-                                acc = acc + s_lat[row[s] + g_bat[g] - 1];
-                                g = g_next[g];
+                            for (int s = 0; s < S; ++s) {
+                                cand[s] = act[s] && (((route_mask[s * 32 + lane] >> (b - 1)) & 1ull) != 0);
+                                anyc |= __ballot_sync(kFull, cand[s]);
                             }
-                            fold[s] = acc;
+                            if (anyc == 0) {
+#pragma unroll
+                                for (int s = 0; s < S; ++s) cand[s] = act[s];
+                            }
                         }
-                        double wt = fold[s];
-                        if (busy[s]) {  // sched.hpp:80-83
-                            const double x = c_est[s] - (t - c_start[s]);
-                            wt = wt + ((0.0 < x) ? x : 0.0);
+                        if (p.any_bad) {
+#pragma unroll
+                            for (int s = S - 1; s >= 0; --s) {
+                                const unsigned bb = __ballot_sync(kFull, cand[s] && row[s] < 0);
+                                if (bb) bad_o = s * 32 + __ffs(bb) - 1;
+                            }
                         }
-                        wv[s] = wt;
                         if (check_wait) {  // engine.hpp:208-217
-                            double gw = fold[s];
-                            if (busy[s]) {
+#pragma unroll
+                            for (int s = 0; s < S; ++s) {
+                                if (!cand[s] || row[s] < 0) continue;
                                 const double y = c_comp[s] - t;
-                                gw = gw + ((0.0 < y) ? y : 0.0);
+                                const double gw = fold[s] + ((busy[s] && 0.0 < y) ? y : 0.0);
+                                const double dd = fabs(gw - wv[s]);
+                                wdiff = (wdiff < dd) ? dd : wdiff;
                             }
-                            const double dd = fabs(gw - wt);
-                            wdiff = (wdiff < dd) ? dd : wdiff;
                         }
                     }
-                }
-                // ---- decision ----
-                int ch = -1;  // chosen order index
-                int kind;
-                if constexpr (SCHED == MSV_ELSA) {
-                    // Step A (sched.hpp:125-130): first in order with sla > alpha*(w + beta*est).
-#pragma unroll
-                    for (int s = S - 1; s >= 0; --s) {
-                        const bool ok = cand[s] && row[s] >= 0;
-                        const bool pred =
-                            ok && (unit_ab ? (sla > wv[s] + est_n[s]) : (sla > d.alpha * (wv[s] + d.beta * est_n[s])));
-                        const unsigned bA = __ballot_sync(kFull, pred);
-                        if (bA) ch = s * 32 + __ffs(bA) - 1;
-                    }
-                    kind = MSV_SLACK_SATISFYING;
-                    if (ch < 0) {  // Step B (sched.hpp:132-142): argmin w + est, earliest on ties
-                        uint64_t fb[S];
-                        uint64_t vmin = ~0ull;
-#pragma unroll
-                        for (int s = 0; s < S; ++s) {
-                            fb[s] = (cand[s] && row[s] >= 0) ? msv_dbits(wv[s] + est_n[s]) : ~0ull;
-                            vmin = fb[s] < vmin ? fb[s] : vmin;
-                        }
-                        vmin = seg_min_u64<32>(vmin);
+                    // ---- decision ----
+                    int ch = -1;  // chosen order index
+                    int kind;
+                    if constexpr (SCHED == MSV_ELSA) {
+                        // Step A (sched.hpp:125-130): first in order with sla > alpha*(w + beta*est).
 #pragma unroll
                         for (int s = S - 1; s >= 0; --s) {
-                            const unsigned bB = __ballot_sync(kFull, fb[s] == vmin && vmin != ~0ull);
-                            if (bB) ch = s * 32 + __ffs(bB) - 1;
+                            const bool ok = FULL ? (cand[s] && row[s] >= 0) : act[s];
+                            bool pred;
+                            if constexpr (UNIT) pred = ok && (sla > wv[s] + est_n[s]);
+                            else pred = ok && (sla > alpha * (wv[s] + beta * est_n[s]));
+                            const unsigned bA = __ballot_sync(kFull, pred);
+                            if (bA) ch = s * 32 + __ffs(bA) - 1;
                         }
-                        kind = MSV_FASTEST_FALLBACK;
-                    }
-                    // a size missing from the profile is a LookupError once the scan reaches it
-                    if (bad_o != (1 << 30) && (kind == MSV_FASTEST_FALLBACK || bad_o < ch)) {
-                        status = MSV_LOOKUP;
-                        break;
-                    }
-                } else {
-                    // FIFS (sched.hpp:154-170): idle -> max k, min id; else min queue length, min id.
-                    uint32_t mi = ~0u;
+                        kind = MSV_SLACK_SATISFYING;
+                        if (ch < 0) {  // Step B (sched.hpp:132-142): argmin w + est, earliest on ties
+                            uint64_t fb[S];
+                            uint64_t vmin = ~0ull;
 #pragma unroll
-                    for (int s = 0; s < S; ++s) {
-                        const uint32_t key =
-                            (cand[s] && !busy[s]) ? (((0x7FFFu - ((uint32_t)pk[s] >> 8)) << 16) | ((uint32_t)pk[s] & 0xffu)) : ~0u;
-                        mi = key < mi ? key : mi;
-                    }
-                    mi = __reduce_min_sync(kFull, mi);
-                    uint32_t key2[S];
-                    if (mi != ~0u) {
-                        kind = MSV_IDLE_LARGEST;
-                        // the key encodes (k, id): its owner is the lane slot with that pid
+                            for (int s = 0; s < S; ++s) {
+                                const bool ok = FULL ? (cand[s] && row[s] >= 0) : act[s];
+                                fb[s] = ok ? msv_dbits(wv[s] + est_n[s]) : ~0ull;
+                                vmin = fb[s] < vmin ? fb[s] : vmin;
+                            }
+                            vmin = seg_min_u64<32>(vmin);
 #pragma unroll
-                        for (int s = 0; s < S; ++s) key2[s] = (cand[s] && !busy[s]) ? (((0x7FFFu - ((uint32_t)pk[s] >> 8)) << 16) | ((uint32_t)pk[s] & 0xffu)) : ~0u;
+                            for (int s = S - 1; s >= 0; --s) {
+                                const unsigned bB = __ballot_sync(kFull, fb[s] == vmin && vmin != ~0ull);
+                                if (bB) ch = s * 32 + __ffs(bB) - 1;
+                            }
+                            kind = MSV_FASTEST_FALLBACK;
+                        }
+                        // a size missing from the profile is a LookupError once the scan reaches it
+                        if (FULL && bad_o != (1 << 30) && (kind == MSV_FASTEST_FALLBACK || bad_o < ch)) {
+                            status = MSV_LOOKUP;
+                            return;
+                        }
                     } else {
-                        kind = MSV_SHORTEST_QUEUE;
-                        uint32_t mq = ~0u;
+                        // FIFS (sched.hpp:154-170): idle -> max k, min id; else shortest queue, min id.
+                        uint32_t key[S];
+                        uint32_t mi = ~0u;
 #pragma unroll
                         for (int s = 0; s < S; ++s) {
-                            const uint32_t len = (uint32_t)qn[s] + gn[s];
-                            key2[s] = cand[s] ? (((len < 0xFFFFFFu ? len : 0xFFFFFFu) << 8) | ((uint32_t)pk[s] & 0xffu)) : ~0u;
-                            mq = key2[s] < mq ? key2[s] : mq;
+                            key[s] = (cand[s] && !busy[s])
+                                         ? (((0x7FFFu - ((uint32_t)pk[s] >> 8)) << 16) | ((uint32_t)pk[s] & 0xffu))
+                                         : ~0u;
+                            mi = key[s] < mi ? key[s] : mi;
                         }
-                        mi = __reduce_min_sync(kFull, mq);
-                    }
+                        mi = __reduce_min_sync(kFull, mi);
+                        kind = MSV_IDLE_LARGEST;
+                        if (mi == ~0u) {
+                            kind = MSV_SHORTEST_QUEUE;
 #pragma unroll
-                    for (int s = S - 1; s >= 0; --s) {
-                        const unsigned bs = __ballot_sync(kFull, key2[s] == mi);
-                        if (bs) ch = s * 32 + __ffs(bs) - 1;
-                    }
-                    if (p.any_bad) {  // the chosen partition's latency lookup fails (engine.hpp:226)
-                        bool mine = false;
-#pragma unroll
-                        for (int s = 0; s < S; ++s) mine |= (s * 32 + lane == ch) && row[s] < 0;
-                        if (__any_sync(kFull, mine)) {
-                            status = MSV_LOOKUP;
-                            break;
-                        }
-                    }
-                }
-                // ---- start or enqueue on the chosen partition (engine.hpp:225-230) ----
-#pragma unroll
-                for (int s = 0; s < S; ++s) {
-                    if (s * 32 + lane == ch) {
-                        const double est = est_n[s];
-                        if (!busy[s]) {
-                            busy[s] = true;
-                            c_start[s] = t;
-                            c_est[s] = est;
-                            c_comp[s] = t + est;
-                            c_arr[s] = t;
-                            c_meta[s] = (uint64_t)i | ((uint64_t)b << 40);
-                        } else {
-                            if (gn[s] == 0 && qn[s] < QC) {
-                                const int e = (s * QC + ((qh[s] + qn[s]) & (QC - 1))) * 32 + lane;
-                                q_est[e] = est;
-                                q_arr[e] = t;
-                                q_meta[e] = (uint64_t)i | ((uint64_t)b << 40);
-                                qn[s] += 1;
-                            } else {
-                                if (gn[s] == 0) g_head[s * 32 + lane] = (uint32_t)i;
-                                else g_next[g_tail[s * 32 + lane]] = (uint32_t)i;
-                                g_tail[s * 32 + lane] = (uint32_t)i;
-                                gn[s] += 1;
+                            for (int s = 0; s < S; ++s) {
+                                const uint32_t len = (uint32_t)qn[s] + gn[s];
+                                key[s] = cand[s] ? (((len < 0xFFFFFFu ? len : 0xFFFFFFu) << 8) | ((uint32_t)pk[s] & 0xffu))
+                                                 : ~0u;
+                                mi = key[s] < mi ? key[s] : mi;
                             }
-                            if (fold[s] >= 0.0) fold[s] = fold[s] + est;
+                            mi = __reduce_min_sync(kFull, mi);
                         }
-                        if (REC) {
-                            rec[i].partition = pk[s] & 0xff;
-                            rec[i].kind = kind;
+#pragma unroll
+                        for (int s = S - 1; s >= 0; --s) {
+                            const unsigned bs = __ballot_sync(kFull, key[s] == mi);
+                            if (bs) ch = s * 32 + __ffs(bs) - 1;
+                        }
+                        if (FULL && p.any_bad) {  // the chosen partition's latency lookup fails (engine.hpp:226)
+                            bool mine = false;
+#pragma unroll
+                            for (int s = 0; s < S; ++s) mine |= (s * 32 + lane == ch) && row[s] < 0;
+                            if (__any_sync(kFull, mine)) {
+                                status = MSV_LOOKUP;
+                                return;
+                            }
+                        }
+                    }
+                    // ---- start or enqueue on the chosen partition (engine.hpp:225-230) ----
+#pragma unroll
+                    for (int s = 0; s < S; ++s) {
+                        if (s * 32 + lane == ch) {
+                            const double est = est_n[s];
+                            const uint64_t meta = (uint64_t)i | ((uint64_t)b << 40);
+                            if (!busy[s]) {
+                                busy[s] = true;
+                                c_start[s] = t;
+                                c_est[s] = est;
+                                c_comp[s] = t + est;
+                                c_arr[s] = t;
+                                c_meta[s] = meta;
+                            } else {
+                                if (gn[s] == 0 && qn[s] < QC) {
+                                    const int e = (qh[s] + qn[s]) & (QC - 1);
+                                    W.q_est[s][e][lane] = est;
+                                    W.q_arr[s][e][lane] = t;
+                                    W.q_meta[s][e][lane] = meta;
+                                    qn[s] += 1;
+                                } else {
+                                    if (gn[s] == 0) W.g_head[s][lane] = (uint32_t)i;
+                                    else g_next[W.g_tail[s][lane]] = (uint32_t)i;
+                                    W.g_tail[s][lane] = (uint32_t)i;
+                                    gn[s] += 1;
+                                }
+                                fold[s] = fold[s] + est;  // appending extends the left fold exactly
+                            }
+                            if (REC) {
+                                rec[i].partition = pk[s] & 0xff;
+                                rec[i].kind = kind;
+                            }
                         }
                     }
                 }
             }
-        }
+        };
+        if (d.alpha == 1.0 && d.beta == 1.0) simulate(std::true_type{});
+        else simulate(std::false_type{});
         drain(INFINITY);  // after the last arrival: drain everything, no horizon cut-off
 
         // ---- publish (engine.hpp:233-252) ----
@@ -388,27 +413,25 @@ __global__ void __launch_bounds__(kSimWarpsPerBlock * 32, WarpCfg<S>::min_blocks
     }
 }
 
+template <int S, int SCHED>
+void* pick_flags(bool rec, bool full) {
+    if (rec) return (void*)&sim_warp_kernel<S, SCHED, true, true>;
+    return full ? (void*)&sim_warp_kernel<S, SCHED, false, true> : (void*)&sim_warp_kernel<S, SCHED, false, false>;
+}
+
 }  // namespace
 
-void* sim_warp_fn(int S, int sched, bool rec) {
-#define MSV_PICKW(s)                                                                                           \
-    if (S == s) {                                                                                              \
-        if (sched == MSV_ELSA)                                                                                 \
-            return rec ? (void*)&sim_warp_kernel<s, MSV_ELSA, true> : (void*)&sim_warp_kernel<s, MSV_ELSA, false>; \
-        return rec ? (void*)&sim_warp_kernel<s, MSV_FIFS, true> : (void*)&sim_warp_kernel<s, MSV_FIFS, false>;     \
-    }
-    MSV_PICKW(1)
-    MSV_PICKW(2)
-    MSV_PICKW(4)
-#undef MSV_PICKW
+void* sim_warp_fn(int S, int sched, bool rec, bool full) {
+    if (S == 1) return sched == MSV_ELSA ? pick_flags<1, MSV_ELSA>(rec, full) : pick_flags<1, MSV_FIFS>(rec, full);
+    if (S == 2) return sched == MSV_ELSA ? pick_flags<2, MSV_ELSA>(rec, full) : pick_flags<2, MSV_FIFS>(rec, full);
+    if (S == 4) return sched == MSV_ELSA ? pick_flags<4, MSV_ELSA>(rec, full) : pick_flags<4, MSV_FIFS>(rec, full);
     return nullptr;
 }
 
 size_t sim_warp_smem_bytes(int S, int n_cells) {
-    const int qc = S == 1 ? 8 : (S == 2 ? 4 : 2);
     const size_t tab = ((size_t)2 * n_cells * sizeof(double) + 15) & ~(size_t)15;
-    // per warp: rings (est, arr, meta) + overflow head/tail per lane slot
-    return tab + (size_t)kSimWarpsPerBlock * (3 * S * qc * 32 * sizeof(double) + 2 * S * 32 * sizeof(uint32_t));
+    const size_t per_warp = S == 1 ? sizeof(WarpSmem<1>) : (S == 2 ? sizeof(WarpSmem<2>) : sizeof(WarpSmem<4>));
+    return tab + (size_t)kSimWarpsPerBlock * per_warp;
 }
 
 }  // namespace msv

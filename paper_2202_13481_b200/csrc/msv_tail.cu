@@ -132,33 +132,67 @@ __global__ void __launch_bounds__(kTailThreads)
                 __syncthreads();
                 break;
             }
+            // Percentiles still in radix mode with the same (pos, prefix) share one
+            // histogram (always the case in the first pass).
+            int hsrc[kMaxTails];
             for (int q = 0; q < n_p; ++q) {
+                hsrc[q] = q;
                 if (S.state[q] == 0)
+                    for (int q2 = 0; q2 < q; ++q2)
+                        if (S.state[q2] == 0 && S.pos[q2] == S.pos[q] && S.prefix[q2] == S.prefix[q]) {
+                            hsrc[q] = q2;
+                            break;
+                        }
+            }
+            for (int q = 0; q < n_p; ++q) {
+                if (S.state[q] == 0 && hsrc[q] == q)
                     for (int k = threadIdx.x; k < kBins; k += blockDim.x) S.hist[q][k] = 0;
                 if (S.state[q] == 1 && threadIdx.x == 0) S.fill[q] = 0;
             }
             __syncthreads();
-            for (long long base = 0; base < n; base += blockDim.x) {
-                const long long i = base + threadIdx.x;
-                const bool valid = i < n;
-                const uint64_t v = valid ? order_key(msv_dbits(x[i])) : 0;
-                for (int q = 0; q < n_p; ++q) {
-                    const int st = S.state[q];
-                    if (st == 2) continue;
-                    const int pos = S.pos[q];
-                    const bool hit = valid && (pos == 64 || (v >> pos) == S.prefix[q]);
-                    if (st == 0) {
-                        const int d = pos < kDigit ? pos : kDigit;
-                        const unsigned bin = hit ? (unsigned)((v >> (pos - d)) & (uint64_t)((1 << d) - 1)) : 0xffffffffu;
-                        const unsigned peers = __match_any_sync(kFull, bin);
-                        if (hit && (threadIdx.x & 31) == __ffs(peers) - 1)
-                            atomicAdd(&S.hist[q][bin], (unsigned)__popc(peers));
-                    } else {
-                        const unsigned m = __ballot_sync(kFull, hit);
-                        unsigned slot = 0;
-                        if ((threadIdx.x & 31) == 0 && m) slot = atomicAdd(&S.fill[q], (unsigned)__popc(m));
-                        slot = __shfl_sync(kFull, slot, 0);
-                        if (hit) S.buf[q][slot + __popc(m & ((1u << (threadIdx.x & 31)) - 1u))] = v;
+            // pass parameters in registers (constant during the pass)
+            int st_r[kMaxTails], pos_r[kMaxTails], sh_r[kMaxTails];
+            uint64_t pre_r[kMaxTails];
+            unsigned dmask_r[kMaxTails];
+#pragma unroll
+            for (int q = 0; q < kMaxTails; ++q) {
+                const bool on = q < n_p;
+                st_r[q] = on ? S.state[q] : 2;
+                if (on && st_r[q] == 0 && hsrc[q] != q) st_r[q] = 3;  // rides on another histogram
+                pos_r[q] = on ? S.pos[q] : 0;
+                pre_r[q] = on ? S.prefix[q] : 0;
+                const int d = pos_r[q] < kDigit ? pos_r[q] : kDigit;
+                sh_r[q] = pos_r[q] - d;
+                dmask_r[q] = (1u << d) - 1u;
+            }
+            constexpr int U = 4;  // independent loads in flight per thread
+            const int lane = threadIdx.x & 31;
+            for (long long base = 0; base < n; base += (long long)blockDim.x * U) {
+                uint64_t v[U];
+                bool valid[U];
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const long long i = base + (long long)u * blockDim.x + threadIdx.x;
+                    valid[u] = i < n;
+                    v[u] = valid[u] ? order_key(msv_dbits(__ldg(x + i))) : 0;
+                }
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+#pragma unroll
+                    for (int q = 0; q < kMaxTails; ++q) {
+                        if (st_r[q] >= 2) continue;
+                        const bool hit = valid[u] && (pos_r[q] == 64 || (v[u] >> pos_r[q]) == pre_r[q]);
+                        if (st_r[q] == 0) {
+                            const unsigned bin = hit ? (unsigned)((v[u] >> sh_r[q]) & dmask_r[q]) : 0xffffffffu;
+                            const unsigned peers = __match_any_sync(kFull, bin);
+                            if (hit && lane == __ffs(peers) - 1) atomicAdd(&S.hist[q][bin], (unsigned)__popc(peers));
+                        } else {
+                            const unsigned m = __ballot_sync(kFull, hit);
+                            unsigned slot = 0;
+                            if (lane == 0 && m) slot = atomicAdd(&S.fill[q], (unsigned)__popc(m));
+                            slot = __shfl_sync(kFull, slot, 0);
+                            if (hit) S.buf[q][slot + __popc(m & ((1u << lane) - 1u))] = v[u];
+                        }
                     }
                 }
             }
@@ -173,7 +207,8 @@ __global__ void __launch_bounds__(kTailThreads)
                     const int per = (nb + blockDim.x - 1) / blockDim.x;
                     const int b0 = threadIdx.x * per;
                     unsigned int sum = 0;
-                    for (int k = b0; k < b0 + per && k < nb; ++k) sum += S.hist[q][k];
+                    const unsigned int* H = S.hist[hsrc[q]];
+                    for (int k = b0; k < b0 + per && k < nb; ++k) sum += H[k];
                     // read before the scan's barriers: the owning thread rewrites S.rank[q] below
                     const long long r = S.rank[q];
                     unsigned int total;
@@ -182,12 +217,12 @@ __global__ void __launch_bounds__(kTailThreads)
                         unsigned int cum = before;
                         int k = b0;
                         for (; k < b0 + per; ++k) {
-                            if ((long long)(cum + S.hist[q][k]) >= r) break;
-                            cum += S.hist[q][k];
+                            if ((long long)(cum + H[k]) >= r) break;
+                            cum += H[k];
                         }
                         S.rank[q] = r - cum;
                         S.prefix[q] = ((pos == 64) ? 0ull : (S.prefix[q] << d)) | (uint64_t)k;
-                        S.cnt[q] = S.hist[q][k];
+                        S.cnt[q] = H[k];
                         S.pos[q] = pos - d;
                     }
                     __syncthreads();

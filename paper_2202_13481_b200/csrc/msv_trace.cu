@@ -6,36 +6,25 @@
 namespace msv {
 
 namespace {
-// BatchDistribution::sample's lower_bound (workload.hpp:48-53).
-__device__ __forceinline__ int32_t cdf_sample(const double* __restrict__ cdf, int n, double u) {
-    int lo = 0, len = n;
-    while (len > 0) {
-        const int half = len >> 1;
-        if (__ldg(cdf + lo + half) < u) {
-            lo += half + 1;
-            len -= half + 1;
-        } else {
-            len = half;
-        }
-    }
-    if (lo == n) lo = n - 1;
-    return lo + 1;
+// BatchDistribution::sample's lower_bound (workload.hpp:48-53): first i with
+// !(cdf[i] < u), clamped to the last bin. guide[floor(u*G)] is lower_bound(cdf, j/G)
+// <= the answer (u >= j/G, cdf nondecreasing), so a forward scan from it is exact.
+__device__ __forceinline__ int32_t cdf_sample(const double* __restrict__ cdf, const int16_t* __restrict__ guide,
+                                              int n, double u) {
+    int i = __ldg(guide + (int)(u * (double)kGuide));  // u*G is exact (G = 2^8, u on the 2^-53 grid)
+    while (i < n && __ldg(cdf + i) < u) ++i;
+    if (i == n) i = n - 1;
+    return i + 1;
 }
 
 __global__ void __launch_bounds__(kTraceWarpsPerBlock * 32)
     trace_gen_kernel(const TraceJob* __restrict__ jobs, int n_jobs, int variant) {
     __shared__ uint64_t s_mt[kTraceWarpsPerBlock][MSV_MT_N];
-    __shared__ double s_gap[kTraceWarpsPerBlock][MSV_MT_M];
-    __shared__ double s_arr[kTraceWarpsPerBlock][MSV_MT_M];
-    __shared__ int32_t s_bat[kTraceWarpsPerBlock][MSV_MT_M];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int job = blockIdx.x * kTraceWarpsPerBlock + warp;
     if (job >= n_jobs) return;
     const TraceJob J = jobs[job];
     uint64_t* mt = s_mt[warp];
-    double* gap = s_gap[warp];
-    double* arr = s_arr[warp];
-    int32_t* bat = s_bat[warp];
 
     // mt19937_64(seed): x[0] = seed; x[i] = f*(x[i-1] ^ (x[i-1] >> 62)) + i.
     if (lane == 0) {
@@ -48,9 +37,9 @@ __global__ void __launch_bounds__(kTraceWarpsPerBlock * 32)
     }
     __syncwarp();
 
-    double t = 0.0;  // meaningful in lane 0 only
+    double t = 0.0;  // last arrival so far (warp-uniform)
     int64_t n = 0;
-    bool first = true, stop = false;
+    bool stop = false;
     while (!stop) {
         // Regenerate the 312-word block. Words [0,156) read only old words;
         // words [156,312) read new[i-156] (and word 311 reads new[0]). Within a
@@ -72,40 +61,39 @@ __global__ void __launch_bounds__(kTraceWarpsPerBlock * 32)
             __syncwarp();
         }
         // Draw order (workload.hpp:104-111): gap_0, then (batch_p, gap_{p+1}) —
-        // i.e. word 2p is query p's gap, word 2p+1 its batch.
-        for (int p = lane; p < MSV_MT_M; p += 32) {
-            const double ug = msv_uniform(msv_mt_temper(mt[2 * p]));
-            gap[p] = -msv_log1p_neg(-ug, variant) / J.rate_per_ms;  // rng.hpp:20
-            const double ub = msv_uniform(msv_mt_temper(mt[2 * p + 1]));
-            bat[p] = cdf_sample(J.cdf, J.b_max, ub);
-        }
-        __syncwarp();
-        // Sequential arrival accumulation, exactly `t += gap` (workload.hpp:111).
-        int cnt = 0;
-        if (lane == 0) {
-            for (int p = 0; p < MSV_MT_M; ++p) {
-                const double g = gap[p];
-                t = first ? g : t + g;
-                first = false;
-                if (!(t < J.duration_ms)) {
-                    stop = true;
-                    break;
-                }
-                arr[p] = t;
-                ++cnt;
+        // i.e. word 2p is query p's gap, word 2p+1 its batch. Pairs are handled in
+        // rounds of 32 (lane = pair); the arrival times are the sequential sums
+        // t_p = t_{p-1} + gap_p (workload.hpp:108-111, t_{-1} = 0.0 since 0.0 + g == g),
+        // carried lane to lane by a shuffle chain so the rounding order is the
+        // reference's.
+        for (int r = 0; r * 32 < MSV_MT_M && !stop; ++r) {
+            const int p = r * 32 + lane;
+            const int nvalid = min(32, MSV_MT_M - r * 32);
+            double g = 0.0;
+            int32_t bt = 0;
+            if (lane < nvalid) {
+                const double ug = msv_uniform(msv_mt_temper(mt[2 * p]));
+                g = -msv_log1p_neg(-ug, variant) / J.rate_per_ms;  // rng.hpp:20
+                const double ub = msv_uniform(msv_mt_temper(mt[2 * p + 1]));
+                bt = cdf_sample(J.cdf, J.guide, J.b_max, ub);
             }
-        }
-        cnt = __shfl_sync(kFull, cnt, 0);
-        stop = __shfl_sync(kFull, stop, 0);
-        for (int p = lane; p < cnt; p += 32) {
-            const int64_t idx = n + p;
-            if (idx < J.cap) {
-                J.arrival[idx] = arr[p];
-                J.batch[idx] = bat[p];
+            double acc = (lane == 0) ? t + g : 0.0;
+#pragma unroll
+            for (int k = 1; k < 32; ++k) {
+                const double prev = __shfl_sync(kFull, acc, k - 1);
+                if (lane == k) acc = prev + g;
             }
+            // `while (t < duration)`: arrivals are non-decreasing, so the kept ones are a prefix.
+            const unsigned keep = __ballot_sync(kFull, lane < nvalid && acc < J.duration_ms);
+            const int cnt = (keep == kFull) ? 32 : (__ffs(~keep) - 1);
+            if (lane < cnt && n + lane < J.cap) {
+                J.arrival[n + lane] = acc;
+                J.batch[n + lane] = bt;
+            }
+            n += cnt;
+            if (cnt < nvalid || n > J.cap) stop = true;
+            t = __shfl_sync(kFull, acc, nvalid - 1);
         }
-        n += cnt;
-        if (n > J.cap) stop = true;
         __syncwarp();
     }
     if (lane == 0) {
