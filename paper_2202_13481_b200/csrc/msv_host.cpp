@@ -419,6 +419,37 @@ int grid_build(msv_ctx* ctx, const msv_scenario* sc, int64_t n, const double* ta
             s0 = s1;
         }
     }
+    // Expected work per scenario for longest-first scheduling: queries x (1 + 4 rho^2),
+    // rho = offered load over the plan's nominal capacity sum_p 1000 / E_b[latency(k_p, b)].
+    std::vector<double> cost(n);
+    {
+        std::map<std::tuple<int, int, int>, double> cap_qps;
+        for (int64_t i = 0; i < n; ++i) {
+            if (!g->generated) {
+                cost[i] = (double)g->cap[i];
+                continue;
+            }
+            const msv_scenario& s = sc[i];
+            auto key = std::make_tuple(s.plan, s.profile, s.dist);
+            auto it = cap_qps.find(key);
+            if (it == cap_qps.end()) {
+                const Profile& pr = ctx->profiles[s.profile];
+                const Dist& ds = ctx->dists[s.dist];
+                double c = 0.0;
+                for (int32_t k : ctx->plans[s.plan].flat) {
+                    const auto kt = std::lower_bound(pr.sizes.begin(), pr.sizes.end(), k);
+                    if (kt == pr.sizes.end() || *kt != k) continue;
+                    const size_t r0 = (size_t)(kt - pr.sizes.begin()) * pr.b_max;
+                    double e = 0.0;
+                    for (size_t b = 0; b < ds.pmf.size() && b < (size_t)pr.b_max; ++b) e += ds.pmf[b] * pr.lat[r0 + b];
+                    if (e > 0.0) c += 1000.0 / e;
+                }
+                it = cap_qps.emplace(key, c).first;
+            }
+            const double rho = it->second > 0.0 ? s.rate_qps / it->second : 1.0;
+            cost[i] = (s.rate_qps * s.duration_ms / 1000.0) * (1.0 + 4.0 * rho * rho);
+        }
+    }
     int64_t qoff_global = 0;
     for (msv_grid::Wave& w : g->waves) {
         w.q0 = qoff_global;
@@ -434,7 +465,7 @@ int grid_build(msv_ctx* ctx, const msv_scenario* sc, int64_t n, const double* ta
         for (int64_t i = w.s0; i < w.s1; ++i) cls[class_of(g->P[i], sc[i].scheduler)].push_back((int32_t)i);
         for (auto& kv : cls) {
             std::stable_sort(kv.second.begin(), kv.second.end(),
-                             [&](int32_t a, int32_t b) { return g->cap[a] > g->cap[b]; });
+                             [&](int32_t a, int32_t b) { return cost[a] > cost[b]; });
             w.classes.emplace_back(kv.first, std::move(kv.second));
         }
     }

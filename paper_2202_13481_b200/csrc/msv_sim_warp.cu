@@ -28,7 +28,7 @@ constexpr uint64_t kQid = (1ull << 40) - 1;
 template <int S>
 struct WarpCfg {
     static constexpr int qcap = S == 1 ? 8 : (S == 2 ? 4 : 2);  // shared ring entries per slot
-    static constexpr int min_blocks = S == 1 ? 5 : (S == 2 ? 4 : 2);
+    static constexpr int min_blocks = S == 1 ? 7 : (S == 2 ? 4 : 2);
 };
 
 // Per-warp shared-memory layout (after the block's profile table).
@@ -113,9 +113,11 @@ __global__ void __launch_bounds__(kSimWarpsPerBlock * 32, WarpCfg<S>::min_blocks
         // Exact left fold of slot s's FIFO (sched.hpp:78-79): ring part, then overflow list.
         auto refold = [&](int s) {
             double acc = 0.0;
+#pragma unroll 1
             for (int k = 0; k < qn[s]; ++k) acc = acc + W.q_est[s][(qh[s] + k) & (QC - 1)][lane];
             if (gn[s] > 0) {
                 uint32_t g = W.g_head[s][lane];
+#pragma unroll 1
                 for (uint32_t k = 0; k < gn[s]; ++k) {
                     acc = acc + s_lat[row[s] + g_bat[g] - 1];
                     g = g_next[g];
