@@ -119,14 +119,15 @@ def cpu_baseline(specs, budget_s: float):
     ora.run_grid(probe, threads=1)
     per = max(time.perf_counter() - t0, 1e-3)  # one scenario on one core
     n = int(max(cores, min(len(specs), budget_s * cores / per)))
-    sample = [specs[int(i)] for i in order[:n]]
+    idx = [int(i) for i in order[:n]]
+    sample = [specs[i] for i in idx]
     t0 = time.perf_counter()
     r = ora.run_grid(sample, threads=cores)
     dt = time.perf_counter() - t0
     q = int(r["total"].sum())
     return {"value": q / dt, "unit": UNIT, "cores": cores, "kind": ora.kind,
             "sample": f"{len(sample)} of the grid's scenarios (all load levels), {q} simulated queries, "
-                      f"{dt:.1f} s wall on {cores} threads"}, r, sample
+                      f"{dt:.1f} s wall on {cores} threads"}, r, idx
 
 
 def run_reference(args):
@@ -184,9 +185,11 @@ def main():
         dev_ms = eng.event_elapsed_ms(0, 1)
     eng.synchronize()
     launches = eng.kernel_launches() - launches0
-    # per-stage timing of one more launch (events on the library stream)
+    # per-stage timing of one more launch, stages back to back (events on the library stream)
+    grid.set_overlap(False)
     grid.launch()
     stage = grid.timing()
+    grid.set_overlap(True)
     res = grid.results()
     if world > 1:
         td.barrier()
@@ -209,6 +212,7 @@ def main():
         p99 = torch.cat(gathered).cpu()
 
     # ---- end-to-end through the public C-ABI call with host buffers (e2e) ----
+    eng.run_grid(specs, (0.95, 0.99))  # untimed: sizes the context's reusable buffers
     h0, d0 = eng.transfer_bytes()
     if world > 1:
         td.barrier()
@@ -251,8 +255,17 @@ def main():
         allp = p99.numpy()
         line["p99_ms_by_load"] = {f"{l:.1f}": round(float(np.mean(allp[loads == l])), 4) for l in np.unique(loads)}
         if not args.no_cpu_baseline:
-            b, _, _ = cpu_baseline(specs, args.cpu_seconds)
+            b, ref, idx = cpu_baseline(specs, args.cpu_seconds)
             line["cpu_baseline"] = b
+            # the CPU sample doubles as a full-size parity check of the timed device run
+            line["parity"] = {
+                "scenarios_checked": len(idx),
+                "queries_checked": int(ref["total"].sum()),
+                "placement_hash_equal": bool(np.array_equal(res["placement_hash"][idx], ref["placement_hash"])),
+                "tails_equal": bool(np.array_equal(res["tail"][idx], ref["tail"], equal_nan=True)),
+                "counts_equal": bool(all(np.array_equal(res[k][idx], ref[k]) for k in
+                                         ("total", "violations", "measured", "measured_violations"))),
+                "against": b["kind"]}
         print(json.dumps(line), flush=True)
     if world > 1:
         td.destroy_process_group()

@@ -60,7 +60,7 @@ typedef struct msv_ctx msv_ctx;
 
 /* One simulation cell: (plan x profile x dist x rate x seed x scheduler).
  * Replaces the argument list of run() (engine.hpp:115-117) plus sample_trace()
- * (workload.hpp:97-98) when the trace is generated on the device. 88 bytes. */
+ * (workload.hpp:97-98) when the trace is generated on the device. 80 bytes. */
 typedef struct {
     int32_t profile;         /* msv_upload_profile handle (ProfileTable)           */
     int32_t dist;            /* msv_upload_dist handle (BatchDistribution); grid only */
@@ -188,6 +188,9 @@ int msv_grid_destroy(msv_grid* grid);
 int msv_grid_timing(msv_grid* grid, float* total_ms, float* trace_ms, float* sim_ms,
                     float* tail_ms);
 int64_t msv_grid_queries(msv_grid* grid);   /* simulated queries of one launch */
+/* Chunks of a large grid run on concurrent streams by default (on = 1); with on = 0
+ * the stages run back to back and msv_grid_timing reports each stage. */
+int msv_grid_set_overlap(msv_grid* grid, int on);
 int msv_synchronize(msv_ctx* ctx);
 int64_t msv_kernel_launches(msv_ctx* ctx); /* kernels launched by this context so far */
 /* CUDA events on the context stream (slots 0..7) for timing loops of launches. */

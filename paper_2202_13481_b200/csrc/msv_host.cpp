@@ -131,6 +131,9 @@ struct msv_ctx {
     int64_t launches = 0;
     int64_t h2d = 0, d2h = 0;
     cudaEvent_t ev[8] = {};
+    cudaStream_t aux[4] = {};    // chunk streams of overlapped grid launches
+    cudaEvent_t aux_ev[4] = {};
+    cudaEvent_t fork_ev = nullptr;
     std::vector<Profile> profiles;
     std::vector<Dist> dists;
     std::vector<Plan> plans;
@@ -202,6 +205,11 @@ struct ClassKey {
     }
 };
 
+constexpr int kMaxChunks = 2;           // concurrent chunks per wave (sweep: 2 best)
+constexpr int64_t kChunkScenarios = 2048;  // smallest chunk worth its own stream
+constexpr int kCounterSlots = 1024;      // work-stealing counters per launch (chunk x class)
+constexpr int kAuxStreams = kMaxChunks;
+
 ClassKey class_of(int P, int sched) {
     ClassKey c{32, 1, sched};
     if (P <= 4) c.W = 4;
@@ -235,12 +243,22 @@ struct msv_grid {
     std::vector<int32_t> P, usage_off;
     std::vector<uint8_t> bad;  // plan has a size the profile lacks
     int64_t usage_total = 0;
-    struct Wave {
-        int64_t s0 = 0, s1 = 0;  // scenarios [s0, s1)
-        int64_t q0 = 0, q1 = 0;  // trace slots [q0, q1)
+    // A chunk is a set of scenarios launched together (K1 -> K2 per class -> K3) on one
+    // stream; chunks of a wave run on different streams so one chunk's K1/K3 fill the
+    // issue slots and the tail of another's K2. Job arrays are in launch order, so a
+    // chunk's trace / tail jobs are the contiguous range [l0, l1).
+    struct Chunk {
+        int64_t l0 = 0, l1 = 0;
         std::vector<std::pair<ClassKey, std::vector<int32_t>>> classes;
         std::vector<int64_t> work_off;  // offset of each class's work list in d_work
     };
+    struct Wave {
+        int64_t s0 = 0, s1 = 0;  // scenarios [s0, s1)
+        int64_t q0 = 0, q1 = 0;  // trace slots [q0, q1)
+        std::vector<Chunk> chunks;
+    };
+    std::vector<int32_t> launch_order;  // scenario index of each launch slot
+    bool overlap = true;                // chunks on concurrent streams
     std::vector<Wave> waves;
     int64_t max_wave_q = 0;
     GridBufs own;            // buffers of a persistent grid (msv_grid_create)
@@ -461,12 +479,25 @@ int grid_build(msv_ctx* ctx, const msv_scenario* sc, int64_t n, const double* ta
         w.q1 = w.q0 + q;
         qoff_global += q;
         g->max_wave_q = std::max(g->max_wave_q, q);
-        std::map<ClassKey, std::vector<int32_t>> cls;
-        for (int64_t i = w.s0; i < w.s1; ++i) cls[class_of(g->P[i], sc[i].scheduler)].push_back((int32_t)i);
-        for (auto& kv : cls) {
-            std::stable_sort(kv.second.begin(), kv.second.end(),
-                             [&](int32_t a, int32_t b) { return cost[a] > cost[b]; });
-            w.classes.emplace_back(kv.first, std::move(kv.second));
+        // Deal the wave's scenarios, most expensive first, round-robin into chunks.
+        std::vector<int32_t> ord;
+        for (int64_t i = w.s0; i < w.s1; ++i) ord.push_back((int32_t)i);
+        std::stable_sort(ord.begin(), ord.end(), [&](int32_t a, int32_t b) { return cost[a] > cost[b]; });
+        const int64_t ns_w = w.s1 - w.s0;
+        int max_chunks = kMaxChunks;
+        if (const char* e = getenv("MSV_MAX_CHUNKS")) max_chunks = std::max(1, std::min(kMaxChunks, atoi(e)));
+        const int n_chunks = (int)std::max<int64_t>(1, std::min<int64_t>(max_chunks, ns_w / kChunkScenarios));
+        std::vector<std::vector<int32_t>> members(n_chunks);
+        for (size_t j = 0; j < ord.size(); ++j) members[j % n_chunks].push_back(ord[j]);
+        for (int c = 0; c < n_chunks; ++c) {
+            msv_grid::Chunk ch;
+            ch.l0 = (int64_t)g->launch_order.size();
+            g->launch_order.insert(g->launch_order.end(), members[c].begin(), members[c].end());
+            ch.l1 = (int64_t)g->launch_order.size();
+            std::map<ClassKey, std::vector<int32_t>> cls;
+            for (int32_t i : members[c]) cls[class_of(g->P[i], sc[i].scheduler)].push_back(i);  // cost order kept
+            for (auto& kv : cls) ch.classes.emplace_back(kv.first, std::move(kv.second));
+            w.chunks.push_back(std::move(ch));
         }
     }
     // Device buffers.
@@ -485,7 +516,7 @@ int grid_build(msv_ctx* ctx, const msv_scenario* sc, int64_t n, const double* ta
     MSV_CUDA_TRY(g->B->d_usage.ensure(std::max<int64_t>(g->usage_total, 1) * sizeof(msv_usage)));
     MSV_CUDA_TRY(g->B->d_nq.ensure(std::max<int64_t>(n, 1) * 8));
     MSV_CUDA_TRY(g->B->d_tovf.ensure(std::max<int64_t>(n, 1) * 4));
-    MSV_CUDA_TRY(g->B->d_counter.ensure(64 * sizeof(int32_t)));
+    MSV_CUDA_TRY(g->B->d_counter.ensure(kCounterSlots * sizeof(int32_t)));
     if (n_tails) MSV_CUDA_TRY(cudaMemcpy(g->B->d_p.p, tail_p, n_tails * sizeof(double), cudaMemcpyHostToDevice));
 
     // Compact profile table of this grid (staged in shared memory by the kernel).
@@ -597,18 +628,25 @@ int grid_build(msv_ctx* ctx, const msv_scenario* sc, int64_t n, const double* ta
                           parts_h.size() * sizeof(DevPart) + masks_h.size() * 8 + glat.size() * 16 +
                           n_tails * sizeof(double));
     if (n) {
+        std::vector<msv::TraceJob> tj_l(n);
+        std::vector<msv::TailJob> lj_l(n);
+        for (int64_t l = 0; l < n; ++l) {
+            tj_l[l] = tj[g->launch_order[l]];
+            lj_l[l] = lj[g->launch_order[l]];
+        }
         MSV_CUDA_TRY(cudaMemcpy(g->B->d_scen.p, g->h_scen.data(), n * sizeof(DevScen), cudaMemcpyHostToDevice));
-        MSV_CUDA_TRY(cudaMemcpy(g->B->d_tjobs.p, tj.data(), n * sizeof(msv::TraceJob), cudaMemcpyHostToDevice));
-        MSV_CUDA_TRY(cudaMemcpy(g->B->d_tailjobs.p, lj.data(), n * sizeof(msv::TailJob), cudaMemcpyHostToDevice));
+        MSV_CUDA_TRY(cudaMemcpy(g->B->d_tjobs.p, tj_l.data(), n * sizeof(msv::TraceJob), cudaMemcpyHostToDevice));
+        MSV_CUDA_TRY(cudaMemcpy(g->B->d_tailjobs.p, lj_l.data(), n * sizeof(msv::TailJob), cudaMemcpyHostToDevice));
         MSV_CUDA_TRY(cudaMemset(g->B->d_tovf.p, 0, n * 4));
     }
-    // Work lists of every (wave, class).
+    // Work lists of every (wave, chunk, class).
     std::vector<int32_t> work_h;
     for (msv_grid::Wave& w : g->waves)
-        for (auto& c : w.classes) {
-            w.work_off.push_back((int64_t)work_h.size());
-            work_h.insert(work_h.end(), c.second.begin(), c.second.end());
-        }
+        for (msv_grid::Chunk& ch : w.chunks)
+            for (auto& c : ch.classes) {
+                ch.work_off.push_back((int64_t)work_h.size());
+                work_h.insert(work_h.end(), c.second.begin(), c.second.end());
+            }
     MSV_CUDA_TRY(g->B->d_work.ensure(std::max<size_t>(work_h.size(), 1) * 4));
     if (!work_h.empty())
         MSV_CUDA_TRY(cudaMemcpy(g->B->d_work.p, work_h.data(), work_h.size() * 4, cudaMemcpyHostToDevice));
@@ -639,75 +677,118 @@ void debug_sync(cudaStream_t st, const char* what) {
     fprintf(stderr, "[msv] %s done: %s\n", what, cudaGetErrorString(e));
 }
 
+// Launch one chunk's K1 -> K2 (per class) -> K3 on `st`. Stage events (optional) bracket
+// the three stages when the launch is not overlapped.
+int launch_chunk(msv_grid* g, const msv_grid::Chunk& ch, int counter_base, cudaStream_t st, cudaEvent_t e1,
+                 cudaEvent_t e2) {
+    msv_ctx* ctx = g->ctx;
+    const int64_t nl = ch.l1 - ch.l0;
+    if (g->generated && nl > 0) {
+        MSV_CUDA_TRY(msv::launch_trace_gen(g->B->d_tjobs.as<msv::TraceJob>() + ch.l0, (int)nl, ctx->log1p, st));
+        debug_sync(st, "trace_gen");
+        ctx->launches += 1;
+    }
+    if (e1) MSV_CUDA_TRY(cudaEventRecord(e1, st));
+    for (size_t c = 0; c < ch.classes.size(); ++c) {
+        const ClassKey& k = ch.classes[c].first;
+        const int32_t nwork = (int32_t)ch.classes[c].second.size();
+        msv::SimParams p;
+        p.scen = g->B->d_scen.as<DevScen>();
+        p.out = g->B->d_out.as<DevOut>();
+        p.usage = g->B->d_usage.as<msv_usage>();
+        p.work = g->B->d_work.as<int32_t>() + ch.work_off[c];
+        p.n_work = nwork;
+        p.counter = g->B->d_counter.as<int32_t>() + ((counter_base + (int)c) % kCounterSlots);
+        p.lat = g->B->d_glat.as<double>();
+        p.util = g->B->d_gutil.as<double>();
+        p.n_cells = g->n_cells;
+        p.any_routing = p.any_bad = p.any_check_wait = 0;
+        for (int32_t si : ch.classes[c].second) {
+            if (g->scen[si].routing >= 0) p.any_routing = 1;
+            if (g->bad[si]) p.any_bad = 1;
+            if (g->scen[si].flags & MSV_FLAG_CHECK_WAIT) p.any_check_wait = 1;
+        }
+        const bool full = g->records || p.any_routing || p.any_bad || p.any_check_wait;
+        const int occ = msv::sim_max_blocks_per_sm(k.W, k.S, k.sched, g->records, full, g->n_cells);
+        if (occ <= 0) return fail(MSV_CUDA, "sim kernel: no occupancy for class");
+        const int segs_per_block = msv::kSimWarpsPerBlock * (32 / k.W);
+        const int need = (nwork + segs_per_block - 1) / segs_per_block;
+        int occ_used = occ;
+        if (const char* e = getenv("MSV_SIM_BLOCK_SLACK")) occ_used = std::max(1, occ - atoi(e));
+        const int blocks = std::max(1, std::min(need, occ_used * ctx->sms));
+        MSV_CUDA_TRY(msv::launch_sim(k.W, k.S, k.sched, g->records, p, blocks, st));
+        debug_sync(st, "sim");
+        ctx->launches += 1;
+    }
+    if (e2) MSV_CUDA_TRY(cudaEventRecord(e2, st));
+    if (!g->tail_p.empty() && nl > 0) {
+        MSV_CUDA_TRY(msv::launch_tail(g->B->d_tailjobs.as<msv::TailJob>() + ch.l0, (int)nl, g->B->d_p.as<double>(),
+                                      (int)g->tail_p.size(), st));
+        debug_sync(st, "tail");
+        ctx->launches += 1;
+    }
+    return MSV_OK;
+}
+
 int grid_launch(msv_grid* g) {
     msv_ctx* ctx = g->ctx;
     cudaStream_t st = ctx->stream;
-    float tr = 0, si = 0, ta = 0;
+    int rc;
+    // counters are zeroed once per launch; each (chunk, class) owns one
     MSV_CUDA_TRY(cudaEventRecord(g->ev[0], st));
+    MSV_CUDA_TRY(cudaMemsetAsync(g->B->d_counter.p, 0, kCounterSlots * sizeof(int32_t), st));
+    size_t total_chunks = 0;
+    for (const msv_grid::Wave& w : g->waves) total_chunks += w.chunks.size();
+    const bool overlap = g->overlap && total_chunks > 1;
+    if (overlap) {
+        for (int a = 0; a < kAuxStreams; ++a) {
+            if (!ctx->aux[a]) MSV_CUDA_TRY(cudaStreamCreateWithFlags(&ctx->aux[a], cudaStreamNonBlocking));
+            if (!ctx->aux_ev[a]) MSV_CUDA_TRY(cudaEventCreateWithFlags(&ctx->aux_ev[a], cudaEventDisableTiming));
+        }
+        if (!ctx->fork_ev) MSV_CUDA_TRY(cudaEventCreateWithFlags(&ctx->fork_ev, cudaEventDisableTiming));
+    }
+    int counter_base = 0;
+    float tr = 0, si = 0, ta = 0;
     for (size_t wi = 0; wi < g->waves.size(); ++wi) {
         const msv_grid::Wave& w = g->waves[wi];
-        const int64_t ns = w.s1 - w.s0;
-        cudaEvent_t e1 = g->ev[1], e2 = g->ev[2], e3 = g->ev[3];
-        if (g->generated) {
-            MSV_CUDA_TRY(msv::launch_trace_gen(g->B->d_tjobs.as<msv::TraceJob>() + w.s0, (int)ns, ctx->log1p, st));
-            debug_sync(st, "trace_gen");
-            ctx->launches += 1;
-        }
-        MSV_CUDA_TRY(cudaEventRecord(e1, st));
-        MSV_CUDA_TRY(cudaMemsetAsync(g->B->d_counter.p, 0, 64 * sizeof(int32_t), st));
-        for (size_t c = 0; c < w.classes.size(); ++c) {
-            const ClassKey& k = w.classes[c].first;
-            const int32_t nwork = (int32_t)w.classes[c].second.size();
-            msv::SimParams p;
-            p.scen = g->B->d_scen.as<DevScen>();
-            p.out = g->B->d_out.as<DevOut>();
-            p.usage = g->B->d_usage.as<msv_usage>();
-            p.work = g->B->d_work.as<int32_t>() + w.work_off[c];
-            p.n_work = nwork;
-            p.counter = g->B->d_counter.as<int32_t>() + (c % 64);
-            p.lat = g->B->d_glat.as<double>();
-            p.util = g->B->d_gutil.as<double>();
-            p.n_cells = g->n_cells;
-            p.any_routing = p.any_bad = p.any_check_wait = 0;
-            for (int32_t si : w.classes[c].second) {
-                if (g->scen[si].routing >= 0) p.any_routing = 1;
-                if (g->bad[si]) p.any_bad = 1;
-                if (g->scen[si].flags & MSV_FLAG_CHECK_WAIT) p.any_check_wait = 1;
+        if (overlap) {
+            // fork: every aux stream starts after everything queued on the main stream
+            MSV_CUDA_TRY(cudaEventRecord(ctx->fork_ev, st));
+            for (size_t c = 0; c < w.chunks.size(); ++c) {
+                cudaStream_t sc = ctx->aux[c % kAuxStreams];
+                MSV_CUDA_TRY(cudaStreamWaitEvent(sc, ctx->fork_ev, 0));
+                if ((rc = launch_chunk(g, w.chunks[c], counter_base, sc, nullptr, nullptr))) return rc;
+                counter_base += (int)w.chunks[c].classes.size();
             }
-            const bool full = g->records || p.any_routing || p.any_bad || p.any_check_wait;
-            const int occ = msv::sim_max_blocks_per_sm(k.W, k.S, k.sched, g->records, full, g->n_cells);
-            if (occ <= 0) return fail(MSV_CUDA, "sim kernel: no occupancy for class");
-            const int segs_per_block = msv::kSimWarpsPerBlock * (32 / k.W);
-            const int need = (nwork + segs_per_block - 1) / segs_per_block;
-            const int blocks = std::max(1, std::min(need, occ * ctx->sms));
-            MSV_CUDA_TRY(msv::launch_sim(k.W, k.S, k.sched, g->records, p, blocks, st));
-            debug_sync(st, "sim");
-            ctx->launches += 1;
-        }
-        MSV_CUDA_TRY(cudaEventRecord(e2, st));
-        if (!g->tail_p.empty()) {
-            MSV_CUDA_TRY(msv::launch_tail(g->B->d_tailjobs.as<msv::TailJob>() + w.s0, (int)ns, g->B->d_p.as<double>(),
-                                          (int)g->tail_p.size(), st));
-            debug_sync(st, "tail");
-            ctx->launches += 1;
-        }
-        MSV_CUDA_TRY(cudaEventRecord(e3, st));
-        if (g->waves.size() > 1 || wi + 1 == g->waves.size()) {
-            // per-wave stage timing (events are reused, so accumulate after each wave)
-            if (g->waves.size() > 1) {
-                MSV_CUDA_TRY(cudaEventSynchronize(e3));
-                float a = 0, b = 0, c2 = 0;
-                cudaEventElapsedTime(&a, g->ev[0], e1);
-                cudaEventElapsedTime(&b, e1, e2);
-                cudaEventElapsedTime(&c2, e2, e3);
-                tr += a;
-                si += b;
-                ta += c2;
-                MSV_CUDA_TRY(cudaEventRecord(g->ev[0], st));
+            // join: the main stream continues after every chunk of this wave
+            for (size_t a = 0; a < std::min<size_t>(w.chunks.size(), kAuxStreams); ++a) {
+                MSV_CUDA_TRY(cudaEventRecord(ctx->aux_ev[a], ctx->aux[a]));
+                MSV_CUDA_TRY(cudaStreamWaitEvent(st, ctx->aux_ev[a], 0));
+            }
+        } else {
+            for (const msv_grid::Chunk& ch : w.chunks) {
+                cudaEvent_t e0 = g->ev[0], e1 = g->ev[1], e2 = g->ev[2], e3 = g->ev[3];
+                if (wi > 0 || &ch != &w.chunks.front()) MSV_CUDA_TRY(cudaEventRecord(e0, st));
+                if ((rc = launch_chunk(g, ch, counter_base, st, e1, e2))) return rc;
+                counter_base += (int)ch.classes.size();
+                MSV_CUDA_TRY(cudaEventRecord(e3, st));
+                if (total_chunks > 1) {  // events are reused: accumulate stage times per chunk
+                    MSV_CUDA_TRY(cudaEventSynchronize(e3));
+                    float a = 0, b = 0, c2 = 0;
+                    cudaEventElapsedTime(&a, e0, e1);
+                    cudaEventElapsedTime(&b, e1, e2);
+                    cudaEventElapsedTime(&c2, e2, e3);
+                    tr += a;
+                    si += b;
+                    ta += c2;
+                }
             }
         }
     }
-    if (g->waves.size() > 1) {
+    if (overlap) {
+        MSV_CUDA_TRY(cudaEventRecord(g->ev[3], st));
+        g->t_total = -2;  // total only (stages overlap), resolved lazily
+    } else if (total_chunks > 1) {
         g->t_trace = tr;
         g->t_sim = si;
         g->t_tail = ta;
@@ -813,6 +894,14 @@ int msv_destroy(msv_ctx* ctx) {
     cudaStreamSynchronize(ctx->stream);
     for (cudaEvent_t e : ctx->ev)
         if (e) cudaEventDestroy(e);
+    for (int a = 0; a < 4; ++a) {
+        if (ctx->aux[a]) {
+            cudaStreamSynchronize(ctx->aux[a]);
+            cudaStreamDestroy(ctx->aux[a]);
+        }
+        if (ctx->aux_ev[a]) cudaEventDestroy(ctx->aux_ev[a]);
+    }
+    if (ctx->fork_ev) cudaEventDestroy(ctx->fork_ev);
     cudaStreamDestroy(ctx->stream);
     delete ctx;
     return MSV_OK;
@@ -997,7 +1086,11 @@ int msv_grid_destroy(msv_grid* grid) {
 int msv_grid_timing(msv_grid* g, float* total_ms, float* trace_ms, float* sim_ms, float* tail_ms) {
     if (!g) return fail(MSV_PARAM, "null grid");
     SetDevice sd(g->ctx->device);
-    if (g->t_total < 0) {
+    if (g->t_total == -2.0f) {  // overlapped chunks: only the total is defined
+        MSV_CUDA_TRY(cudaEventSynchronize(g->ev[3]));
+        cudaEventElapsedTime(&g->t_total, g->ev[0], g->ev[3]);
+        g->t_trace = g->t_sim = g->t_tail = -1.0f;
+    } else if (g->t_total < 0) {
         MSV_CUDA_TRY(cudaEventSynchronize(g->ev[3]));
         cudaEventElapsedTime(&g->t_trace, g->ev[0], g->ev[1]);
         cudaEventElapsedTime(&g->t_sim, g->ev[1], g->ev[2]);
@@ -1008,6 +1101,12 @@ int msv_grid_timing(msv_grid* g, float* total_ms, float* trace_ms, float* sim_ms
     if (trace_ms) *trace_ms = g->t_trace;
     if (sim_ms) *sim_ms = g->t_sim;
     if (tail_ms) *tail_ms = g->t_tail;
+    return MSV_OK;
+}
+
+int msv_grid_set_overlap(msv_grid* g, int on) {
+    if (!g) return fail(MSV_PARAM, "null grid");
+    g->overlap = on != 0;
     return MSV_OK;
 }
 

@@ -307,19 +307,34 @@ class Engine:
         return self._routings[key]
 
     def scenarios(self, specs: Iterable[GridSpec]) -> C.Array:
+        """Marshal specs into an msv_scenario array (column-wise through numpy)."""
         specs = list(specs)
-        arr = (N.Scenario * max(len(specs), 1))()
-        for i, s in enumerate(specs):
-            sc = arr[i]
-            sc.profile = self.profile(s.table)
-            sc.dist = self.dist(s.dist)
-            sc.plan = self.plan(s.plan)
-            sc.scheduler = N.MSV_ELSA if s.scheduler == "elsa" else N.MSV_FIFS
-            sc.routing = self.routing(s.routing) if s.routing is not None else -1
-            sc.flags = N.MSV_FLAG_CHECK_WAIT if s.check_wait else 0
-            sc.sla_ms, sc.alpha, sc.beta = s.sla.sla_target_ms, s.sla.alpha, s.sla.beta
-            sc.rate_qps, sc.duration_ms = s.rate_qps, s.duration_ms
-            sc.warmup_fraction, sc.seed = s.warmup_fraction, s.seed
+        n = len(specs)
+        arr = (N.Scenario * max(n, 1))()
+        if n == 0:
+            return arr
+        a = np.ctypeslib.as_array(arr)
+        plan_h: dict[int, int] = {}  # per plan object; uploads are cached by value in self.plan
+
+        def ph(p):
+            h = plan_h.get(id(p))
+            if h is None:
+                h = plan_h[id(p)] = self.plan(p)
+            return h
+
+        a["profile"] = [self.profile(s.table) for s in specs]
+        a["dist"] = [self.dist(s.dist) for s in specs]
+        a["plan"] = [ph(s.plan) for s in specs]
+        a["scheduler"] = [N.MSV_ELSA if s.scheduler == "elsa" else N.MSV_FIFS for s in specs]
+        a["routing"] = [self.routing(s.routing) if s.routing is not None else -1 for s in specs]
+        a["flags"] = [N.MSV_FLAG_CHECK_WAIT if s.check_wait else 0 for s in specs]
+        a["sla_ms"] = [s.sla.sla_target_ms for s in specs]
+        a["alpha"] = [s.sla.alpha for s in specs]
+        a["beta"] = [s.sla.beta for s in specs]
+        a["rate_qps"] = [s.rate_qps for s in specs]
+        a["duration_ms"] = [s.duration_ms for s in specs]
+        a["warmup_fraction"] = [s.warmup_fraction for s in specs]
+        a["seed"] = np.array([s.seed for s in specs], dtype=np.uint64)
         return arr
 
     # ---- hot path ----
@@ -494,6 +509,9 @@ class DeviceGrid:
 
     def queries(self) -> int:
         return int(self.eng._lib.msv_grid_queries(self._g))
+
+    def set_overlap(self, on: bool) -> None:
+        check(self.eng._lib.msv_grid_set_overlap(self._g, 1 if on else 0), "msv_grid_set_overlap")
 
     def results(self, usage: bool = False) -> dict:
         n = len(self.specs)
