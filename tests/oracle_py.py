@@ -225,6 +225,33 @@ class Oracle:
         return {"knees": knees, "ratios": ratios, "counts": counts, "gpus": gpus}
 
 
+    def lbt(self, plan, scheduler, table, sla, dist, opt):
+        """latency_bounded_throughput (metrics.hpp:81-120) of the compiled reference."""
+        seeds = _a(list(opt.seeds), np.uint64)
+        qps, inf, sims = C.c_double(), C.c_int(), C.c_int()
+        rc = self.L.oraref_lbt(C.byref(self.plan(plan)), 1 if scheduler == "elsa" else 0, C.byref(self.profile(table)),
+                               C.c_double(sla.sla_target_ms), C.c_double(sla.alpha), C.c_double(sla.beta),
+                               C.byref(self.dist(dist)), C.c_double(opt.duration_ms), _p(seeds, C.c_uint64),
+                               len(seeds), C.c_double(opt.rel_tol), C.c_double(opt.tail_p),
+                               C.c_double(opt.lambda_min), C.c_double(opt.warmup_fraction), opt.max_doublings,
+                               C.byref(qps), C.byref(inf), C.byref(sims))
+        if rc:
+            raise self.err(rc)
+        return qps.value, bool(inf.value), sims.value
+
+    def best_homogeneous(self, table, dist, sla, total_gpcs, num_gpus, gpcs_per_gpu, duration_ms, seeds):
+        s = _a(list(seeds), np.uint64)
+        k, qps = C.c_int(), C.c_double()
+        rc = self.L.oraref_best_homogeneous(C.byref(self.profile(table)), C.byref(self.dist(dist)),
+                                            C.c_double(sla.sla_target_ms), C.c_double(sla.alpha),
+                                            C.c_double(sla.beta), total_gpcs, num_gpus, gpcs_per_gpu,
+                                            C.c_double(duration_ms), _p(s, C.c_uint64), len(s), C.byref(k),
+                                            C.byref(qps))
+        if rc:
+            raise self.err(rc)
+        return k.value, qps.value
+
+
 _BEST = None
 
 
