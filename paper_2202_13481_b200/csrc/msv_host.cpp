@@ -210,11 +210,15 @@ constexpr int64_t kChunkScenarios = 2048;  // smallest chunk worth its own strea
 constexpr int kCounterSlots = 1024;      // work-stealing counters per launch (chunk x class)
 constexpr int kAuxStreams = kMaxChunks;
 
+// Kernel class of a plan with P partitions. The one-scenario-per-warp kernel serves
+// every P <= 32 (its per-arrival cost barely depends on P); the segmented kernel
+// (several scenarios per warp, W lanes each) is selected only when MSV_SEGMENTED=1.
 ClassKey class_of(int P, int sched) {
+    static const bool segmented = getenv("MSV_SEGMENTED") && atoi(getenv("MSV_SEGMENTED")) != 0;
     ClassKey c{32, 1, sched};
-    if (P <= 4) c.W = 4;
-    else if (P <= 8) c.W = 8;
-    else if (P <= 16) c.W = 16;
+    if (segmented && P <= 4) c.W = 4;
+    else if (segmented && P <= 8) c.W = 8;
+    else if (segmented && P <= 16) c.W = 16;
     else if (P <= 32) c.W = 32;
     else if (P <= 64) c.S = 2;
     else c.S = 4;
@@ -418,8 +422,10 @@ int grid_build(msv_ctx* ctx, const msv_scenario* sc, int64_t n, const double* ta
     // Waves: bound the per-launch trace working set (arrival 8 + batch 4 + link 4 +
     // sample 8 [+ record 24] bytes per query slot).
     const size_t per_q = 24 + (records ? sizeof(msv_record) : 0);
-    size_t budget = free_device_bytes() / 2;
-    if (budget > ((size_t)48 << 30)) budget = (size_t)48 << 30;
+    // Keep enough trace slots resident that a wave of 1e6-query scenarios still fills
+    // every warp slot of the simulation kernel (~4,100 on a B200).
+    size_t budget = free_device_bytes() / 10 * 7;
+    if (budget > ((size_t)140 << 30)) budget = (size_t)140 << 30;
     const int64_t max_q = std::max<int64_t>((int64_t)(budget / per_q), 1 << 20);
     // Long scenarios first inside each wave (work stealing balances the rest).
     std::vector<int64_t> order(n);

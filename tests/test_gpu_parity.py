@@ -298,3 +298,30 @@ def test_reference_unit_tests_against_device_engine():
     print(r.stdout[-3000:])
     assert "42 test cases" in summary, summary
     assert failed == ["FAILED: execution noise"], summary + "\n" + r.stdout[-2000:]
+
+
+def test_segmented_kernel_classes_subprocess():
+    """The segmented kernel (32/W scenarios per warp, W = 4/8/16) is opt-in
+    (MSV_SEGMENTED=1, read once per process): run the class-width grid in a child."""
+    import os
+    import sys
+    code = ("import sys; sys.path.insert(0, %r); from tests.test_gpu_parity import _class_grid_check; "
+            "_class_grid_check(); print('SEGMENTED_OK')" % str(ROOT))
+    env = dict(os.environ, MSV_SEGMENTED="1")
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env, timeout=600)
+    assert r.returncode == 0 and "SEGMENTED_OK" in r.stdout, r.stdout[-2000:] + r.stderr[-2000:]
+
+
+def _class_grid_check():
+    eng = Engine(0)
+    ref = O.best_oracle()
+    m = W.model("mobilenet")
+    plans = [PartitionPlan(1, 7, [[7]]), PartitionPlan(1, 7, [[3, 2, 1, 1]]), PartitionPlan(2, 7, [[1] * 7, [4, 3]]),
+             PartitionPlan(3, 7, [[1] * 7, [1] * 7, [2, 2, 2]])]
+    specs = []
+    for p in plans:
+        rate = 0.85 * W.capacity_qps(m, p)
+        for sched in ("elsa", "fifs"):
+            specs += [W._spec(m, p, rate, 3000, s, sched) for s in (1, 2, 3)]
+        specs += [W._spec(m, p, 1.6 * W.capacity_qps(m, p), 2000, 9, "elsa")]
+    assert_grid_equal(eng.run_grid(specs), ref.run_grid(specs))
