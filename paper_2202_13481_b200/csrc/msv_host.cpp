@@ -211,18 +211,38 @@ constexpr int kCounterSlots = 1024;      // work-stealing counters per launch (c
 constexpr int kAuxStreams = kMaxChunks;
 
 // Kernel class of a plan with P partitions. The one-scenario-per-warp kernel serves
-// every P <= 32 (its per-arrival cost barely depends on P); the segmented kernel
-// (several scenarios per warp, W lanes each) is selected only when MSV_SEGMENTED=1.
-ClassKey class_of(int P, int sched) {
-    static const bool segmented = getenv("MSV_SEGMENTED") && atoi(getenv("MSV_SEGMENTED")) != 0;
+// every P <= 32 by default (its per-arrival cost barely depends on P). The segmented
+// kernel (G = 32/W scenarios per warp) halves the instructions per query but keeps
+// only n/G warps busy, so it pays only when the wave holds enough small plans to fill
+// the device: `seg_w` is the narrowest segment width the wave can afford (32 = none).
+// MSV_SEGMENTED=0 disables it, =1 forces the narrowest width for every P <= 16.
+int segmented_mode() {
+    static const int mode = getenv("MSV_SEGMENTED") ? (atoi(getenv("MSV_SEGMENTED")) != 0 ? 1 : 0) : -1;
+    return mode;
+}
+
+ClassKey class_of(int P, int sched, int seg_w) {
     ClassKey c{32, 1, sched};
-    if (segmented && P <= 4) c.W = 4;
-    else if (segmented && P <= 8) c.W = 8;
-    else if (segmented && P <= 16) c.W = 16;
+    if (segmented_mode() == 1) seg_w = 4;
+    if (P <= 4 && seg_w <= 4) c.W = 4;
+    else if (P <= 8 && seg_w <= 8) c.W = 8;
+    else if (P <= 16 && seg_w <= 16) c.W = 16;
     else if (P <= 32) c.W = 32;
     else if (P <= 64) c.S = 2;
     else c.S = 4;
     return c;
+}
+
+// Narrowest segment width worth launching for a wave with n4 plans of P <= 4 and n8
+// of P <= 8 on `sms` SMs: G scenarios per warp must still leave >= half of the
+// segmented kernel's warp slots (6 blocks x 4 warps per SM) busy. W = 16 never
+// pays (two segments cost as much per arrival as one warp-wide scenario).
+int wave_seg_width(int64_t n4, int64_t n8, int sms) {
+    if (segmented_mode() == 0) return 32;
+    const int64_t half_slots = (int64_t)sms * 6 * msv::kSimWarpsPerBlock / 2;
+    if (n4 / 8 >= half_slots) return 4;
+    if (n8 / 4 >= half_slots) return 8;
+    return 32;
 }
 
 std::string fmt_num(double v) {
@@ -490,6 +510,12 @@ int grid_build(msv_ctx* ctx, const msv_scenario* sc, int64_t n, const double* ta
         for (int64_t i = w.s0; i < w.s1; ++i) ord.push_back((int32_t)i);
         std::stable_sort(ord.begin(), ord.end(), [&](int32_t a, int32_t b) { return cost[a] > cost[b]; });
         const int64_t ns_w = w.s1 - w.s0;
+        int64_t n4 = 0, n8 = 0;
+        for (int64_t i = w.s0; i < w.s1; ++i) {
+            n4 += g->P[i] <= 4;
+            n8 += g->P[i] <= 8;
+        }
+        const int seg_w = wave_seg_width(n4, n8, ctx->sms);
         int max_chunks = kMaxChunks;
         if (const char* e = getenv("MSV_MAX_CHUNKS")) max_chunks = std::max(1, std::min(kMaxChunks, atoi(e)));
         const int n_chunks = (int)std::max<int64_t>(1, std::min<int64_t>(max_chunks, ns_w / kChunkScenarios));
@@ -501,7 +527,7 @@ int grid_build(msv_ctx* ctx, const msv_scenario* sc, int64_t n, const double* ta
             g->launch_order.insert(g->launch_order.end(), members[c].begin(), members[c].end());
             ch.l1 = (int64_t)g->launch_order.size();
             std::map<ClassKey, std::vector<int32_t>> cls;
-            for (int32_t i : members[c]) cls[class_of(g->P[i], sc[i].scheduler)].push_back(i);  // cost order kept
+            for (int32_t i : members[c]) cls[class_of(g->P[i], sc[i].scheduler, seg_w)].push_back(i);  // cost order kept
             for (auto& kv : cls) ch.classes.emplace_back(kv.first, std::move(kv.second));
             w.chunks.push_back(std::move(ch));
         }
