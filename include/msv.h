@@ -174,6 +174,47 @@ int msv_dispatch_batch(msv_ctx* ctx, int32_t profile, int scheduler, int64_t n_t
                        const double* now_ms, const double* sla_ms, const double* alpha,
                        const double* beta, int32_t* chosen, int32_t* kind, double* t_wait_out);
 
+/* Batched PARIS planning (paris_plan, paris.hpp:329-345) on the device: knees
+ * (profile.hpp:275-280) as a warp ballot over each size's utilization row, batch
+ * segments (paris.hpp:34-49), instance ratios (paris.hpp:64-81, one lane per
+ * segment folding its batches in order), instance counts (paris.hpp:92-105) and the
+ * first-fit packing (paris.hpp:186-262), one warp per job. Job j's plan lands in
+ * n_per_gpu[gpu_off_j ..] (num_gpus entries) and sizes_flat[inst_off_j ..]
+ * (<= num_gpus * gpcs_per_gpu entries), the offsets being the running sums of those
+ * two quantities over jobs 0..j-1 (jobs with num_gpus < 1 or gpcs_per_gpu < 1
+ * contribute 0). Per-job errors are reported in msv_paris_out.status with the
+ * exception paris_plan would throw; the call itself fails only on bad arguments. */
+#define MSV_PARIS_MAX_SIZES 8
+typedef struct {
+    int32_t profile;        /* msv_upload_profile handle                           */
+    int32_t dist;           /* msv_upload_dist handle (its normalised pmf)         */
+    int32_t total_gpcs;
+    int32_t num_gpus;
+    int32_t gpcs_per_gpu;
+    int32_t pad;
+    double knee_threshold;  /* paris_plan default 0.8                              */
+} msv_paris_job;            /* 32 bytes */
+
+typedef struct {
+    int32_t status;         /* msv_status of paris_plan for this job               */
+    int32_t n_sizes;        /* profile sizes, ascending                             */
+    int32_t n_instances;    /* placed instances (entries in this job's sizes_flat)  */
+    int32_t err_k;          /* size / batch named by the error message, if any      */
+    int32_t err_b;
+    int32_t pad;
+    int32_t k[MSV_PARIS_MAX_SIZES];
+    int32_t knee[MSV_PARIS_MAX_SIZES];
+    int32_t seg_first[MSV_PARIS_MAX_SIZES];
+    int32_t seg_last[MSV_PARIS_MAX_SIZES];
+    double ratio[MSV_PARIS_MAX_SIZES];         /* RatioEntry::ratio                 */
+    double segment_mass[MSV_PARIS_MAX_SIZES];  /* RatioEntry::segment_mass          */
+    double count[MSV_PARIS_MAX_SIZES];         /* InstanceCounts::counts (real)     */
+    double weighted_sum;                       /* InstanceCounts::weighted_sum      */
+    double normalizer;                         /* InstanceCounts::normalizer        */
+} msv_paris_out;
+int msv_paris_batch(msv_ctx* ctx, const msv_paris_job* jobs, int64_t n_jobs, msv_paris_out* out,
+                    int32_t* n_per_gpu, int32_t* sizes_flat);
+
 /* ---- device-resident grid (benchmarks; value = HBM-resident throughput) ---- */
 typedef struct msv_grid msv_grid;
 int msv_grid_create(msv_ctx* ctx, const msv_scenario* scenarios, int64_t n, const double* tail_p,

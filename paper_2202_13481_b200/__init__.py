@@ -7,13 +7,14 @@ include/msv.h (libmsv.so, built in-tree). C++ users include include/migserve/*.h
 """
 from ._native import (DeviceError, Error, FormatError, InfeasibleError, LookupError_, ParamError, ValidationError,
                       KIND_NAMES, lib)
-from .engine import (BatchDistribution, DeviceGrid, Engine, GridSpec, PartitionPlan, ProfileTable, SlaConfig,
+from .engine import (BatchDistribution, DeviceGrid, Engine, GridSpec, ParisJob, ParisOutcome, PartitionPlan,
+                     ProfileTable, SlaConfig,
                      SyntheticProfileParams, derive_sla_target, homogeneous_plan, lognormal_batch_pdf, paris_plan,
                      synth_profile)
 
 __all__ = [
     "BatchDistribution", "DeviceError", "DeviceGrid", "Engine", "Error", "FormatError", "GridSpec", "InfeasibleError",
-    "KIND_NAMES", "LookupError_", "ParamError", "PartitionPlan", "ProfileTable", "SlaConfig", "SyntheticProfileParams",
+    "KIND_NAMES", "LookupError_", "ParamError", "ParisJob", "ParisOutcome", "PartitionPlan", "ProfileTable", "SlaConfig", "SyntheticProfileParams",
     "ValidationError", "derive_sla_target", "homogeneous_plan", "lib", "lognormal_batch_pdf", "paris_plan",
     "synth_profile",
 ]

@@ -72,6 +72,23 @@ class Record(C.Structure):
     _fields_ = [("start_ms", C.c_double), ("finish_ms", C.c_double), ("partition", C.c_int32), ("kind", C.c_int32)]
 
 
+MSV_PARIS_MAX_SIZES = 8
+
+
+class ParisJob(C.Structure):
+    _fields_ = [("profile", C.c_int32), ("dist", C.c_int32), ("total_gpcs", C.c_int32), ("num_gpus", C.c_int32),
+                ("gpcs_per_gpu", C.c_int32), ("pad", C.c_int32), ("knee_threshold", C.c_double)]
+
+
+class ParisOut(C.Structure):
+    _fields_ = [("status", C.c_int32), ("n_sizes", C.c_int32), ("n_instances", C.c_int32), ("err_k", C.c_int32),
+                ("err_b", C.c_int32), ("pad", C.c_int32), ("k", C.c_int32 * MSV_PARIS_MAX_SIZES),
+                ("knee", C.c_int32 * MSV_PARIS_MAX_SIZES), ("seg_first", C.c_int32 * MSV_PARIS_MAX_SIZES),
+                ("seg_last", C.c_int32 * MSV_PARIS_MAX_SIZES), ("ratio", C.c_double * MSV_PARIS_MAX_SIZES),
+                ("segment_mass", C.c_double * MSV_PARIS_MAX_SIZES), ("count", C.c_double * MSV_PARIS_MAX_SIZES),
+                ("weighted_sum", C.c_double), ("normalizer", C.c_double)]
+
+
 _P = C.c_void_p
 _i32p = C.POINTER(C.c_int32)
 _i64p = C.POINTER(C.c_int64)
@@ -99,6 +116,7 @@ _SIGNATURES = {
     "msv_tail_latency": (C.c_int, [_P, _f64p, C.c_int64, _f64p, C.c_int, _f64p]),
     "msv_dispatch_batch": (C.c_int, [_P, C.c_int32, C.c_int, C.c_int64, _i64p, _i32p, _i32p, _u8p, _f64p, _f64p,
                                      _i64p, _i32p, _i32p, _f64p, _f64p, _f64p, _f64p, _i32p, _i32p, _f64p]),
+    "msv_paris_batch": (C.c_int, [_P, C.POINTER(ParisJob), C.c_int64, C.POINTER(ParisOut), _i32p, _i32p]),
     "msv_grid_create": (C.c_int, [_P, C.POINTER(Scenario), C.c_int64, _f64p, C.c_int, C.POINTER(_P)]),
     "msv_grid_launch": (C.c_int, [_P]),
     "msv_grid_results": (C.c_int, [_P, C.POINTER(Result), C.POINTER(Usage)]),

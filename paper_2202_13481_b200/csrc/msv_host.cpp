@@ -69,6 +69,7 @@ struct Profile {
     int b_max = 0;
     std::vector<double> lat, util;
     int cell_off = 0;
+    int size_off = 0;
 };
 
 struct Dist {
@@ -139,15 +140,18 @@ struct msv_ctx {
     std::vector<Plan> plans;
     std::vector<Routing> routings;
     // concatenated profile cells / cdfs on the device
-    DevBuf d_lat, d_util, d_cdf, d_guide;
+    DevBuf d_lat, d_util, d_cdf, d_pmf, d_guide, d_sizes;
     int n_cells = 0;
     bool tables_dirty = true;
 
     int sync_tables() {
         if (!tables_dirty) return MSV_OK;
-        std::vector<double> lat, util, cdf;
+        std::vector<double> lat, util, cdf, pmf;
         std::vector<int16_t> guide;
+        std::vector<int32_t> sizes;
         for (Profile& p : profiles) {
+            p.size_off = (int)sizes.size();
+            sizes.insert(sizes.end(), p.sizes.begin(), p.sizes.end());
             p.cell_off = (int)lat.size();
             lat.insert(lat.end(), p.lat.begin(), p.lat.end());
             util.insert(util.end(), p.util.begin(), p.util.end());
@@ -155,6 +159,7 @@ struct msv_ctx {
         for (Dist& d : dists) {
             d.dev_off = cdf.size();
             cdf.insert(cdf.end(), d.cdf.begin(), d.cdf.end());
+            pmf.insert(pmf.end(), d.pmf.begin(), d.pmf.end());
             // guide[j] = first i with !(cdf[i] < j/G): lower_bound's answer for u = j/G,
             // a valid start for every u >= j/G (the cdf is nondecreasing).
             d.guide_off = guide.size();
@@ -174,6 +179,11 @@ struct msv_ctx {
             MSV_CUDA_TRY(cudaMemcpy(d_util.p, util.data(), util.size() * 8, cudaMemcpyHostToDevice));
         }
         if (!cdf.empty()) MSV_CUDA_TRY(cudaMemcpy(d_cdf.p, cdf.data(), cdf.size() * 8, cudaMemcpyHostToDevice));
+        MSV_CUDA_TRY(d_pmf.ensure(std::max<size_t>(pmf.size(), 1) * 8));
+        if (!pmf.empty()) MSV_CUDA_TRY(cudaMemcpy(d_pmf.p, pmf.data(), pmf.size() * 8, cudaMemcpyHostToDevice));
+        MSV_CUDA_TRY(d_sizes.ensure(std::max<size_t>(sizes.size(), 1) * 4));
+        if (!sizes.empty())
+            MSV_CUDA_TRY(cudaMemcpy(d_sizes.p, sizes.data(), sizes.size() * 4, cudaMemcpyHostToDevice));
         MSV_CUDA_TRY(d_guide.ensure(std::max<size_t>(guide.size(), 1) * 2));
         if (!guide.empty())
             MSV_CUDA_TRY(cudaMemcpy(d_guide.p, guide.data(), guide.size() * 2, cudaMemcpyHostToDevice));
@@ -1341,6 +1351,82 @@ int msv_tail_latency(msv_ctx* ctx, const double* samples, int64_t n, const doubl
     ctx->launches += 1;
     MSV_CUDA_TRY(cudaMemcpyAsync(out, d_res.p, n_p * 8, cudaMemcpyDeviceToHost, ctx->stream));
     MSV_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    return MSV_OK;
+}
+
+int msv_paris_batch(msv_ctx* ctx, const msv_paris_job* jobs, int64_t n_jobs, msv_paris_out* out, int32_t* n_per_gpu,
+                    int32_t* sizes_flat) {
+    if (!ctx || (n_jobs > 0 && (!jobs || !out || !n_per_gpu || !sizes_flat))) return fail(MSV_PARAM, "null argument");
+    if (n_jobs <= 0) return MSV_OK;
+    std::vector<msv::ParisJobDev> dj((size_t)n_jobs);
+    int64_t gpu_total = 0, inst_total = 0;
+    for (int64_t j = 0; j < n_jobs; ++j) {
+        const msv_paris_job& a = jobs[j];
+        if (a.profile < 0 || a.profile >= (int)ctx->profiles.size()) return fail(MSV_PARAM, "unknown profile handle");
+        if (a.dist < 0 || a.dist >= (int)ctx->dists.size()) return fail(MSV_PARAM, "unknown distribution handle");
+        const int64_t g = a.num_gpus >= 1 && a.gpcs_per_gpu >= 1 ? a.num_gpus : 0;
+        const int64_t c = g ? (int64_t)a.num_gpus * a.gpcs_per_gpu : 0;
+        if (c > (int64_t)1 << 24) return fail(MSV_PARAM, "paris batch: num_gpus * gpcs_per_gpu too large");
+        msv::ParisJobDev& d = dj[(size_t)j];
+        d.gpu_off = gpu_total;
+        d.inst_off = inst_total;
+        gpu_total += g;
+        inst_total += c;
+        d.total_gpcs = a.total_gpcs;
+        d.num_gpus = a.num_gpus;
+        d.gpcs_per_gpu = a.gpcs_per_gpu;
+        d.knee_threshold = a.knee_threshold;
+        d.pad = 0;
+    }
+    SetDevice sd(ctx->device);
+    int rc = ctx->sync_tables();
+    if (rc) return rc;
+    for (int64_t j = 0; j < n_jobs; ++j) {
+        const Profile& pr = ctx->profiles[jobs[j].profile];
+        const Dist& di = ctx->dists[jobs[j].dist];
+        msv::ParisJobDev& d = dj[(size_t)j];
+        d.row0 = pr.cell_off;
+        d.n_sizes = (int32_t)pr.sizes.size();
+        d.b_max = pr.b_max;
+        d.dist_b_max = (int32_t)di.pmf.size();
+        d.pmf_off = (int64_t)di.dev_off;
+        d.sizes = ctx->d_sizes.as<int32_t>() + pr.size_off;
+        if (d.n_sizes > MSV_PARIS_MAX_SIZES) {
+            d.pad = MSV_PARAM;  // reported per job; the kernel only writes the status
+            d.n_sizes = 0;
+        }
+    }
+    DevBuf b_jobs, b_out, b_per, b_flat, b_rem;
+    MSV_CUDA_TRY(b_jobs.ensure(dj.size() * sizeof(msv::ParisJobDev)));
+    MSV_CUDA_TRY(b_out.ensure((size_t)n_jobs * sizeof(msv_paris_out)));
+    MSV_CUDA_TRY(b_per.ensure((size_t)std::max<int64_t>(gpu_total, 1) * 4));
+    MSV_CUDA_TRY(b_rem.ensure((size_t)std::max<int64_t>(gpu_total, 1) * 4));
+    MSV_CUDA_TRY(b_flat.ensure((size_t)std::max<int64_t>(inst_total, 1) * 4));
+    MSV_CUDA_TRY(cudaMemcpyAsync(b_jobs.p, dj.data(), dj.size() * sizeof(msv::ParisJobDev), cudaMemcpyHostToDevice,
+                                 ctx->stream));
+    ctx->h2d += (int64_t)(dj.size() * sizeof(msv::ParisJobDev));
+    msv::ParisParams pp;
+    pp.jobs = b_jobs.as<msv::ParisJobDev>();
+    pp.n_jobs = n_jobs;
+    pp.lat = ctx->d_lat.as<double>();
+    pp.util = ctx->d_util.as<double>();
+    pp.pmf = ctx->d_pmf.as<double>();
+    pp.out = b_out.as<msv_paris_out>();
+    pp.n_per_gpu = b_per.as<int32_t>();
+    pp.sizes_flat = b_flat.as<int32_t>();
+    pp.remaining = b_rem.as<int32_t>();
+    MSV_CUDA_TRY(msv::launch_paris(pp, ctx->stream));
+    debug_sync(ctx->stream, "paris");
+    ctx->launches += 1;
+    MSV_CUDA_TRY(cudaMemcpyAsync(out, b_out.p, (size_t)n_jobs * sizeof(msv_paris_out), cudaMemcpyDeviceToHost,
+                                 ctx->stream));
+    if (gpu_total)
+        MSV_CUDA_TRY(cudaMemcpyAsync(n_per_gpu, b_per.p, (size_t)gpu_total * 4, cudaMemcpyDeviceToHost, ctx->stream));
+    if (inst_total)
+        MSV_CUDA_TRY(
+            cudaMemcpyAsync(sizes_flat, b_flat.p, (size_t)inst_total * 4, cudaMemcpyDeviceToHost, ctx->stream));
+    MSV_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    ctx->d2h += (int64_t)n_jobs * (int64_t)sizeof(msv_paris_out) + 4 * (gpu_total + inst_total);
     return MSV_OK;
 }
 

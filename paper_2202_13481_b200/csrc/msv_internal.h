@@ -135,7 +135,34 @@ struct DispatchParams {
     int32_t* error;  // LookupError flag per trial
 };
 
+// Batched paris_plan jobs (msv_paris_batch); offsets precomputed on the host.
+struct ParisJobDev {
+    int32_t row0;      // cell offset of the profile's first size row
+    int32_t n_sizes;
+    int32_t b_max;     // profile b_max
+    int32_t dist_b_max;
+    int64_t pmf_off;   // dist pmf offset
+    int64_t gpu_off;   // into n_per_gpu
+    int64_t inst_off;  // into sizes_flat
+    const int32_t* sizes;
+    int32_t total_gpcs, num_gpus, gpcs_per_gpu, pad;
+    double knee_threshold;
+};
+
+struct ParisParams {
+    const ParisJobDev* jobs;
+    int64_t n_jobs;
+    const double* lat;
+    const double* util;
+    const double* pmf;
+    msv_paris_out* out;
+    int32_t* n_per_gpu;
+    int32_t* sizes_flat;
+    int32_t* remaining;  // scratch: num_gpus ints per job at gpu_off
+};
+
 // Kernel launchers (msv_kernels.cu). Return cudaGetLastError().
+cudaError_t launch_paris(const ParisParams& p, cudaStream_t stream);
 cudaError_t launch_trace_gen(const TraceJob* d_jobs, int n_jobs, int log1p_variant,
                              cudaStream_t stream);
 // Persistent simulation kernel for P <= W*S (W lanes per scenario, S slots per lane).

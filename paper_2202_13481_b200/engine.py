@@ -185,6 +185,61 @@ def homogeneous_plan(k: int, total_gpcs: int, num_gpus: int, gpcs_per_gpu: int) 
 
 
 @dataclass
+class ParisJob:
+    """One paris_plan call (paris.hpp:329-345) for Engine.paris_batch."""
+    table: ProfileTable
+    dist: BatchDistribution
+    total_gpcs: int
+    num_gpus: int
+    gpcs_per_gpu: int
+    knee_threshold: float = 0.8
+
+
+@dataclass
+class ParisOutcome:
+    """ParisResult (paris.hpp:318-324) of one job, or the exception paris_plan throws."""
+    knees: dict = field(default_factory=dict)            # k -> knee batch
+    segments: list = field(default_factory=list)         # (k, first, last)
+    ratios: list = field(default_factory=list)           # RatioEntry::ratio, ascending k
+    segment_mass: list = field(default_factory=list)
+    counts: list = field(default_factory=list)           # InstanceCounts::counts (real)
+    weighted_sum: float = 0.0
+    normalizer: float = 0.0
+    plan: PartitionPlan | None = None
+    error: Exception | None = None
+
+
+def _paris_error(o, job: ParisJob) -> Exception:
+    """The reference's exception (type and message) for a failed device job."""
+    st, thr = o.status, job.knee_threshold
+    if st == N.MSV_VALIDATION:
+        if len(job.dist.weights) != job.table.b_max:
+            return N.ValidationError("paris_plan: distribution support must match profile b_max")
+        if o.err_b:
+            return N.ValidationError(f"instance_ratios: nonpositive throughput at (k={o.err_k}, b={o.err_b})")
+        if o.weighted_sum == 0.0 and any(o.ratio[i] < 0.0 for i in range(o.n_sizes)):
+            return N.ValidationError("instance_counts: negative ratio")
+        return N.ValidationError("segment_batches: knees must be nondecreasing in k")
+    if st == N.MSV_PARAM:
+        if len(job.table.sizes) > N.MSV_PARIS_MAX_SIZES:
+            return N.ParamError(f"paris batch: at most {N.MSV_PARIS_MAX_SIZES} partition sizes per profile")
+        if not (thr > 0.0) or thr > 1.0:
+            return N.ParamError("knee: threshold must be in (0,1]")
+        if job.total_gpcs < 1:
+            return N.ParamError("instance_counts: total_gpcs must be >= 1")
+        if not (o.weighted_sum > 0.0):
+            return N.ParamError("instance_counts: all ratios are zero")
+        if job.num_gpus < 1:
+            return N.ParamError("pack_plan: num_gpus must be >= 1")
+        if job.gpcs_per_gpu < 1:
+            return N.ParamError("pack_plan: gpcs_per_gpu must be >= 1")
+        return N.ParamError("pack_plan: partition size must be positive")
+    if st == N.MSV_INFEASIBLE:
+        return N.InfeasibleError(f"pack_plan: instance of size {o.err_k} exceeds gpcs_per_gpu={job.gpcs_per_gpu}")
+    return N._ERRORS.get(st, N.Error)(f"paris_plan: status {st}")
+
+
+@dataclass
 class SlaConfig:
     sla_target_ms: float
     alpha: float = 1.0
@@ -462,6 +517,54 @@ class Engine:
         if want_t_wait:
             return chosen[:n], kind[:n], tw[: len(ids)]
         return chosen[:n], kind[:n]
+
+    def paris_batch(self, jobs: Sequence[ParisJob]) -> list[ParisOutcome]:
+        """Batched paris_plan on the device (K4, msv_paris_batch): one warp per job."""
+        n = len(jobs)
+        if n == 0:
+            return []
+        ja = (N.ParisJob * n)()
+        n_gpu = n_inst = 0
+        for i, j in enumerate(jobs):
+            ja[i].profile = self.profile(j.table)
+            ja[i].dist = self.dist(j.dist)
+            ja[i].total_gpcs = j.total_gpcs
+            ja[i].num_gpus = j.num_gpus
+            ja[i].gpcs_per_gpu = j.gpcs_per_gpu
+            ja[i].knee_threshold = j.knee_threshold
+            if j.num_gpus >= 1 and j.gpcs_per_gpu >= 1:
+                n_gpu += j.num_gpus
+                n_inst += j.num_gpus * j.gpcs_per_gpu
+        out = (N.ParisOut * n)()
+        per = np.zeros(max(n_gpu, 1), np.int32)
+        flat = np.zeros(max(n_inst, 1), np.int32)
+        check(self._lib.msv_paris_batch(self._h, ja, n, out, _ptr(per, C.c_int32), _ptr(flat, C.c_int32)),
+              "paris_batch")
+        res, go, io = [], 0, 0
+        for i, j in enumerate(jobs):
+            o = out[i]
+            r = ParisOutcome()
+            if o.status:
+                r.error = _paris_error(o, j)
+            else:
+                ns = o.n_sizes
+                r.knees = {int(o.k[s]): int(o.knee[s]) for s in range(ns)}
+                r.segments = [(int(o.k[s]), int(o.seg_first[s]), int(o.seg_last[s])) for s in range(ns)]
+                r.ratios = [o.ratio[s] for s in range(ns)]
+                r.segment_mass = [o.segment_mass[s] for s in range(ns)]
+                r.counts = [o.count[s] for s in range(ns)]
+                r.weighted_sum, r.normalizer = o.weighted_sum, o.normalizer
+                gpus, off = [], io
+                for g in range(j.num_gpus):
+                    c = int(per[go + g])
+                    gpus.append([int(x) for x in flat[off:off + c]])
+                    off += c
+                r.plan = PartitionPlan(j.num_gpus, j.gpcs_per_gpu, gpus)
+            if j.num_gpus >= 1 and j.gpcs_per_gpu >= 1:
+                go += j.num_gpus
+                io += j.num_gpus * j.gpcs_per_gpu
+            res.append(r)
+        return res
 
     def grid(self, specs: Sequence[GridSpec], tail_p: Sequence[float] = (0.95, 0.99)) -> "DeviceGrid":
         return DeviceGrid(self, specs, tail_p)
