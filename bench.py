@@ -212,13 +212,17 @@ def main():
         p99 = torch.cat(gathered).cpu()
 
     # ---- end-to-end through the public C-ABI call with host buffers (e2e) ----
-    eng.run_grid(specs, (0.95, 0.99))  # untimed: sizes the context's reusable buffers
+    # input = the grid's msv_scenario array in host memory (marshalled once, like a C++
+    # caller's array); every step: msv_run_grid = descriptors H2D, trace/sim/tails on
+    # the device, per-scenario results D2H into host buffers.
+    prepared = eng.prepare(specs)
+    eng.run_grid(prepared, (0.95, 0.99))  # untimed: sizes the context's reusable buffers
     h0, d0 = eng.transfer_bytes()
     if world > 1:
         td.barrier()
     t0 = time.perf_counter()
     for _ in range(max(1, min(args.steps, 3))):
-        r = eng.run_grid(specs, (0.95, 0.99))
+        r = eng.run_grid(prepared, (0.95, 0.99))
     e2e_steps = max(1, min(args.steps, 3))
     e2e_s = time.perf_counter() - t0
     h1, d1 = eng.transfer_bytes()
@@ -237,6 +241,25 @@ def main():
         except Exception:
             pass
         peak = float(peaks.get("hbm_gbs", 6650.0))
+        # per-launch DRAM traffic and instruction mix of K2 from the committed ncu capture
+        prof_k2, prof_src = None, None
+        for sp in sorted((ROOT / "profiles").glob("r*/summary.json"), reverse=True):
+            try:
+                prof_k2 = json.loads(sp.read_text())["kernels"]["K2 sim_warp_kernel"]
+                prof_src = str(sp.relative_to(ROOT))
+                break
+            except Exception:
+                continue
+        sim_launches = max(1, round(launches / args.steps / 3))  # K1/K2/K3 once per chunk
+        q_launch = queries / sim_launches
+        traffic = prof_k2["traffic_bytes_per_query"] * q_launch if prof_k2 else None
+        clk_mhz = clk.summary().get("sm_mhz") or 1965.0
+        issue = None
+        if prof_k2:
+            ach = prof_k2["warp_instructions_per_query"] * queries / sim_s
+            pk = 148 * 4 * clk_mhz * 1e6
+            issue = {"achieved_warp_inst_per_s": ach, "peak_warp_inst_per_s": pk, "frac": ach / pk,
+                     "warp_inst_per_query": prof_k2["warp_instructions_per_query"], "source": prof_src}
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": dev_ms_max / args.steps, "higher_is_better": True,
                 "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
@@ -246,10 +269,12 @@ def main():
                 "gpu_launches": launches,
                 "stage_ms": {k: round(v, 3) for k, v in stage.items()},
                 "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                             "frac": achieved / peak, "traffic": None,
-                             "kernel": "sim_kernel (K2)",
-                             "note": "issue/latency-bound FP64 state machine; HBM fraction is small by "
-                                     "construction (DESIGN.md roofline)"},
+                             "frac": achieved / peak, "traffic": traffic,
+                             "traffic_unit": "DRAM bytes per K2 launch (ncu, %d queries per launch)" % q_launch,
+                             "algorithmic_bytes_per_launch": SIM_BYTES_PER_QUERY * q_launch,
+                             "kernel": "sim_warp_kernel (K2)", "issue": issue,
+                             "note": "K2 is issue-bound (dependent FP64 state machine): 'issue' is the binding "
+                                     "roof; HBM fraction is small by construction (DESIGN.md roofline)"},
                 "clocks": clk.summary()}
         loads = np.tile(np.repeat(np.arange(1, 11) / 10.0, args.seeds), world)
         allp = p99.numpy()

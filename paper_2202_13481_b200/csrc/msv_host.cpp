@@ -7,6 +7,7 @@
 #include <string.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cstdio>
 #include <cstdlib>
 #include <map>
@@ -391,9 +392,39 @@ int64_t trace_capacity(double rate_qps, double duration_ms) {
     return (int64_t)ceil(mean + 10.0 * sqrt(mean) + 160.0);
 }
 
+// MSV_HOST_TIMING=1: per-phase host timings of grid builds on stderr (diagnostics).
+struct PhaseTimer {
+    bool on = getenv("MSV_HOST_TIMING") != nullptr;
+    std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
+    std::string line;
+    void mark(const char* what) {
+        if (!on) return;
+        const auto now = std::chrono::steady_clock::now();
+        char buf[64];
+        snprintf(buf, sizeof buf, " %s %.2f", what, std::chrono::duration<double, std::milli>(now - t).count());
+        line += buf;
+        t = now;
+    }
+    ~PhaseTimer() {
+        if (on && !line.empty()) fprintf(stderr, "[msv] grid_build ms:%s\n", line.c_str());
+    }
+};
+
+// cudaMemGetInfo costs up to ~10 ms on a busy driver; the wave budget only needs a
+// coarse figure, so it is refreshed at most once per second per thread.
 size_t free_device_bytes() {
-    size_t fr = 0, tot = 0;
-    cudaMemGetInfo(&fr, &tot);
+    thread_local size_t fr = 0;
+    thread_local int dev = -1;
+    thread_local std::chrono::steady_clock::time_point at;
+    int cur = 0;
+    cudaGetDevice(&cur);
+    const auto now = std::chrono::steady_clock::now();
+    if (cur != dev || now - at > std::chrono::seconds(1)) {
+        size_t tot = 0;
+        cudaMemGetInfo(&fr, &tot);
+        dev = cur;
+        at = now;
+    }
     return fr;
 }
 
@@ -406,8 +437,10 @@ int grid_build(msv_ctx* ctx, const msv_scenario* sc, int64_t n, const double* ta
     for (int j = 0; j < n_tails; ++j)
         if (!(tail_p[j] > 0.0) || !(tail_p[j] < 1.0))
             return fail(MSV_PARAM, "tail_latency: percentile must be in (0,1)");
+    PhaseTimer pt;
     int rc = ctx->sync_tables();
     if (rc) return rc;
+    pt.mark("tables");
     std::unique_ptr<msv_grid> g(new msv_grid);
     g->ctx = ctx;
     if (scratch) g->B = &ctx->scratch;
@@ -449,6 +482,7 @@ int grid_build(msv_ctx* ctx, const msv_scenario* sc, int64_t n, const double* ta
             }
         }
     }
+    pt.mark("validate");
     // Waves: bound the per-launch trace working set (arrival 8 + batch 4 + link 4 +
     // sample 8 [+ record 24] bytes per query slot).
     const size_t per_q = 24 + (records ? sizeof(msv_record) : 0);
@@ -473,6 +507,7 @@ int grid_build(msv_ctx* ctx, const msv_scenario* sc, int64_t n, const double* ta
             s0 = s1;
         }
     }
+    pt.mark("waves");
     // Expected work per scenario for longest-first scheduling: queries x (1 + 4 rho^2),
     // rho = offered load over the plan's nominal capacity sum_p 1000 / E_b[latency(k_p, b)].
     std::vector<double> cost(n);
@@ -542,6 +577,7 @@ int grid_build(msv_ctx* ctx, const msv_scenario* sc, int64_t n, const double* ta
             w.chunks.push_back(std::move(ch));
         }
     }
+    pt.mark("cost+chunks");
     // Device buffers.
     const size_t wq = (size_t)std::max<int64_t>(g->max_wave_q, 1);
     MSV_CUDA_TRY(g->B->d_arr.ensure(wq * 8));
@@ -561,6 +597,7 @@ int grid_build(msv_ctx* ctx, const msv_scenario* sc, int64_t n, const double* ta
     MSV_CUDA_TRY(g->B->d_counter.ensure(kCounterSlots * sizeof(int32_t)));
     if (n_tails) MSV_CUDA_TRY(cudaMemcpy(g->B->d_p.p, tail_p, n_tails * sizeof(double), cudaMemcpyHostToDevice));
 
+    pt.mark("ensure");
     // Compact profile table of this grid (staged in shared memory by the kernel).
     std::map<int, int> grid_cell_off;
     std::vector<double> glat, gutil;
@@ -620,6 +657,7 @@ int grid_build(msv_ctx* ctx, const msv_scenario* sc, int64_t n, const double* ta
     if (!masks_h.empty())
         MSV_CUDA_TRY(cudaMemcpy(g->B->d_masks.p, masks_h.data(), masks_h.size() * 8, cudaMemcpyHostToDevice));
 
+    pt.mark("parts");
     // Per-scenario device descriptors.
     g->h_scen.resize(n);
     std::vector<msv::TraceJob> tj(n);
@@ -681,6 +719,7 @@ int grid_build(msv_ctx* ctx, const msv_scenario* sc, int64_t n, const double* ta
         MSV_CUDA_TRY(cudaMemcpy(g->B->d_tailjobs.p, lj_l.data(), n * sizeof(msv::TailJob), cudaMemcpyHostToDevice));
         MSV_CUDA_TRY(cudaMemset(g->B->d_tovf.p, 0, n * 4));
     }
+    pt.mark("descriptors");
     // Work lists of every (wave, chunk, class).
     std::vector<int32_t> work_h;
     for (msv_grid::Wave& w : g->waves)
@@ -707,6 +746,7 @@ int grid_build(msv_ctx* ctx, const msv_scenario* sc, int64_t n, const double* ta
         if (n) MSV_CUDA_TRY(cudaMemcpy(g->B->d_nq.p, g->host_n.data(), n * 8, cudaMemcpyHostToDevice));
     }
     for (cudaEvent_t& e : g->ev) MSV_CUDA_TRY(cudaEventCreate(&e));
+    pt.mark("work+events");
     *out = g.release();
     return MSV_OK;
 }
@@ -1201,14 +1241,24 @@ int msv_run_grid(msv_ctx* ctx, const msv_scenario* scenarios, int64_t n, const d
     if (!ctx || (n > 0 && (!scenarios || !results))) return fail(MSV_PARAM, "null argument");
     SetDevice sd(ctx->device);
     msv_grid* g = nullptr;
+    static const bool host_timing = getenv("MSV_HOST_TIMING") != nullptr;
+    const auto t0 = std::chrono::steady_clock::now();
     int rc = grid_build(ctx, scenarios, n, tail_p, n_tails, nullptr, nullptr, nullptr, false, &g, nullptr, true);
     if (rc) return rc;
     std::unique_ptr<msv_grid> guard(g);
+    const auto t1 = std::chrono::steady_clock::now();
     rc = grid_launch(g);
     if (rc) return rc;
+    const auto t2 = std::chrono::steady_clock::now();
     std::vector<int64_t> retry;
     rc = grid_results(g, results, usage, nullptr, &retry);
     if (rc) return rc;
+    if (host_timing) {
+        const auto t3 = std::chrono::steady_clock::now();
+        auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
+        fprintf(stderr, "[msv] run_grid n=%lld build %.2f ms, enqueue %.2f ms, results+sync %.2f ms\n",
+                (long long)n, ms(t0, t1), ms(t1, t2), ms(t2, t3));
+    }
     // Traces longer than the Poisson-tail capacity (a >10-sigma Poisson count):
     // rerun those scenarios alone with the capacity quadrupled until they fit.
     std::vector<int64_t> caps_prev;

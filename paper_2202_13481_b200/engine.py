@@ -276,6 +276,14 @@ _REPLAY_DIST = BatchDistribution(np.ones(1))
 # ---------------------------------------------------------------------------
 # device context
 # ---------------------------------------------------------------------------
+@dataclass
+class PreparedGrid:
+    """A grid's msv_scenario array (include/msv.h), marshalled once for repeated calls."""
+    array: object
+    n: int
+    n_partitions: int
+
+
 class Engine:
     """One msv_ctx: a CUDA device, its memory and stream."""
 
@@ -393,8 +401,16 @@ class Engine:
         return arr
 
     # ---- hot path ----
-    def run_grid(self, specs: Sequence[GridSpec], tail_p: Sequence[float] = (0.95, 0.99), usage: bool = False
-                 ) -> dict:
+    def run_grid(self, specs, tail_p: Sequence[float] = (0.95, 0.99), usage: bool = False) -> dict:
+        """One msv_run_grid call. `specs` is a list of GridSpec, or the msv_scenario array
+        Engine.scenarios() built from one (the C-ABI input, marshalled once)."""
+        if isinstance(specs, PreparedGrid):
+            sc, n, n_use = specs.array, specs.n, specs.n_partitions
+            ps = _arr(list(tail_p) or [0.5], np.float64)
+            res = (N.Result * max(n, 1))()
+            use = (N.Usage * max(n_use, 1))() if usage else None
+            check(self._lib.msv_run_grid(self._h, sc, n, _ptr(ps, C.c_double), len(tail_p), res, use), "run_grid")
+            return results_to_numpy(res, n, len(tail_p), use, n_use)
         sc = self.scenarios(specs)
         n = len(specs)
         ps = _arr(list(tail_p) or [0.5], np.float64)
@@ -517,6 +533,9 @@ class Engine:
         if want_t_wait:
             return chosen[:n], kind[:n], tw[: len(ids)]
         return chosen[:n], kind[:n]
+
+    def prepare(self, specs: Sequence[GridSpec]) -> PreparedGrid:
+        return PreparedGrid(self.scenarios(specs), len(specs), sum(s.plan.total_instances() for s in specs))
 
     def paris_batch(self, jobs: Sequence[ParisJob]) -> list[ParisOutcome]:
         """Batched paris_plan on the device (K4, msv_paris_batch): one warp per job."""

@@ -1,0 +1,160 @@
+#!/usr/bin/env python3
+"""Summarise ncu captures of the bench command into profiles/<round>/.
+
+    python tools/summarize_profiles.py r01 gpurun_out/r01/full.ncu-rep [more.ncu-rep ...] \
+        --launches gpurun_out/r01/launches.csv --bench gpurun_out/r01/bench.log \
+        --reference gpurun_out/r01/bench_ref.log
+
+Writes <kernel>_raw.csv (ncu --page raw), sim_opcodes.csv (SASS opcode histogram of
+K2 from the source page), launches_bench.csv and summary.json with per-launch figures
+(duration, warp instructions per query, issue utilisation, DRAM bytes per launch and
+per query) and each kernel's share of the launch list. Per-launch times under ncu are
+serialised and cold-cache: the shares, not the absolutes, compare with bench.py.
+"""
+from __future__ import annotations
+
+import argparse
+import collections
+import csv
+import io
+import json
+import re
+import shutil
+import subprocess
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parents[1]
+SHORT = {"trace_gen_kernel": "K1 trace_gen_kernel", "sim_warp_kernel": "K2 sim_warp_kernel",
+         "sim_kernel": "K2 sim_kernel (segmented)", "tail_kernel": "K3 tail_kernel", "paris_kernel": "K4 paris_kernel"}
+METRICS = {
+    "duration_ms": "gpu__time_duration.sum",
+    "warp_instructions": "smsp__inst_executed.sum",
+    "issue_active_pct": "smsp__issue_active.avg.pct_of_peak_sustained_active",
+    "dram_read": "dram__bytes_read.sum",
+    "dram_write": "dram__bytes_write.sum",
+    "registers": "launch__registers_per_thread",
+    "warps_active_per_sm": "sm__warps_active.avg.per_cycle_active",
+    "grid": "launch__grid_size",
+    "threads_per_instruction": "smsp__thread_inst_executed_per_inst_executed.ratio",
+}
+UNIT = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12, "ms": 1, "us": 1e-3, "ns": 1e-6}
+
+
+def ncu_csv(rep: Path, *args) -> list[list[str]]:
+    out = subprocess.run(["ncu", "-i", str(rep), *args, "--csv"], capture_output=True, text=True, check=True).stdout
+    return list(csv.reader(io.StringIO(out)))
+
+
+def short(name: str) -> str:
+    for k, v in SHORT.items():
+        if re.search(rf"\b{k}\b", name):
+            return v
+    return name
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("round")
+    ap.add_argument("reps", nargs="+", type=Path)
+    ap.add_argument("--launches", type=Path)
+    ap.add_argument("--bench", type=Path)
+    ap.add_argument("--reference", type=Path)
+    ap.add_argument("--queries-per-launch", type=float, default=None,
+                    help="simulated queries one K1/K2 launch covers (default: from the bench line)")
+    a = ap.parse_args()
+    out = ROOT / "profiles" / a.round
+    out.mkdir(parents=True, exist_ok=True)
+    bench = None
+    if a.bench and a.bench.exists():
+        lines = [l for l in a.bench.read_text().splitlines() if l.startswith("{")]
+        bench = json.loads(lines[-1]) if lines else None
+        if bench:
+            (out / "bench_line.json").write_text(json.dumps(bench, indent=1) + "\n")
+    if a.reference and a.reference.exists():
+        lines = [l for l in a.reference.read_text().splitlines() if l.startswith("{")]
+        if lines:
+            (out / "bench_reference_line.json").write_text(json.dumps(json.loads(lines[-1]), indent=1) + "\n")
+    qpl = a.queries_per_launch
+    if qpl is None and bench:
+        cfg = bench["config"]
+        launches_per_step = bench["gpu_launches"] / bench["steps"]
+        qpl = cfg["scenarios_per_gpu"] * cfg["queries_per_scenario"] / (launches_per_step / 3.0)
+    kernels = {}
+    for rep in a.reps:
+        rows = ncu_csv(rep, "--page", "raw")
+        head, units = rows[0], rows[1]
+        for r in rows[2:]:
+            name = short(r[head.index("Kernel Name")])
+            if name in kernels:
+                continue
+            k = {"kernel": r[head.index("Kernel Name")]}
+            for key, m in METRICS.items():
+                if m not in head:
+                    continue
+                i = head.index(m)
+                try:
+                    v = float(r[i].replace(",", ""))
+                except ValueError:
+                    continue
+                if key.startswith("dram"):
+                    v *= UNIT.get(units[i], 1)
+                elif key == "duration_ms":
+                    v *= UNIT.get(units[i], 1) if units[i] != "ms" else 1
+                k[key] = v
+            if not k.get("warp_instructions", 0.0) == k.get("warp_instructions", 0.0):
+                continue  # an incomplete capture (NaN counters): take the kernel from another report
+            if "dram_read" in k and "dram_write" in k:
+                k["traffic_bytes_per_launch"] = k["dram_read"] + k["dram_write"]
+                if qpl:
+                    k["traffic_bytes_per_query"] = k["traffic_bytes_per_launch"] / (
+                        qpl * (0.9 if name.startswith("K3") else 1.0))
+            if qpl and "warp_instructions" in k:
+                k["warp_instructions_per_query"] = k["warp_instructions"] / qpl
+            kernels[name] = k
+            with open(out / f"{name.split()[0].lower()}_raw.csv", "w", newline="") as f:
+                csv.writer(f).writerows([head, units, r])
+        if any(short(r[head.index("Kernel Name")]).startswith("K2") for r in rows[2:]):
+            src = ncu_csv(rep, "--page", "source", "--print-source", "cuda,sass")
+            ops, tot = collections.Counter(), 0
+            for r in src:
+                if len(r) > 8 and r[0] == "" and r[2].startswith("0x"):
+                    try:
+                        n = int(r[7])
+                    except ValueError:
+                        continue
+                    s = re.sub(r"^@!?U?P\w+\s+", "", r[3].strip())
+                    ops[s.split()[0] if s else "?"] += n
+                    tot += n
+            with open(out / "sim_opcodes.csv", "w", newline="") as f:
+                w = csv.writer(f)
+                w.writerow(["opcode", "warp_instructions", "share", "per_query"])
+                for o, n in ops.most_common():
+                    w.writerow([o, n, round(n / tot, 5), round(n / qpl, 3) if qpl else ""])
+    shares = {}
+    if a.launches and a.launches.exists():
+        shutil.copy(a.launches, out / "launches_bench.csv")
+        tot = collections.defaultdict(float)
+        cnt = collections.Counter()
+        for r in csv.reader(open(a.launches)):
+            if len(r) > 10 and r[0].isdigit() and r[-3] == "gpu__time_duration.sum":
+                k = short(r[4])
+                tot[k] += float(r[-1].replace(",", ""))
+                cnt[k] += 1
+        s = sum(tot.values())
+        shares = {k: {"launches": cnt[k], "total_ms": round(v / 1e6, 3), "share": round(v / s, 4)}
+                  for k, v in tot.items()}
+    summary = {
+        "note": "ncu --set full --clock-control none captures of `python bench.py --no-cpu-baseline --steps 1 "
+                "--warmup 3` (default grid: 10,240 scenarios x 1e5 queries, two chunks per step) on one B200; "
+                "per-launch figures. ncu times are serialised / cold-cache: compare shares, not absolutes.",
+        "queries_per_launch": qpl,
+        "issue_peak_warp_inst_per_s": "148 SMs x 4 schedulers x SM clock (1 warp-instruction / scheduler / clk)",
+        "kernels": kernels,
+        "launch_shares_bench": shares,
+    }
+    (out / "summary.json").write_text(json.dumps(summary, indent=1) + "\n")
+    print(json.dumps(summary, indent=1))
+
+
+if __name__ == "__main__":
+    main()
