@@ -9,7 +9,7 @@ import re
 from pathlib import Path
 
 PKG = Path(__file__).resolve().parent
-LIB_PATH = PKG / "libmsv.so"
+LIB_PATH = Path(os.environ["MSV_LIB"]) if os.environ.get("MSV_LIB") else PKG / "libmsv.so"  # MSV_LIB: A/B builds
 HEADER = PKG.parent / "include" / "msv.h"
 
 MSV_OK, MSV_PARAM, MSV_FORMAT, MSV_VALIDATION, MSV_LOOKUP, MSV_INFEASIBLE, MSV_CUDA = range(7)

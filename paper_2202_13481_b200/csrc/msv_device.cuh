@@ -13,6 +13,44 @@ namespace msv {
 constexpr unsigned kFull = 0xffffffffu;
 constexpr uint64_t kSignBit = 1ull << 63;
 
+// Explicit 32-bit shared-memory addressing. `opaque` hides a value's provenance from
+// the compiler so a per-lane shared base stays in one register instead of being
+// re-derived from special registers (SR_TID, SR_CgaCtaId) at every use.
+__device__ __forceinline__ uint32_t opaque(uint32_t x) {
+    asm volatile("" : "+r"(x));
+    return x;
+}
+__device__ __forceinline__ uint32_t smem_addr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ double lds_f64(uint32_t a) {
+    double v;
+    asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ uint64_t lds_u64(uint32_t a) {
+    uint64_t v;
+    asm volatile("ld.shared.u64 %0, [%1];" : "=l"(v) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ int32_t lds_s32(uint32_t a) {
+    int32_t v;
+    asm volatile("ld.shared.s32 %0, [%1];" : "=r"(v) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ uint32_t lds_u32(uint32_t a) {
+    uint32_t v;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ void sts_f64(uint32_t a, double v) {
+    asm volatile("st.shared.f64 [%0], %1;" ::"r"(a), "d"(v) : "memory");
+}
+__device__ __forceinline__ void sts_u64(uint32_t a, uint64_t v) {
+    asm volatile("st.shared.u64 [%0], %1;" ::"r"(a), "l"(v) : "memory");
+}
+__device__ __forceinline__ void sts_u32(uint32_t a, uint32_t v) {
+    asm volatile("st.shared.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+
 // Order-preserving map of IEEE doubles onto uint64 (total order of finite values).
 __device__ __forceinline__ uint64_t order_key(uint64_t b) { return (b & kSignBit) ? ~b : (b | kSignBit); }
 __device__ __forceinline__ uint64_t order_unkey(uint64_t k) { return (k & kSignBit) ? (k & ~kSignBit) : ~k; }
