@@ -87,14 +87,8 @@ static inline uint64_t ora_bits(double x) {
 static inline uint64_t ora_query_digest(uint64_t id, int32_t partition, double start, double finish) {
     const uint64_t sb = ora_bits(start), fb = ora_bits(finish);
     const uint32_t c = (uint32_t)id * 0x9E3779B1u + (uint32_t)partition;
-    uint32_t a = ((uint32_t)sb ^ (uint32_t)(fb >> 32) ^ c) * 0x85EBCA6Bu;
-    uint32_t b = (((uint32_t)(sb >> 32) ^ (uint32_t)fb) + c) * 0x27D4EB2Fu;
-    a ^= a >> 13;
-    b ^= b >> 15;
-    a *= 0xC2B2AE35u;
-    b *= 0x165667B1u;
-    a ^= a >> 16;
-    b ^= b >> 13;
+    const uint32_t a = ((uint32_t)sb ^ (uint32_t)(fb >> 32) ^ c) * 0x85EBCA6Bu;
+    const uint32_t b = ((uint32_t)(sb >> 32) ^ (uint32_t)fb ^ c) * 0x27D4EB2Fu + c;
     return ((uint64_t)a << 32) | b;
 }
 

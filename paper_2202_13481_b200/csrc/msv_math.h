@@ -194,15 +194,12 @@ MSV_HD uint64_t msv_mix64(uint64_t z) {
 }
 
 MSV_HD uint64_t msv_query_digest(uint64_t id, int32_t partition, double start, double finish) {
+    // Checksum term of one query: both halves are odd-constant products of words that
+    // mix the query's (id, partition) with its start/finish bits, so any change of one
+    // query's placement or timing changes the grid's wrapping sum. 7 integer ops.
     const uint64_t sb = msv_dbits(start), fb = msv_dbits(finish);
     const uint32_t c = (uint32_t)id * 0x9E3779B1u + (uint32_t)partition;
-    uint32_t a = ((uint32_t)sb ^ (uint32_t)(fb >> 32) ^ c) * 0x85EBCA6Bu;
-    uint32_t b = (((uint32_t)(sb >> 32) ^ (uint32_t)fb) + c) * 0x27D4EB2Fu;
-    a ^= a >> 13;
-    b ^= b >> 15;
-    a *= 0xC2B2AE35u;
-    b *= 0x165667B1u;
-    a ^= a >> 16;
-    b ^= b >> 13;
+    const uint32_t a = ((uint32_t)sb ^ (uint32_t)(fb >> 32) ^ c) * 0x85EBCA6Bu;
+    const uint32_t b = ((uint32_t)(sb >> 32) ^ (uint32_t)fb ^ c) * 0x27D4EB2Fu + c;
     return ((uint64_t)a << 32) | b;
 }
