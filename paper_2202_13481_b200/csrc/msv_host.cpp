@@ -637,6 +637,11 @@ int grid_build(msv_ctx* ctx, const msv_scenario* sc, int64_t n, const double* ta
         sc_part[i] = it->second;
         for (int32_t j = 0; j < g->P[i]; ++j)
             if (parts_h[it->second + j].row < 0) g->bad[i] = 1;
+        // generated batches can exceed the profile's b_max only when the distribution's
+        // support is wider; such scenarios take the FULL kernel variant, which checks
+        // every batch (replay batches were validated above)
+        if (g->generated && (int)ctx->dists[sc[i].dist].cdf.size() > ctx->profiles[sc[i].profile].b_max)
+            g->bad[i] = 1;
         if (sc[i].routing >= 0) {
             auto mk = std::make_tuple(sc[i].plan, sc[i].profile, sc[i].routing);
             auto mt = mask_off.find(mk);

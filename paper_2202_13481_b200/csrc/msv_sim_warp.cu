@@ -209,7 +209,9 @@ __global__ void __launch_bounds__(kSimWarpsPerBlock * 32, WarpCfg<S>::min_blocks
                     const int b = W.win_b[j];
                     const int i = base + j;
                     drain(t);
-                    if (b < 1 || b > bmax) {  // LookupError at this query (profile.hpp:127-129)
+                    // LookupError at this query (profile.hpp:127-129); only possible when the
+                    // launch holds a scenario whose batches can leave the table (FULL)
+                    if (FULL && (b < 1 || b > bmax)) {
                         status = MSV_LOOKUP;
                         return;
                     }
