@@ -112,9 +112,10 @@ __global__ void __launch_bounds__(kSimWarpsPerBlock * 32, WarpCfg<S>::min_blocks
 
         // Exact left fold of slot s's FIFO (sched.hpp:78-79): ring part, then overflow list.
         auto refold = [&](int s) {
-            double acc = 0.0;
+            if (qn[s] == 0) return 0.0;  // (an overflow list implies a full ring)
+            double acc = W.q_est[s][qh[s]][lane];  // 0.0 + e == e exactly (e > 0)
 #pragma unroll 1
-            for (int k = 0; k < qn[s]; ++k) acc = acc + W.q_est[s][(qh[s] + k) & (QC - 1)][lane];
+            for (int k = 1; k < qn[s]; ++k) acc = acc + W.q_est[s][(qh[s] + k) & (QC - 1)][lane];
             if (gn[s] > 0) {
                 uint32_t g = W.g_head[s][lane];
 #pragma unroll 1
