@@ -105,7 +105,6 @@ __global__ void __launch_bounds__(kSimWarpsPerBlock * 32, WarpCfg<S>::min_blocks
             c_meta[s] = 0;
         }
         uint32_t viol = 0, mviol = 0;
-        uint32_t khi_min = ~0u, khi_max = 0;  // coarse key range of the samples, for K3
         uint64_t hash = 0;
         double wdiff = 0.0;
         int m0 = -1, status = 0;
@@ -145,9 +144,6 @@ __global__ void __launch_bounds__(kSimWarpsPerBlock * 32, WarpCfg<S>::min_blocks
                     if (c_arr[s] >= warmup) {
                         mviol += met ? 0u : 1u;
                         samples[(uint32_t)q - (uint32_t)m0] = lat;
-                        const uint32_t kh = (uint32_t)(msv_dbits(lat) >> 32) | 0x80000000u;  // order key, high word
-                        khi_min = kh < khi_min ? kh : khi_min;
-                        khi_max = kh > khi_max ? kh : khi_max;
                     }
                     hash += msv_query_digest(q, pk[s] & 0xff, c_start[s], now);
                     if (REC) {
@@ -386,8 +382,6 @@ __global__ void __launch_bounds__(kSimWarpsPerBlock * 32, WarpCfg<S>::min_blocks
         const uint64_t hsum = seg_sum_u64<32>(hash, kFull);
         lf = seg_max_f64<32>(lf, kFull);
         const double wd = seg_max_f64<32>(wdiff, kFull);
-        khi_min = __reduce_min_sync(kFull, khi_min);
-        khi_max = __reduce_max_sync(kFull, khi_max);
         if (lane == 0) {
             DevOut o;
             o.violations = (int64_t)v0;
@@ -397,8 +391,10 @@ __global__ void __launch_bounds__(kSimWarpsPerBlock * 32, WarpCfg<S>::min_blocks
             o.horizon_ms = (d.duration_ms < lf) ? lf : d.duration_ms;  // engine.hpp:237
             o.max_wait_diff = wd;
             o.hash = hsum;
-            o.lat_min_bits = (uint64_t)khi_min << 32;  // bounds every sample's order key
-            o.lat_max_bits = ((uint64_t)khi_max << 32) | 0xffffffffull;
+            // key range of non-negative latencies: [+0.0, +inf] (K3's first pass
+            // splits on the exponent)
+            o.lat_min_bits = kSignBit;
+            o.lat_max_bits = 0xFFF0000000000000ull;
             o.status = status;
             o.pad = 0;
             p.out[sidx] = o;
