@@ -169,6 +169,7 @@ def main():
 
     # ---- device-resident throughput (value) ----
     grid = eng.grid(specs, (0.95, 0.99))
+    grid.set_usage(False)  # the metric needs counts and tails, not per-partition usage
     for _ in range(args.warmup):
         grid.launch()
     eng.synchronize()

@@ -232,6 +232,10 @@ int64_t msv_grid_queries(msv_grid* grid);   /* simulated queries of one launch *
 /* Chunks of a large grid run on concurrent streams by default (on = 1); with on = 0
  * the stages run back to back and msv_grid_timing reports each stage. */
 int msv_grid_set_overlap(msv_grid* grid, int on);
+/* Per-partition usage (busy / weighted busy / queries, engine.hpp:57-62) is accumulated
+ * by default (on = 1); with on = 0 the launch skips it and msv_grid_results must be
+ * called with usage = NULL. msv_run_grid accumulates usage only when asked for it. */
+int msv_grid_set_usage(msv_grid* grid, int on);
 int msv_synchronize(msv_ctx* ctx);
 int64_t msv_kernel_launches(msv_ctx* ctx); /* kernels launched by this context so far */
 /* CUDA events on the context stream (slots 0..7) for timing loops of launches. */

@@ -125,6 +125,7 @@ _SIGNATURES = {
                                   C.POINTER(C.c_float)]),
     "msv_grid_queries": (C.c_int64, [_P]),
     "msv_grid_set_overlap": (C.c_int, [_P, C.c_int]),
+    "msv_grid_set_usage": (C.c_int, [_P, C.c_int]),
     "msv_synchronize": (C.c_int, [_P]),
     "msv_kernel_launches": (C.c_int64, [_P]),
     "msv_event_record": (C.c_int, [_P, C.c_int]),

@@ -294,6 +294,7 @@ struct msv_grid {
     };
     std::vector<int32_t> launch_order;  // scenario index of each launch slot
     bool overlap = true;                // chunks on concurrent streams
+    bool usage = true;                  // accumulate per-partition usage (msv_grid_set_usage)
     std::vector<Wave> waves;
     int64_t max_wave_q = 0;
     GridBufs own;            // buffers of a persistent grid (msv_grid_create)
@@ -790,12 +791,13 @@ int launch_chunk(msv_grid* g, const msv_grid::Chunk& ch, int counter_base, cudaS
         p.util = g->B->d_gutil.as<double>();
         p.n_cells = g->n_cells;
         p.any_routing = p.any_bad = p.any_check_wait = 0;
+        p.any_usage = g->usage ? 1 : 0;
         for (int32_t si : ch.classes[c].second) {
             if (g->scen[si].routing >= 0) p.any_routing = 1;
             if (g->bad[si]) p.any_bad = 1;
             if (g->scen[si].flags & MSV_FLAG_CHECK_WAIT) p.any_check_wait = 1;
         }
-        const bool full = g->records || p.any_routing || p.any_bad || p.any_check_wait;
+        const bool full = g->records || p.any_routing || p.any_bad || p.any_check_wait || p.any_usage;
         const int occ = msv::sim_max_blocks_per_sm(k.W, k.S, k.sched, g->records, full, g->n_cells);
         if (occ <= 0) return fail(MSV_CUDA, "sim kernel: no occupancy for class");
         const int segs_per_block = msv::kSimWarpsPerBlock * (32 / k.W);
@@ -888,6 +890,8 @@ int grid_launch(msv_grid* g) {
 
 int grid_results(msv_grid* g, msv_result* res, msv_usage* usage, msv_record* records,
                  std::vector<int64_t>* retry_trace) {
+    if (usage && !g->usage && g->usage_total)
+        return fail(MSV_PARAM, "grid: launched without usage accumulation (msv_grid_set_usage)");
     msv_ctx* ctx = g->ctx;
     MSV_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
     const int64_t n = g->n;
@@ -1191,6 +1195,12 @@ int msv_grid_timing(msv_grid* g, float* total_ms, float* trace_ms, float* sim_ms
     return MSV_OK;
 }
 
+int msv_grid_set_usage(msv_grid* g, int on) {
+    if (!g) return fail(MSV_PARAM, "null grid");
+    g->usage = on != 0;
+    return MSV_OK;
+}
+
 int msv_grid_set_overlap(msv_grid* g, int on) {
     if (!g) return fail(MSV_PARAM, "null grid");
     g->overlap = on != 0;
@@ -1251,6 +1261,7 @@ int msv_run_grid(msv_ctx* ctx, const msv_scenario* scenarios, int64_t n, const d
     int rc = grid_build(ctx, scenarios, n, tail_p, n_tails, nullptr, nullptr, nullptr, false, &g, nullptr, true);
     if (rc) return rc;
     std::unique_ptr<msv_grid> guard(g);
+    g->usage = usage != nullptr;
     const auto t1 = std::chrono::steady_clock::now();
     rc = grid_launch(g);
     if (rc) return rc;
@@ -1282,6 +1293,7 @@ int msv_run_grid(msv_ctx* ctx, const msv_scenario* scenarios, int64_t n, const d
                         caps.data());
         if (rc) return rc;
         std::unique_ptr<msv_grid> guard2(g2);
+        g2->usage = usage != nullptr;
         rc = grid_launch(g2);
         if (rc) return rc;
         usage_n = g2->usage_total;

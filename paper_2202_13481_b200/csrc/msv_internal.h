@@ -85,6 +85,7 @@ struct SimParams {
     int32_t any_routing;     // some scenario uses segment routing
     int32_t any_bad;         // some plan has a size the profile lacks
     int32_t any_check_wait;  // some scenario sets MSV_FLAG_CHECK_WAIT
+    int32_t any_usage;       // per-partition usage (PartitionUsage) requested
 };
 
 // Trace generation job (sample_trace, workload.hpp:97-113).

@@ -410,7 +410,7 @@ int sim_max_blocks_per_sm(int W, int S, int sched, bool records, bool full, int 
 }
 
 cudaError_t launch_sim(int W, int S, int sched, bool records, const SimParams& p, int blocks, cudaStream_t stream) {
-    const bool full = records || p.any_routing || p.any_bad || p.any_check_wait;
+    const bool full = records || p.any_routing || p.any_bad || p.any_check_wait || p.any_usage;
     void* fn = sim_fn_for(W, S, sched, records, full);
     if (!fn) return cudaErrorInvalidValue;
     const size_t smem = sim_smem_bytes(W, S, p.n_cells);

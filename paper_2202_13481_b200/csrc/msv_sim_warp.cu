@@ -137,9 +137,11 @@ __global__ void __launch_bounds__(kSimWarpsPerBlock * 32, WarpCfg<S>::min_blocks
                     const double ran = now - c_start[s];
                     const uint64_t q = c_meta[s] & kQid;
                     const int cb = (int)(c_meta[s] >> 40);
-                    bms[s] = bms[s] + ran;
-                    wbms[s] = wbms[s] + ran * s_util[row[s] + cb - 1];
-                    nq[s] += 1;
+                    if (FULL) {  // PartitionUsage (engine.hpp:175-177); plain launches skip it
+                        bms[s] = bms[s] + ran;
+                        wbms[s] = wbms[s] + ran * s_util[row[s] + cb - 1];
+                        nq[s] += 1;
+                    }
                     viol += met ? 0u : 1u;
                     if (c_arr[s] >= warmup) {
                         mviol += met ? 0u : 1u;
@@ -373,10 +375,11 @@ __global__ void __launch_bounds__(kSimWarpsPerBlock * 32, WarpCfg<S>::min_blocks
         drain(INFINITY);  // after the last arrival: drain everything, no horizon cut-off
 
         // ---- publish (engine.hpp:233-252) ----
-        double lf = 0.0;  // last completion = each lane's final c_comp (completions per lane ascend)
+        // last completion = each slot's final c_comp (completions per slot ascend; a slot
+        // that never ran keeps 0.0, below every completion and the duration)
+        double lf = 0.0;
 #pragma unroll
-        for (int s = 0; s < S; ++s)
-            if (nq[s] > 0) lf = (lf < c_comp[s]) ? c_comp[s] : lf;
+        for (int s = 0; s < S; ++s) lf = (lf < c_comp[s]) ? c_comp[s] : lf;
         const uint64_t v0 = seg_sum_u64<32>((uint64_t)viol, kFull);
         const uint64_t v2 = seg_sum_u64<32>((uint64_t)mviol, kFull);
         const uint64_t hsum = seg_sum_u64<32>(hash, kFull);
@@ -399,7 +402,7 @@ __global__ void __launch_bounds__(kSimWarpsPerBlock * 32, WarpCfg<S>::min_blocks
             o.pad = 0;
             p.out[sidx] = o;
         }
-        if (d.usage_off >= 0) {
+        if (FULL && p.any_usage && d.usage_off >= 0) {
 #pragma unroll
             for (int s = 0; s < S; ++s) {
                 if (act[s]) {

@@ -635,6 +635,9 @@ class DeviceGrid:
     def set_overlap(self, on: bool) -> None:
         check(self.eng._lib.msv_grid_set_overlap(self._g, 1 if on else 0), "msv_grid_set_overlap")
 
+    def set_usage(self, on: bool) -> None:
+        check(self.eng._lib.msv_grid_set_usage(self._g, 1 if on else 0), "msv_grid_set_usage")
+
     def results(self, usage: bool = False) -> dict:
         n = len(self.specs)
         res = (N.Result * max(n, 1))()
