@@ -207,6 +207,20 @@ __global__ void __launch_bounds__(kSimWarpsPerBlock * 32, WarpCfg<S>::min_blocks
                     const double t = W.win_t[j];
                     const int b = W.win_b[j];
                     const int i = base + j;
+                    // The new query's latency on each partition depends on its batch only:
+                    // load it ahead of the drain (FULL: batch clamped into the table for
+                    // the load, missing sizes read 0).
+                    double est_n[S];
+#pragma unroll
+                    for (int s = 0; s < S; ++s) {
+                        if (FULL) {
+                            const int bl = min(max(b, 1), bmax);
+                            est_n[s] = s_lat[(row[s] < 0 ? 0 : row[s]) + bl - 1];
+                            if (row[s] < 0) est_n[s] = 0.0;
+                        } else {
+                            est_n[s] = s_lat[row[s] + b - 1];
+                        }
+                    }
                     drain(t);
                     // LookupError at this query (profile.hpp:127-129); only possible when the
                     // launch holds a scenario whose batches can leave the table (FULL)
@@ -216,14 +230,12 @@ __global__ void __launch_bounds__(kSimWarpsPerBlock * 32, WarpCfg<S>::min_blocks
                     }
                     // ---- candidates and Eq. 1 waits (sched.hpp:77-85) ----
                     bool cand[S];
-                    double est_n[S], wv[S];
+                    double wv[S];
 #pragma unroll
                     for (int s = 0; s < S; ++s) {
                         cand[s] = act[s];
                         const double x = c_est[s] - (t - c_start[s]);
                         wv[s] = fold[s] + ((busy[s] && 0.0 < x) ? x : 0.0);
-                        if (FULL) est_n[s] = row[s] >= 0 ? s_lat[row[s] + b - 1] : 0.0;
-                        else est_n[s] = s_lat[row[s] + b - 1];
                     }
                     int bad_o = 1 << 30;  // order index of the first candidate whose size is missing
                     if (FULL) {
@@ -260,7 +272,27 @@ __global__ void __launch_bounds__(kSimWarpsPerBlock * 32, WarpCfg<S>::min_blocks
                     // ---- decision ----
                     int ch = -1;  // chosen order index
                     int kind;
-                    if constexpr (SCHED == MSV_ELSA) {
+                    bool mine[S];  // this lane's slot s is the chosen partition
+                    if constexpr (SCHED == MSV_ELSA && S == 1 && !FULL) {
+                        // One slot per lane: the chosen lane is the lowest set bit of the
+                        // ballot, i.e. the lane with no set bit below it — no bit scan on the
+                        // critical path.
+                        const unsigned below = (1u << lane) - 1u;
+                        bool pred;
+                        if constexpr (UNIT) pred = act[0] && (sla > wv[0] + est_n[0]);
+                        else pred = act[0] && (sla > alpha * (wv[0] + beta * est_n[0]));
+                        const unsigned bA = __ballot_sync(kFull, pred);  // Step A (sched.hpp:125-130)
+                        mine[0] = pred && (bA & below) == 0;
+                        kind = MSV_SLACK_SATISFYING;
+                        if (bA == 0) {  // Step B (sched.hpp:132-142): argmin w + est, earliest on ties
+                            const uint64_t fb = act[0] ? msv_dbits(wv[0] + est_n[0]) : ~0ull;
+                            const uint64_t vmin = seg_min_u64<32>(fb);
+                            const bool hit = fb == vmin && vmin != ~0ull;
+                            const unsigned bB = __ballot_sync(kFull, hit);
+                            mine[0] = hit && (bB & below) == 0;
+                            kind = MSV_FASTEST_FALLBACK;
+                        }
+                    } else if constexpr (SCHED == MSV_ELSA) {
                         // Step A (sched.hpp:125-130): first in order with sla > alpha*(w + beta*est).
 #pragma unroll
                         for (int s = S - 1; s >= 0; --s) {
@@ -333,10 +365,14 @@ __global__ void __launch_bounds__(kSimWarpsPerBlock * 32, WarpCfg<S>::min_blocks
                             }
                         }
                     }
+                    if constexpr (!(SCHED == MSV_ELSA && S == 1 && !FULL)) {
+#pragma unroll
+                        for (int s = 0; s < S; ++s) mine[s] = s * 32 + lane == ch;
+                    }
                     // ---- start or enqueue on the chosen partition (engine.hpp:225-230) ----
 #pragma unroll
                     for (int s = 0; s < S; ++s) {
-                        if (s * 32 + lane == ch) {
+                        if (mine[s]) {
                             const double est = est_n[s];
                             const uint64_t meta = (uint64_t)i | ((uint64_t)b << 40);
                             if (!busy[s]) {
