@@ -216,10 +216,11 @@ struct ClassKey {
     }
 };
 
-constexpr int kMaxChunks = 2;           // concurrent chunks per wave (sweep: 2 best)
-constexpr int64_t kChunkScenarios = 2048;  // smallest chunk worth its own stream
+constexpr int kMaxChunks = 8;           // chunks per wave (pipelined over kAuxStreams streams)
+constexpr int kDefaultChunks = 2;
+constexpr int64_t kChunkScenarios = 1024;  // smallest chunk worth its own launch
 constexpr int kCounterSlots = 1024;      // work-stealing counters per launch (chunk x class)
-constexpr int kAuxStreams = kMaxChunks;
+constexpr int kAuxStreams = 2;
 
 // Kernel class of a plan with P partitions. The one-scenario-per-warp kernel serves
 // every P <= 32 by default (its per-arrival cost barely depends on P). The segmented
@@ -562,7 +563,7 @@ int grid_build(msv_ctx* ctx, const msv_scenario* sc, int64_t n, const double* ta
             n8 += g->P[i] <= 8;
         }
         const int seg_w = wave_seg_width(n4, n8, ctx->sms);
-        int max_chunks = kMaxChunks;
+        int max_chunks = kDefaultChunks;
         if (const char* e = getenv("MSV_MAX_CHUNKS")) max_chunks = std::max(1, std::min(kMaxChunks, atoi(e)));
         const int n_chunks = (int)std::max<int64_t>(1, std::min<int64_t>(max_chunks, ns_w / kChunkScenarios));
         std::vector<std::vector<int32_t>> members(n_chunks);
