@@ -60,6 +60,9 @@ __global__ void __launch_bounds__(kSimWarpsPerBlock * 32, WarpCfg<S>::min_blocks
         s_util[c] = p.util[c];
     }
     __syncthreads();
+    // 32-bit shared address of the latency cells, kept in a register: the per-arrival
+    // lookup must not re-derive the shared window base (S2UR) on its critical path
+    const uint32_t lat_sh = opaque(smem_addr(s_lat));
 
     for (;;) {
         int w = 0;
@@ -218,7 +221,7 @@ __global__ void __launch_bounds__(kSimWarpsPerBlock * 32, WarpCfg<S>::min_blocks
                             est_n[s] = s_lat[(row[s] < 0 ? 0 : row[s]) + bl - 1];
                             if (row[s] < 0) est_n[s] = 0.0;
                         } else {
-                            est_n[s] = s_lat[row[s] + b - 1];
+                            est_n[s] = lds_f64(lat_sh + (uint32_t)(row[s] + b - 1) * 8u);
                         }
                     }
                     drain(t);
