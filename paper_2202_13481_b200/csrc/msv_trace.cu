@@ -20,6 +20,7 @@ __device__ __forceinline__ int32_t cdf_sample(const double* __restrict__ cdf, co
 __global__ void __launch_bounds__(kTraceWarpsPerBlock * 32)
     trace_gen_kernel(const TraceJob* __restrict__ jobs, int n_jobs, int variant) {
     __shared__ uint64_t s_mt[kTraceWarpsPerBlock][MSV_MT_N];
+    __shared__ __align__(16) double s_acc[kTraceWarpsPerBlock][32];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int job = blockIdx.x * kTraceWarpsPerBlock + warp;
     if (job >= n_jobs) return;
@@ -77,12 +78,25 @@ __global__ void __launch_bounds__(kTraceWarpsPerBlock * 32)
                 const double ub = msv_uniform(msv_mt_temper(mt[2 * p + 1]));
                 bt = cdf_sample(J.cdf, J.guide, J.b_max, ub);
             }
-            double acc = (lane == 0) ? t + g : 0.0;
+            // the 32 sequential sums run in lane 0 out of shared memory (two gaps per
+            // 16-byte load), then every lane picks its own arrival up again
+            double* sa = s_acc[warp];
+            sa[lane] = g;
+            __syncwarp();
+            if (lane == 0) {
+                double a = t;
 #pragma unroll
-            for (int k = 1; k < 32; ++k) {
-                const double prev = __shfl_sync(kFull, acc, k - 1);
-                if (lane == k) acc = prev + g;
+                for (int k = 0; k < 32; k += 2) {
+                    double2 v = *reinterpret_cast<const double2*>(sa + k);
+                    a = a + v.x;
+                    v.x = a;
+                    a = a + v.y;
+                    v.y = a;
+                    *reinterpret_cast<double2*>(sa + k) = v;
+                }
             }
+            __syncwarp();
+            const double acc = sa[lane];  // lanes >= nvalid carry g = 0 and are masked below
             // `while (t < duration)`: arrivals are non-decreasing, so the kept ones are a prefix.
             const unsigned keep = __ballot_sync(kFull, lane < nvalid && acc < J.duration_ms);
             const int cnt = (keep == kFull) ? 32 : (__ffs(~keep) - 1);
