@@ -91,7 +91,15 @@ MSV_HD double msv_log1p_neg(double x, int variant) {
         const uint32_t hu0 = (uint32_t)(msv_dbits(u) >> 32);
         k = (int)(hu0 >> 20) - 1023;
         c = (k > 0) ? (1.0 - (u - x)) : (x - (u - 1.0));
-        c = c / u;
+        // c is often exactly +-0 (u = x + 1 exact) and 0 / u == c bit for bit; dividing
+        // a stand-in 1.0 instead keeps the device division off its zero-operand slow path
+        // (the select alone would still evaluate c / u)
+        double cn = (c == 0.0) ? 1.0 : c;
+#ifdef __CUDA_ARCH__
+        asm("" : "+d"(cn));  // keep the compiler from folding the stand-in back into c / u
+#endif
+        const double cq = cn / u;
+        c = (c == 0.0) ? c : cq;
         hu = hu0 & 0x000fffffu;
         const uint64_t lo = msv_dbits(u) & 0xffffffffull;
         double un;
