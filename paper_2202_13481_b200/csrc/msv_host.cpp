@@ -565,9 +565,43 @@ int grid_build(msv_ctx* ctx, const msv_scenario* sc, int64_t n, const double* ta
         const int seg_w = wave_seg_width(n4, n8, ctx->sms);
         int max_chunks = kDefaultChunks;
         if (const char* e = getenv("MSV_MAX_CHUNKS")) max_chunks = std::max(1, std::min(kMaxChunks, atoi(e)));
-        const int n_chunks = (int)std::max<int64_t>(1, std::min<int64_t>(max_chunks, ns_w / kChunkScenarios));
+        int n_chunks = (int)std::max<int64_t>(1, std::min<int64_t>(max_chunks, ns_w / kChunkScenarios));
+        // chunk shares (MSV_CHUNK_SPLIT=f0,f1,...: experiment knob; default equal)
+        // two chunks split 3:1 (sweep on the C2 grid: the small second chunk's simulation
+        // fills the first chunk's tail, its trace generation hides under it)
+        std::vector<double> share(n_chunks, 1.0);
+        if (n_chunks == 2) share[0] = 3.0;
+        if (const char* e = getenv("MSV_CHUNK_SPLIT")) {
+            std::vector<double> f;
+            for (const char* c = e; *c;) {
+                char* end = nullptr;
+                const double v = strtod(c, &end);
+                if (end == c) break;
+                if (v > 0) f.push_back(v);
+                c = (*end == ',') ? end + 1 : end;
+            }
+            if (!f.empty() && (int64_t)f.size() <= ns_w) {
+                share = f;
+                n_chunks = (int)f.size();
+            }
+        }
+        double share_sum = 0.0;
+        for (double v : share) share_sum += v;
+        // proportional interleave in cost order: each scenario goes to the chunk furthest
+        // below its share (equal shares: round robin)
         std::vector<std::vector<int32_t>> members(n_chunks);
-        for (size_t j = 0; j < ord.size(); ++j) members[j % n_chunks].push_back(ord[j]);
+        for (size_t j = 0; j < ord.size(); ++j) {
+            int best = 0;
+            double best_def = -1e300;
+            for (int c = 0; c < n_chunks; ++c) {
+                const double def = share[c] / share_sum * (double)(j + 1) - (double)members[c].size();
+                if (def > best_def + 1e-12) {
+                    best_def = def;
+                    best = c;
+                }
+            }
+            members[best].push_back(ord[j]);
+        }
         for (int c = 0; c < n_chunks; ++c) {
             msv_grid::Chunk ch;
             ch.l0 = (int64_t)g->launch_order.size();
