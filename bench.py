@@ -280,7 +280,7 @@ def main():
         loads = np.tile(np.repeat(np.arange(1, 11) / 10.0, args.seeds), world)
         allp = p99.numpy()
         line["p99_ms_by_load"] = {f"{l:.1f}": round(float(np.mean(allp[loads == l])), 4) for l in np.unique(loads)}
-        if not args.no_cpu_baseline:
+        if not args.no_cpu_baseline and world == 1:  # the CPU reference is timed at N=1 only
             b, ref, idx = cpu_baseline(specs, args.cpu_seconds)
             line["cpu_baseline"] = b
             # the CPU sample doubles as a full-size parity check of the timed device run

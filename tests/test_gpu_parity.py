@@ -204,6 +204,29 @@ def test_device_grid_matches_run_grid(eng):
     assert g.timing()["total_ms"] > 0
 
 
+def test_grid_usage_optional(eng):
+    """Usage accumulation is optional (msv_grid_set_usage / msv_run_grid usage=NULL): the
+    results do not change, usage matches the reference when requested, and asking a
+    usage-free launch for usage is a ParamError."""
+    specs = W.c2(seeds=2, queries=3000)
+    with_use = eng.run_grid(specs, usage=True)
+    without = eng.run_grid(specs)
+    assert_grid_equal(with_use, without)
+    g = eng.grid(specs)
+    g.set_usage(False)
+    g.launch()
+    assert_grid_equal(g.results(), without)
+    with pytest.raises(ParamError):
+        g.results(usage=True)
+    g.set_usage(True)
+    g.launch()
+    r = g.results(usage=True)
+    assert np.array_equal(r["usage"]["busy_ms"], with_use["usage"]["busy_ms"])
+    assert np.array_equal(r["usage"]["weighted_busy_ms"], with_use["usage"]["weighted_busy_ms"])
+    assert np.array_equal(r["usage"]["queries"], with_use["usage"]["queries"])
+    assert int(r["usage"]["queries"].sum()) == int(r["total"].sum())
+
+
 # ---------------------------------------------------------------- tails
 def test_tail_latency_exact(eng, ref):
     rng = np.random.default_rng(3)
