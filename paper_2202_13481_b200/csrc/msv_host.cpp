@@ -222,12 +222,12 @@ constexpr int64_t kChunkScenarios = 1024;  // smallest chunk worth its own launc
 constexpr int kCounterSlots = 1024;      // work-stealing counters per launch (chunk x class)
 constexpr int kAuxStreams = 2;
 
-// Kernel class of a plan with P partitions. The one-scenario-per-warp kernel serves
-// every P <= 32 by default (its per-arrival cost barely depends on P). The segmented
-// kernel (G = 32/W scenarios per warp) halves the instructions per query but keeps
-// only n/G warps busy, so it pays only when the wave holds enough small plans to fill
+// Kernel class of a plan with P partitions. The one-scenario-per-warp kernel (W = 32)
+// serves every plan; the segmented kernel runs G = 32/W scenarios per warp (W lanes
+// each, S slots per lane: P <= W*S) and needs fewer instructions per query, but keeps
+// only n/G warps busy, so it pays only when the wave holds enough such plans to fill
 // the device: `seg_w` is the narrowest segment width the wave can afford (32 = none).
-// MSV_SEGMENTED=0 disables it, =1 forces the narrowest width for every P <= 16.
+// MSV_SEGMENTED=0 disables it, =1 forces the narrowest width that fits each plan.
 int segmented_mode() {
     static const int mode = getenv("MSV_SEGMENTED") ? (atoi(getenv("MSV_SEGMENTED")) != 0 ? 1 : 0) : -1;
     return mode;
@@ -245,15 +245,16 @@ ClassKey class_of(int P, int sched, int seg_w) {
     return c;
 }
 
-// Narrowest segment width worth launching for a wave with n4 plans of P <= 4 and n8
-// of P <= 8 on `sms` SMs: G scenarios per warp must still leave >= half of the
-// segmented kernel's warp slots (6 blocks x 4 warps per SM) busy. W = 16 never
-// pays (two segments cost as much per arrival as one warp-wide scenario).
-int wave_seg_width(int64_t n4, int64_t n8, int sms) {
+// Narrowest segment width worth launching for a wave with n4 / n8 / n16 plans of
+// P <= 4 / 8 / 16 on `sms` SMs: G scenarios per warp must still leave >= half of the
+// segmented kernel's warp slots (~5 blocks x 4 warps per SM) busy. (Two slots per lane
+// for 16 < P <= 32 was measured: more instructions per query than the warp kernel.)
+int wave_seg_width(int64_t n4, int64_t n8, int64_t n16, int sms) {
     if (segmented_mode() == 0) return 32;
-    const int64_t half_slots = (int64_t)sms * 6 * msv::kSimWarpsPerBlock / 2;
+    const int64_t half_slots = (int64_t)sms * 5 * msv::kSimWarpsPerBlock / 2;
     if (n4 / 8 >= half_slots) return 4;
     if (n8 / 4 >= half_slots) return 8;
+    if (n16 / 2 >= half_slots) return 16;
     return 32;
 }
 
@@ -557,12 +558,13 @@ int grid_build(msv_ctx* ctx, const msv_scenario* sc, int64_t n, const double* ta
         for (int64_t i = w.s0; i < w.s1; ++i) ord.push_back((int32_t)i);
         std::stable_sort(ord.begin(), ord.end(), [&](int32_t a, int32_t b) { return cost[a] > cost[b]; });
         const int64_t ns_w = w.s1 - w.s0;
-        int64_t n4 = 0, n8 = 0;
+        int64_t n4 = 0, n8 = 0, n16 = 0;
         for (int64_t i = w.s0; i < w.s1; ++i) {
             n4 += g->P[i] <= 4;
             n8 += g->P[i] <= 8;
+            n16 += g->P[i] <= 16;
         }
-        const int seg_w = wave_seg_width(n4, n8, ctx->sms);
+        const int seg_w = wave_seg_width(n4, n8, n16, ctx->sms);
         int max_chunks = kDefaultChunks;
         if (const char* e = getenv("MSV_MAX_CHUNKS")) max_chunks = std::max(1, std::min(kMaxChunks, atoi(e)));
         int n_chunks = (int)std::max<int64_t>(1, std::min<int64_t>(max_chunks, ns_w / kChunkScenarios));

@@ -1,22 +1,27 @@
 // K2 sim_kernel: run() (engine.hpp:115-253) with ELSA (sched.hpp:119-143) or FIFS
-// (sched.hpp:154-170), segmented variant for plans of P <= W partitions, W in
-// {4, 8, 16}: a warp runs G = 32/W scenarios side by side, one segment of W lanes
-// each, all segments advancing one arrival per iteration (lockstep).
+// (sched.hpp:154-170), segmented variant: a warp runs G = 32/W scenarios side by
+// side, one segment of W lanes each, every lane holding S partition slots, so a plan
+// of P <= W*S partitions fits one segment (W in {4, 8, 16}; instantiated with S = 1:
+// two slots per lane for 16 < P <= 32 measured slower than the warp kernel). Slot s of
+// segment lane l owns by_ascending_size order index s*W + l (sched.hpp:96-104). All
+// segments advance one arrival per iteration (lockstep): every warp instruction of
+// the per-arrival path serves G scenarios.
 //
 // Per arrival (every kernel of K2 follows this protocol):
 //   1. every lane retires its own completions with time <= now, in chain order, with
 //      no warp collective (completions on different partitions commute and a
 //      completion precedes an arrival at equal time, engine.hpp:101-107);
 //   2. every lane evaluates Eq. 1 (t_wait, kept as an exact FIFO fold) and Eq. 2 for
-//      its partition; Step A = first set bit of the segment's ballot bits, Step B =
-//      a shuffle-tree argmin over the segment with order tie-break; FIFS = (k, id) /
-//      (queue length, id) key minima;
-//   3. the chosen lane starts the query or appends it to its FIFO (shared-memory
+//      its slots; Step A = first set bit of the segment's ballot bits over the slots in
+//      order, Step B = a shuffle-tree argmin over the segment with order tie-break;
+//      FIFS = (k, id) / (queue length, id) key minima;
+//   3. the chosen slot starts the query or appends it to its FIFO (shared-memory
 //      ring, overflow list threaded through query ids in global memory).
 // Each segment keeps a double-buffered 32-arrival window in shared memory, refilled
 // by cp.async one window ahead. Measured latencies land at samples[q - m0]
 // (arrivals are sorted, so the measured set is the suffix from the first
-// arrival >= warmup), ready for K3.
+// arrival >= warmup), ready for K3. The plain variant (no routing / missing sizes /
+// wait check / usage / records in the launch) carries none of those features' work.
 #include <cuda_pipeline.h>
 
 #include "msv_device.cuh"
@@ -26,29 +31,38 @@ namespace msv {
 namespace {
 
 constexpr uint64_t kQidMask = (1ull << 40) - 1;
-constexpr int kSegMinBlocks = 6;
 
-template <int W>
-struct SegSmem {
+template <int W, int S>
+struct SegCfg {
     static constexpr int G = 32 / W;
-    double q_est[kQCap][32];
-    double q_arr[kQCap][32];
-    uint64_t q_meta[kQCap][32];
-    double win_t[2][32][G];  // [buffer][entry][segment]
-    int32_t win_b[2][32][G];
-    uint32_t g_head[32];     // overflow list head / tail per lane
-    uint32_t g_tail[32];
+    static constexpr int qcap = S == 1 ? kQCap : 4;  // shared ring entries per slot
+    static constexpr int min_blocks = S == 1 ? 6 : 5;
 };
 
-template <int W, int SCHED, bool REC, bool FULL>
-__global__ void __launch_bounds__(kSimWarpsPerBlock * 32, kSegMinBlocks) sim_kernel(const SimParams p) {
+template <int W, int S>
+struct SegSmem {
+    static constexpr int G = SegCfg<W, S>::G;
+    static constexpr int QC = SegCfg<W, S>::qcap;
+    double q_est[S][QC][32];
+    double q_arr[S][QC][32];
+    uint64_t q_meta[S][QC][32];
+    double win_t[2][32][G];  // [buffer][entry][segment]
+    int32_t win_b[2][32][G];
+    uint32_t g_head[S][32];  // overflow list head / tail per lane slot
+    uint32_t g_tail[S][32];
+};
+
+template <int W, int S, int SCHED, bool REC, bool FULL>
+__global__ void __launch_bounds__(kSimWarpsPerBlock * 32, (SegCfg<W, S>::min_blocks))
+    sim_kernel(const SimParams p) {
+    constexpr int QC = SegCfg<W, S>::qcap;
     constexpr bool kFold = (SCHED == MSV_ELSA) || FULL;
     extern __shared__ __align__(16) unsigned char smem[];
     double* s_lat = reinterpret_cast<double*>(smem);
     double* s_util = s_lat + p.n_cells;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const size_t tab_bytes = ((size_t)2 * p.n_cells * sizeof(double) + 15) & ~(size_t)15;
-    SegSmem<W>& M = reinterpret_cast<SegSmem<W>*>(smem + tab_bytes)[warp];
+    SegSmem<W, S>& M = reinterpret_cast<SegSmem<W, S>*>(smem + tab_bytes)[warp];
     for (int c = threadIdx.x; c < p.n_cells; c += blockDim.x) {
         s_lat[c] = p.lat[c];
         s_util[c] = p.util[c];
@@ -65,18 +79,27 @@ __global__ void __launch_bounds__(kSimWarpsPerBlock * 32, kSegMinBlocks) sim_ker
     const DevScen* d = nullptr;
     const double* g_arr = nullptr;
     const int32_t* g_bat = nullptr;
+    double* samples = nullptr;
     double sla = 0.0, warmup = 0.0, alpha = 1.0, beta = 1.0;
     bool unit = true, check_wait = false;
     int bmax = 0;
-    // ---- per-lane partition slot ----
-    bool act = false, busy = false;
-    int32_t row = 0, pk = 0, qh = 0, qn = 0;
-    uint32_t gn = 0, nq = 0;
-    double c_start = 0.0, c_est = 0.0, c_comp = 0.0, c_arr = 0.0, fold = 0.0, bms = 0.0, wbms = 0.0;
-    uint64_t c_meta = 0;
+    // ---- per-lane partition slots ----
+    bool act[S], busy[S];
+    int32_t row[S], pk[S], qh[S], qn[S];
+    uint32_t gn[S], nq[S];
+    double c_start[S], c_est[S], c_comp[S], c_arr[S], fold[S], bms[S], wbms[S];
+    uint64_t c_meta[S];
     uint32_t viol = 0, mviol = 0;
-    uint64_t hash = 0, lmin = ~0ull, lmax = 0;
+    uint64_t hash = 0;
     double wdiff = 0.0;
+#pragma unroll
+    for (int s = 0; s < S; ++s) {
+        act[s] = busy[s] = false;
+        row[s] = pk[s] = qh[s] = qn[s] = 0;
+        gn[s] = nq[s] = 0;
+        c_start[s] = c_est[s] = c_comp[s] = c_arr[s] = fold[s] = bms[s] = wbms[s] = 0.0;
+        c_meta[s] = 0;
+    }
 
     // Async copy of arrivals [from, from+32) into the segment's window buffer b.
     auto prefetch = [&](int from, int b) {
@@ -89,15 +112,18 @@ __global__ void __launch_bounds__(kSimWarpsPerBlock * 32, kSegMinBlocks) sim_ker
         }
         __pipeline_commit();
     };
-    auto refold = [&]() {
-        double acc = 0.0;
+    // Exact left fold of slot s's FIFO (sched.hpp:78-79), starting from the head entry
+    // (0.0 + e == e); an overflow list implies a full ring.
+    auto refold = [&](int s) {
+        if (qn[s] == 0) return 0.0;
+        double acc = M.q_est[s][qh[s]][lane];
 #pragma unroll 1
-        for (int k = 0; k < qn; ++k) acc = acc + M.q_est[(qh + k) & (kQCap - 1)][lane];
-        if (gn > 0) {
-            uint32_t g = M.g_head[lane];
+        for (int k = 1; k < qn[s]; ++k) acc = acc + M.q_est[s][(qh[s] + k) & (QC - 1)][lane];
+        if (gn[s] > 0) {
+            uint32_t g = M.g_head[s][lane];
 #pragma unroll 1
-            for (uint32_t k = 0; k < gn; ++k) {
-                acc = acc + s_lat[row + g_bat[g] - 1];
+            for (uint32_t k = 0; k < gn[s]; ++k) {
+                acc = acc + s_lat[row[s] + g_bat[g] - 1];
                 g = d->next[g];
             }
         }
@@ -118,6 +144,7 @@ __global__ void __launch_bounds__(kSimWarpsPerBlock * 32, kSegMinBlocks) sim_ker
                 n = (int)*d->n;
                 g_arr = d->arrival;
                 g_bat = d->batch;
+                samples = d->samples;
                 sla = d->sla;
                 warmup = d->warmup_ms;
                 alpha = d->alpha;
@@ -130,24 +157,26 @@ __global__ void __launch_bounds__(kSimWarpsPerBlock * 32, kSegMinBlocks) sim_ker
                 buf = 0;
                 m0 = -1;
                 status = 0;
-                act = sl < d->P;
-                row = 0;
-                pk = 0;
-                if (act) {
-                    const DevPart dp = d->parts[sl];
-                    pk = dp.pid | (dp.k << 8);
-                    row = dp.row;
+#pragma unroll
+                for (int s = 0; s < S; ++s) {
+                    const int o = s * W + sl;
+                    act[s] = o < d->P;
+                    row[s] = 0;  // inactive slots read a valid (ignored) cell
+                    pk[s] = 0;
+                    if (act[s]) {
+                        const DevPart dp = d->parts[o];
+                        pk[s] = dp.pid | (dp.k << 8);
+                        row[s] = dp.row;
+                    }
+                    busy[s] = false;
+                    qh[s] = qn[s] = 0;
+                    gn[s] = nq[s] = 0;
+                    c_start[s] = c_est[s] = c_comp[s] = c_arr[s] = 0.0;
+                    fold[s] = bms[s] = wbms[s] = 0.0;
+                    c_meta[s] = 0;
                 }
-                busy = false;
-                qh = qn = 0;
-                gn = nq = 0;
-                c_start = c_est = c_comp = c_arr = 0.0;
-                fold = bms = wbms = 0.0;
-                c_meta = 0;
                 viol = mviol = 0;
                 hash = 0;
-                lmin = ~0ull;
-                lmax = 0;
                 wdiff = 0.0;
                 prefetch(0, 0);
                 prefetch(32, 1);
@@ -169,7 +198,7 @@ __global__ void __launch_bounds__(kSimWarpsPerBlock * 32, kSegMinBlocks) sim_ker
             prefetch(win_base + 32, buf ^ 1);
         }
         double t = -INFINITY;
-        int b = 0;
+        int b = 1;
         if (arrival) {
             t = M.win_t[buf][i - win_base][seg];
             b = M.win_b[buf][i - win_base][seg];
@@ -177,152 +206,224 @@ __global__ void __launch_bounds__(kSimWarpsPerBlock * 32, kSegMinBlocks) sim_ker
         } else if (ending) {
             t = INFINITY;  // drain everything (no horizon cut-off)
         }
+        // the new query's latency on each slot depends on its batch only: load it ahead
+        // of the drain (FULL: batch clamped into the table, missing sizes read 0)
+        double est_n[S];
+#pragma unroll
+        for (int s = 0; s < S; ++s) {
+            if (FULL) {
+                const int bl = min(max(b, 1), max(bmax, 1));
+                est_n[s] = row[s] >= 0 ? s_lat[row[s] + bl - 1] : 0.0;
+            } else {
+                est_n[s] = s_lat[row[s] + b - 1];
+            }
+        }
 
         // ---- 1. completions with time <= t, lane-local, in chain order ----
-        while (busy && c_comp <= t) {  // engine.hpp:167-187
-            const double now = c_comp;
-            const double lat = now - c_arr;
-            const bool met = lat <= sla;
-            const double ran = now - c_start;
-            const uint64_t q = c_meta & kQidMask;
-            const int cb = (int)(c_meta >> 40);
-            bms = bms + ran;
-            wbms = wbms + ran * s_util[row + cb - 1];
-            nq += 1;
-            viol += met ? 0u : 1u;
-            if (c_arr >= warmup) {
-                mviol += met ? 0u : 1u;
-                d->samples[(uint32_t)q - (uint32_t)m0] = lat;
-                const uint64_t lb = msv_dbits(lat) | kSignBit;  // order key (lat >= 0)
-                lmin = lb < lmin ? lb : lmin;
-                lmax = lb > lmax ? lb : lmax;
-            }
-            hash += msv_query_digest(q, pk & 0xff, c_start, now);
-            if (REC) {
-                d->records[q].start_ms = c_start;
-                d->records[q].finish_ms = now;
-            }
-            if (qn > 0) {  // start the queue head now (engine.hpp:181-185)
-                const double est = M.q_est[qh][lane];
-                c_arr = M.q_arr[qh][lane];
-                c_meta = M.q_meta[qh][lane];
-                qh = (qh + 1) & (kQCap - 1);
-                qn -= 1;
-                if (gn > 0) {  // refill the ring from the overflow list
-                    const uint32_t g = M.g_head[lane];
-                    M.g_head[lane] = d->next[g];
-                    gn -= 1;
-                    const int32_t gb = g_bat[g];
-                    const int e2 = (qh + qn) & (kQCap - 1);
-                    M.q_est[e2][lane] = s_lat[row + gb - 1];
-                    M.q_arr[e2][lane] = g_arr[g];
-                    M.q_meta[e2][lane] = (uint64_t)g | ((uint64_t)gb << 40);
-                    qn += 1;
+#pragma unroll
+        for (int s = 0; s < S; ++s) {
+            while (busy[s] && c_comp[s] <= t) {  // engine.hpp:167-187
+                const double now = c_comp[s];
+                const double lat = now - c_arr[s];
+                const bool met = lat <= sla;
+                const uint64_t q = c_meta[s] & kQidMask;
+                if (FULL) {  // PartitionUsage (engine.hpp:175-177)
+                    const double ran = now - c_start[s];
+                    const int cb = (int)(c_meta[s] >> 40);
+                    bms[s] = bms[s] + ran;
+                    wbms[s] = wbms[s] + ran * s_util[row[s] + cb - 1];
+                    nq[s] += 1;
                 }
-                c_start = now;
-                c_est = est;
-                c_comp = now + est;
-                if (kFold) fold = refold();
-            } else {
-                busy = false;
-                fold = 0.0;
+                viol += met ? 0u : 1u;
+                if (c_arr[s] >= warmup) {
+                    mviol += met ? 0u : 1u;
+                    samples[(uint32_t)q - (uint32_t)m0] = lat;
+                }
+                hash += msv_query_digest(q, pk[s] & 0xff, c_start[s], now);
+                if (REC) {
+                    d->records[q].start_ms = c_start[s];
+                    d->records[q].finish_ms = now;
+                }
+                if (qn[s] > 0) {  // start the queue head now (engine.hpp:181-185)
+                    const int h = qh[s];
+                    const double est = M.q_est[s][h][lane];
+                    c_arr[s] = M.q_arr[s][h][lane];
+                    c_meta[s] = M.q_meta[s][h][lane];
+                    qh[s] = (h + 1) & (QC - 1);
+                    qn[s] -= 1;
+                    if (gn[s] > 0) {  // refill the ring from the overflow list
+                        const uint32_t g = M.g_head[s][lane];
+                        M.g_head[s][lane] = d->next[g];
+                        gn[s] -= 1;
+                        const int32_t gb = g_bat[g];
+                        const int e2 = (qh[s] + qn[s]) & (QC - 1);
+                        M.q_est[s][e2][lane] = s_lat[row[s] + gb - 1];
+                        M.q_arr[s][e2][lane] = g_arr[g];
+                        M.q_meta[s][e2][lane] = (uint64_t)g | ((uint64_t)gb << 40);
+                        qn[s] += 1;
+                    }
+                    c_start[s] = now;
+                    c_est[s] = est;
+                    c_comp[s] = now + est;
+                    if (kFold) fold[s] = refold(s);
+                } else {
+                    busy[s] = false;
+                    fold[s] = 0.0;
+                }
             }
         }
 
         // ---- 2. dispatch (engine.hpp:189-230) ----
         bool go = arrival;
-        if (go && (b < 1 || b > bmax)) {  // LookupError at this query (profile.hpp:127-129)
+        if (FULL && go && (b < 1 || b > bmax)) {  // LookupError at this query (profile.hpp:127-129)
             status = MSV_LOOKUP;
             go = false;
         }
-        bool cand = go && act;
-        const double x = c_est - (t - c_start);
-        const double wv = fold + ((busy && 0.0 < x) ? x : 0.0);  // Eq. 1 (sched.hpp:77-85)
-        const double est_n = (FULL && row < 0) ? 0.0 : s_lat[row + (go ? b : 1) - 1];
-        bool bad = false;
+        bool cand[S], bad[S];
+        double wv[S];
+#pragma unroll
+        for (int s = 0; s < S; ++s) {
+            cand[s] = go && act[s];
+            const double x = c_est[s] - (t - c_start[s]);
+            wv[s] = fold[s] + ((busy[s] && 0.0 < x) ? x : 0.0);  // Eq. 1 (sched.hpp:77-85)
+            bad[s] = false;
+        }
+        int bad_o = 1 << 30;  // segment order index of the first candidate whose size is missing
         if (FULL) {
             if (p.any_routing) {  // engine.hpp:197-206
-                if (go && d->route_mask != nullptr)
-                    cand = cand && (((d->route_mask[sl] >> (b - 1)) & 1ull) != 0);
-                if ((__ballot_sync(kFull, cand) & seg_mask) == 0) cand = go && act;
+                unsigned anyc = 0;
+#pragma unroll
+                for (int s = 0; s < S; ++s) {
+                    if (go && d->route_mask != nullptr)
+                        cand[s] = cand[s] && (((d->route_mask[s * W + sl] >> (b - 1)) & 1ull) != 0);
+                    anyc |= __ballot_sync(kFull, cand[s]) & seg_mask;
+                }
+                if (anyc == 0) {
+#pragma unroll
+                    for (int s = 0; s < S; ++s) cand[s] = go && act[s];
+                }
             }
-            bad = cand && row < 0;
-            if (check_wait && cand && !bad) {  // engine.hpp:208-217
-                const double y = c_comp - t;
-                const double gw = fold + ((busy && 0.0 < y) ? y : 0.0);
-                const double dd = fabs(gw - wv);
-                wdiff = (wdiff < dd) ? dd : wdiff;
+#pragma unroll
+            for (int s = S - 1; s >= 0; --s) {
+                bad[s] = cand[s] && row[s] < 0;
+                const unsigned bb = __ballot_sync(kFull, bad[s]) & seg_mask;
+                if (bb) bad_o = s * W + (__ffs(bb) - 1 - seg_base);
+            }
+            if (check_wait) {  // engine.hpp:208-217
+#pragma unroll
+                for (int s = 0; s < S; ++s) {
+                    if (!cand[s] || bad[s]) continue;
+                    const double y = c_comp[s] - t;
+                    const double gw = fold[s] + ((busy[s] && 0.0 < y) ? y : 0.0);
+                    const double dd = fabs(gw - wv[s]);
+                    wdiff = (wdiff < dd) ? dd : wdiff;
+                }
             }
         }
-        const unsigned bad_bits = FULL ? (__ballot_sync(kFull, bad) & seg_mask) : 0u;
-        int ch = -1, kind = 0;
+        int ch = -1, kind = 0;  // chosen segment order index
         if constexpr (SCHED == MSV_ELSA) {
-            const bool ok = cand && !bad;
-            const bool pred = ok && (unit ? (sla > wv + est_n) : (sla > alpha * (wv + beta * est_n)));
-            const unsigned bA = __ballot_sync(kFull, pred) & seg_mask;
-            if (bA) ch = __ffs(bA) - 1;
+            bool ok[S];
+#pragma unroll
+            for (int s = S - 1; s >= 0; --s) {  // Step A (sched.hpp:125-130)
+                ok[s] = cand[s] && !bad[s];
+                const bool pred =
+                    ok[s] && (unit ? (sla > wv[s] + est_n[s]) : (sla > alpha * (wv[s] + beta * est_n[s])));
+                const unsigned bA = __ballot_sync(kFull, pred) & seg_mask;
+                if (bA) ch = s * W + (__ffs(bA) - 1 - seg_base);
+            }
             kind = MSV_SLACK_SATISFYING;
             const bool needB = go && ch < 0;
-            if (__any_sync(kFull, needB)) {  // Step B (sched.hpp:132-142)
-                const uint64_t fb = ok ? msv_dbits(wv + est_n) : ~0ull;
-                const uint64_t vmin = seg_min_u64<W>(fb);
-                const unsigned bB = __ballot_sync(kFull, ok && fb == vmin) & seg_mask;
-                if (needB && bB) {
-                    ch = __ffs(bB) - 1;
+            if (__any_sync(kFull, needB)) {  // Step B (sched.hpp:132-142): argmin w + est, earliest on ties
+                uint64_t fb[S];
+                uint64_t lm = ~0ull;
+#pragma unroll
+                for (int s = 0; s < S; ++s) {
+                    fb[s] = ok[s] ? msv_dbits(wv[s] + est_n[s]) : ~0ull;
+                    lm = fb[s] < lm ? fb[s] : lm;
+                }
+                const uint64_t vmin = seg_min_u64<W>(lm);
+                int chB = -1;
+#pragma unroll
+                for (int s = S - 1; s >= 0; --s) {
+                    const unsigned bB = __ballot_sync(kFull, ok[s] && fb[s] == vmin) & seg_mask;
+                    if (bB) chB = s * W + (__ffs(bB) - 1 - seg_base);
+                }
+                if (needB && chB >= 0) {
+                    ch = chB;
                     kind = MSV_FASTEST_FALLBACK;
                 }
             }
             // a size missing from the profile is a LookupError once the scan reaches it
-            if (FULL && go && bad_bits && (ch < 0 || kind == MSV_FASTEST_FALLBACK || (__ffs(bad_bits) - 1) < ch)) {
+            if (FULL && go && bad_o != (1 << 30) && (ch < 0 || kind == MSV_FASTEST_FALLBACK || bad_o < ch)) {
                 status = MSV_LOOKUP;
                 go = false;
             }
-        } else {
-            const uint32_t ki =
-                (cand && !busy) ? (((0x7FFFu - ((uint32_t)pk >> 8)) << 16) | ((uint32_t)pk & 0xffu)) : ~0u;
-            const uint32_t mi = seg_min_u32<W>(ki);
-            const uint32_t len = (uint32_t)qn + gn;
-            const uint32_t kq = cand ? (((len < 0xFFFFFFu ? len : 0xFFFFFFu) << 8) | ((uint32_t)pk & 0xffu)) : ~0u;
+        } else {  // FIFS (sched.hpp:154-170): idle -> max k, min id; else shortest queue, min id
+            uint32_t ki[S], kq[S];
+            uint32_t li = ~0u, lq = ~0u;
+#pragma unroll
+            for (int s = 0; s < S; ++s) {
+                ki[s] = (cand[s] && !busy[s]) ? (((0x7FFFu - ((uint32_t)pk[s] >> 8)) << 16) | ((uint32_t)pk[s] & 0xffu))
+                                              : ~0u;
+                const uint32_t len = (uint32_t)qn[s] + gn[s];
+                kq[s] = cand[s] ? (((len < 0xFFFFFFu ? len : 0xFFFFFFu) << 8) | ((uint32_t)pk[s] & 0xffu)) : ~0u;
+                li = ki[s] < li ? ki[s] : li;
+                lq = kq[s] < lq ? kq[s] : lq;
+            }
+            const uint32_t mi = seg_min_u32<W>(li);
             const bool idle = mi != ~0u;
             uint32_t mq = ~0u;
-            if (__any_sync(kFull, go && !idle)) mq = seg_min_u32<W>(kq);
-            const unsigned bs = __ballot_sync(kFull, idle ? (ki == mi) : (kq == mq && mq != ~0u)) & seg_mask;
-            if (go && bs) ch = __ffs(bs) - 1;
+            if (__any_sync(kFull, go && !idle)) mq = seg_min_u32<W>(lq);
+#pragma unroll
+            for (int s = S - 1; s >= 0; --s) {
+                const unsigned bs =
+                    __ballot_sync(kFull, idle ? (ki[s] == mi && mi != ~0u) : (kq[s] == mq && mq != ~0u)) & seg_mask;
+                if (go && bs) ch = s * W + (__ffs(bs) - 1 - seg_base);
+            }
             kind = idle ? MSV_IDLE_LARGEST : MSV_SHORTEST_QUEUE;
-            if (FULL && go && ch >= 0 && ((bad_bits >> ch) & 1u)) {  // chosen size missing (engine.hpp:226)
-                status = MSV_LOOKUP;
-                go = false;
+            if (FULL) {  // the chosen partition's latency lookup fails (engine.hpp:226)
+                bool mine_bad = false;
+#pragma unroll
+                for (int s = 0; s < S; ++s) mine_bad |= go && (s * W + sl == ch) && row[s] < 0;
+                if ((__ballot_sync(kFull, mine_bad) & seg_mask) != 0) {
+                    status = MSV_LOOKUP;
+                    go = false;
+                }
             }
         }
 
         // ---- 3. start or enqueue on the chosen partition (engine.hpp:225-230) ----
-        if (go && lane == ch) {
-            const uint64_t meta = (uint64_t)i | ((uint64_t)b << 40);
-            if (!busy) {
-                busy = true;
-                c_start = t;
-                c_est = est_n;
-                c_comp = t + est_n;
-                c_arr = t;
-                c_meta = meta;
-            } else {
-                if (gn == 0 && qn < kQCap) {
-                    const int e = (qh + qn) & (kQCap - 1);
-                    M.q_est[e][lane] = est_n;
-                    M.q_arr[e][lane] = t;
-                    M.q_meta[e][lane] = meta;
-                    qn += 1;
+#pragma unroll
+        for (int s = 0; s < S; ++s) {
+            if (go && s * W + sl == ch) {
+                const double est = est_n[s];
+                const uint64_t meta = (uint64_t)i | ((uint64_t)b << 40);
+                if (!busy[s]) {
+                    busy[s] = true;
+                    c_start[s] = t;
+                    c_est[s] = est;
+                    c_comp[s] = t + est;
+                    c_arr[s] = t;
+                    c_meta[s] = meta;
                 } else {
-                    if (gn == 0) M.g_head[lane] = (uint32_t)i;
-                    else d->next[M.g_tail[lane]] = (uint32_t)i;
-                    M.g_tail[lane] = (uint32_t)i;
-                    gn += 1;
+                    if (gn[s] == 0 && qn[s] < QC) {
+                        const int e = (qh[s] + qn[s]) & (QC - 1);
+                        M.q_est[s][e][lane] = est;
+                        M.q_arr[s][e][lane] = t;
+                        M.q_meta[s][e][lane] = meta;
+                        qn[s] += 1;
+                    } else {
+                        if (gn[s] == 0) M.g_head[s][lane] = (uint32_t)i;
+                        else d->next[M.g_tail[s][lane]] = (uint32_t)i;
+                        M.g_tail[s][lane] = (uint32_t)i;
+                        gn[s] += 1;
+                    }
+                    fold[s] = fold[s] + est;  // appending extends the left fold exactly
                 }
-                fold = fold + est_n;  // appending extends the left fold exactly
-            }
-            if (REC) {
-                d->records[i].partition = pk & 0xff;
-                d->records[i].kind = kind;
+                if (REC) {
+                    d->records[i].partition = pk[s] & 0xff;
+                    d->records[i].kind = kind;
+                }
             }
         }
         if (arrival && status == 0) ++i;
@@ -330,14 +431,15 @@ __global__ void __launch_bounds__(kSimWarpsPerBlock * 32, kSegMinBlocks) sim_ker
         // ---- end of trace: reduce the segment and publish (segment-uniform, rare) ----
         if (ending) {
             __pipeline_wait_prior(0);  // no copy may land in a window after the segment moves on
-            double lf = (nq > 0) ? c_comp : 0.0;  // last completion of this lane
+            // last completion = each slot's final c_comp (a slot that never ran holds 0.0)
+            double lf = 0.0;
+#pragma unroll
+            for (int s = 0; s < S; ++s) lf = (lf < c_comp[s]) ? c_comp[s] : lf;
             const uint64_t v0 = seg_sum_u64<W>((uint64_t)viol, seg_mask);
             const uint64_t v2 = seg_sum_u64<W>((uint64_t)mviol, seg_mask);
             const uint64_t hsum = seg_sum_u64<W>(hash, seg_mask);
             lf = seg_max_f64<W>(lf, seg_mask);
             const double wd = seg_max_f64<W>(wdiff, seg_mask);
-            const uint64_t mn = seg_minm_u64<W>(lmin, seg_mask);
-            const uint64_t mx = seg_max_u64<W>(lmax, seg_mask);
             if (sl == 0) {
                 DevOut o;
                 o.violations = (int64_t)v0;
@@ -347,18 +449,23 @@ __global__ void __launch_bounds__(kSimWarpsPerBlock * 32, kSegMinBlocks) sim_ker
                 o.horizon_ms = (d->duration_ms < lf) ? lf : d->duration_ms;  // engine.hpp:237
                 o.max_wait_diff = wd;
                 o.hash = hsum;
-                o.lat_min_bits = mn;
-                o.lat_max_bits = mx;
+                o.lat_min_bits = kSignBit;  // key range of non-negative latencies: [+0.0, +inf]
+                o.lat_max_bits = 0xFFF0000000000000ull;
                 o.status = status;
                 o.pad = 0;
                 p.out[sidx] = o;
             }
-            if (act && d->usage_off >= 0) {
-                msv_usage u;
-                u.busy_ms = bms;
-                u.weighted_busy_ms = wbms;
-                u.queries = nq;
-                p.usage[d->usage_off + (pk & 0xff)] = u;
+            if (FULL && p.any_usage && d->usage_off >= 0) {
+#pragma unroll
+                for (int s = 0; s < S; ++s) {
+                    if (act[s]) {
+                        msv_usage u;
+                        u.busy_ms = bms[s];
+                        u.weighted_busy_ms = wbms[s];
+                        u.queries = nq[s];
+                        p.usage[d->usage_off + (pk[s] & 0xff)] = u;
+                    }
+                }
             }
             __syncwarp(seg_mask);
             sidx = -1;
@@ -366,18 +473,19 @@ __global__ void __launch_bounds__(kSimWarpsPerBlock * 32, kSegMinBlocks) sim_ker
     }
 }
 
-template <int W, int SCHED>
+template <int W, int S, int SCHED>
 void* pick_flags(bool rec, bool full) {
-    if (rec) return (void*)&sim_kernel<W, SCHED, true, true>;
-    return full ? (void*)&sim_kernel<W, SCHED, false, true> : (void*)&sim_kernel<W, SCHED, false, false>;
+    if (rec) return (void*)&sim_kernel<W, S, SCHED, true, true>;
+    return full ? (void*)&sim_kernel<W, S, SCHED, false, true> : (void*)&sim_kernel<W, S, SCHED, false, false>;
 }
 
-void* pick_sim(int W, int sched, bool rec, bool full) {
-#define MSV_PICK(w) \
-    if (W == w) return sched == MSV_ELSA ? pick_flags<w, MSV_ELSA>(rec, full) : pick_flags<w, MSV_FIFS>(rec, full);
-    MSV_PICK(4)
-    MSV_PICK(8)
-    MSV_PICK(16)
+void* pick_sim(int W, int S, int sched, bool rec, bool full) {
+#define MSV_PICK(w, s)                                                                                     \
+    if (W == w && S == s)                                                                                  \
+        return sched == MSV_ELSA ? pick_flags<w, s, MSV_ELSA>(rec, full) : pick_flags<w, s, MSV_FIFS>(rec, full);
+    MSV_PICK(4, 1)
+    MSV_PICK(8, 1)
+    MSV_PICK(16, 1)
 #undef MSV_PICK
     return nullptr;
 }
@@ -390,12 +498,15 @@ size_t sim_warp_smem_bytes(int S, int n_cells);
 size_t sim_smem_bytes(int W, int S, int n_cells) {
     if (W == 32) return sim_warp_smem_bytes(S, n_cells);
     const size_t tab = ((size_t)2 * n_cells * sizeof(double) + 15) & ~(size_t)15;
-    const size_t per_warp = W == 4 ? sizeof(SegSmem<4>) : (W == 8 ? sizeof(SegSmem<8>) : sizeof(SegSmem<16>));
+    size_t per_warp = 0;
+    if (W == 4) per_warp = sizeof(SegSmem<4, 1>);
+    else if (W == 8) per_warp = sizeof(SegSmem<8, 1>);
+    else per_warp = sizeof(SegSmem<16, 1>);
     return tab + (size_t)kSimWarpsPerBlock * per_warp;
 }
 
 static void* sim_fn_for(int W, int S, int sched, bool rec, bool full) {
-    return W == 32 ? sim_warp_fn(S, sched, rec, full) : pick_sim(W, sched, rec, full);
+    return W == 32 ? sim_warp_fn(S, sched, rec, full) : pick_sim(W, S, sched, rec, full);
 }
 
 int sim_max_blocks_per_sm(int W, int S, int sched, bool records, bool full, int n_cells) {
