@@ -567,7 +567,13 @@ int grid_build(msv_ctx* ctx, const msv_scenario* sc, int64_t n, const double* ta
         const int seg_w = wave_seg_width(n4, n8, n16, ctx->sms);
         int max_chunks = kDefaultChunks;
         if (const char* e = getenv("MSV_MAX_CHUNKS")) max_chunks = std::max(1, std::min(kMaxChunks, atoi(e)));
+        // A second chunk pays only when the first still fills the device for about two
+        // rounds of the warp kernel's slots (28 warps per SM): then its trace generation
+        // hides under that simulation and its simulation fills the first one's tail.
+        // Smaller waves run as one chunk (a half-full launch costs more than the overlap).
+        const int64_t warp_slots = (int64_t)ctx->sms * 28;
         int n_chunks = (int)std::max<int64_t>(1, std::min<int64_t>(max_chunks, ns_w / kChunkScenarios));
+        if (!getenv("MSV_MAX_CHUNKS") && ns_w < 2 * warp_slots) n_chunks = 1;
         // chunk shares (MSV_CHUNK_SPLIT=f0,f1,...: experiment knob; default equal)
         // two chunks split 3:1 (sweep on the C2 grid: the small second chunk's simulation
         // fills the first chunk's tail, its trace generation hides under it)

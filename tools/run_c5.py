@@ -9,7 +9,7 @@ n = int(sys.argv[1]) if len(sys.argv) > 1 else 10000
 q = float(sys.argv[2]) if len(sys.argv) > 2 else 1e6
 eng = Engine(0)
 specs = W.c5(n_scenarios=n, queries=q)
-t0 = time.perf_counter(); g = eng.grid(specs); t1 = time.perf_counter()
+t0 = time.perf_counter(); g = eng.grid(specs); g.set_usage(False); t1 = time.perf_counter()
 g.launch(); tm = g.timing(); t2 = time.perf_counter()
 r = g.results()
 tot = int(r["total"].sum())
