@@ -247,14 +247,14 @@ ClassKey class_of(int P, int sched, int seg_w) {
 
 // Narrowest segment width worth launching for a wave with n4 / n8 / n16 plans of
 // P <= 4 / 8 / 16 on `sms` SMs: G scenarios per warp must still leave >= half of the
-// segmented kernel's warp slots (~5 blocks x 4 warps per SM) busy. (Two slots per lane
-// for 16 < P <= 32 was measured: more instructions per query than the warp kernel.)
+// segmented kernel's warp slots (~5 blocks x 4 warps per SM) busy. Measured without
+// usage accumulation: W = 4 and 8 beat the warp kernel by 20-30 % on full waves; W = 16
+// (and two slots per lane for 16 < P <= 32) lose to it, so they are never chosen here.
 int wave_seg_width(int64_t n4, int64_t n8, int64_t n16, int sms) {
     if (segmented_mode() == 0) return 32;
     const int64_t half_slots = (int64_t)sms * 5 * msv::kSimWarpsPerBlock / 2;
     if (n4 / 8 >= half_slots) return 4;
     if (n8 / 4 >= half_slots) return 8;
-    if (n16 / 2 >= half_slots) return 16;
     return 32;
 }
 
@@ -572,8 +572,11 @@ int grid_build(msv_ctx* ctx, const msv_scenario* sc, int64_t n, const double* ta
         // hides under that simulation and its simulation fills the first one's tail.
         // Smaller waves run as one chunk (a half-full launch costs more than the overlap).
         const int64_t warp_slots = (int64_t)ctx->sms * 28;
+        int64_t warps_w = 0;  // warps the wave occupies (segmented classes pack 32/W scenarios)
+        for (int64_t i = w.s0; i < w.s1; ++i) warps_w += class_of(g->P[i], sc[i].scheduler, seg_w).W;
+        warps_w /= 32;
         int n_chunks = (int)std::max<int64_t>(1, std::min<int64_t>(max_chunks, ns_w / kChunkScenarios));
-        if (!getenv("MSV_MAX_CHUNKS") && ns_w < 2 * warp_slots) n_chunks = 1;
+        if (!getenv("MSV_MAX_CHUNKS") && warps_w < 2 * warp_slots) n_chunks = 1;
         // chunk shares (MSV_CHUNK_SPLIT=f0,f1,...: experiment knob; default equal)
         // two chunks split 3:1 (sweep on the C2 grid: the small second chunk's simulation
         // fills the first chunk's tail, its trace generation hides under it)

@@ -11,6 +11,7 @@ rate = 0.8 * W.capacity_qps(m, p)
 eng = Engine(0)
 g = eng.grid([W._spec(m, p, rate, 1e5, 1 + s) for s in range(n)])
 g.set_overlap(False)
+g.set_usage(False)
 g.launch()
 tm = g.timing()
 print(f"{name} {pn} P={p.total_instances()} sim {g.queries() / tm['sim_ms'] * 1e-6:.2f} G q/s", flush=True)
