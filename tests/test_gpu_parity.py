@@ -13,7 +13,7 @@ import pytest
 
 from paper_2202_13481_b200 import (BatchDistribution, Engine, GridSpec, LookupError_, ParamError, PartitionPlan,
                                    SlaConfig, ValidationError, lognormal_batch_pdf, synth_profile,
-                                   SyntheticProfileParams)
+                                   SyntheticProfileParams, homogeneous_plan)
 from paper_2202_13481_b200 import workloads as W
 from tests import oracle_py as O
 
@@ -348,3 +348,38 @@ def _class_grid_check():
             specs += [W._spec(m, p, rate, 3000, s, sched) for s in (1, 2, 3)]
         specs += [W._spec(m, p, 1.6 * W.capacity_qps(m, p), 2000, 9, "elsa")]
     assert_grid_equal(eng.run_grid(specs), ref.run_grid(specs))
+
+
+def _chunked_grid_hashes():
+    """A grid of mixed plan sizes (warp and segmented classes) as one device grid."""
+    eng = Engine(0)
+    m = W.model("bert_base")
+    specs = []
+    for p in (W.paris(m, 8), W.paris(m, 1), homogeneous_plan(7, 56, 8, 7), homogeneous_plan(1, 14, 2, 7)):
+        rate = 0.8 * W.capacity_qps(m, p)
+        specs += [W._spec(m, p, rate, 400, s) for s in range(1, 1201)]
+    g = eng.grid(specs)
+    g.set_usage(False)
+    g.launch()
+    r = g.results()
+    return r["placement_hash"], r["tail"], r["total"]
+
+
+def test_chunking_and_classes_do_not_change_results():
+    """The launch layout (one or two chunks, 3:1 or equal split, warp vs segmented
+    classes) is a scheduling choice only: every layout gives bit-identical results."""
+    import os
+    import sys
+    base = _chunked_grid_hashes()
+    code = ("import sys, numpy as np; sys.path.insert(0, %r); from tests.test_gpu_parity import _chunked_grid_hashes; "
+            "h, t, n = _chunked_grid_hashes(); np.save(sys.argv[1], np.concatenate([h.view(np.float64), t.ravel(), "
+            "n.astype(np.float64)]))" % str(ROOT))
+    want = np.concatenate([base[0].view(np.float64), base[1].ravel(), base[2].astype(np.float64)])
+    for extra in ({"MSV_MAX_CHUNKS": "2"}, {"MSV_MAX_CHUNKS": "2", "MSV_CHUNK_SPLIT": "1,1"},
+                  {"MSV_SEGMENTED": "1"}, {"MSV_SEGMENTED": "0", "MSV_MAX_CHUNKS": "1"}):
+        out = Path(f"/tmp/msv_chunk_{os.getpid()}.npy")
+        r = subprocess.run([sys.executable, "-c", code, str(out)], capture_output=True, text=True,
+                           env=dict(os.environ, **extra), timeout=600)
+        assert r.returncode == 0, r.stderr[-2000:]
+        got = np.load(out)
+        assert np.array_equal(got.view(np.uint64), want.view(np.uint64)), extra
