@@ -28,7 +28,7 @@ constexpr uint64_t kQid = (1ull << 40) - 1;
 template <int S>
 struct WarpCfg {
     static constexpr int qcap = S == 1 ? 8 : (S == 2 ? 4 : 2);  // shared ring entries per slot
-    static constexpr int min_blocks = S == 1 ? 7 : (S == 2 ? 4 : 2);
+    static constexpr int min_blocks = S == 1 ? 7 : (S == 2 ? 5 : 2);
 };
 
 // Per-warp shared-memory layout (after the block's profile table).
@@ -237,8 +237,12 @@ __global__ void __launch_bounds__(kSimWarpsPerBlock * 32, WarpCfg<S>::min_blocks
 #pragma unroll
                     for (int s = 0; s < S; ++s) {
                         cand[s] = act[s];
-                        const double x = c_est[s] - (t - c_start[s]);
-                        wv[s] = fold[s] + ((busy[s] && 0.0 < x) ? x : 0.0);
+                        // Eq. 1 up front where every slot's wait is needed (FULL, or one slot);
+                        // plain multi-slot ELSA evaluates it slot by slot below, FIFS never
+                        if constexpr (FULL || (SCHED == MSV_ELSA && S == 1)) {
+                            const double x = c_est[s] - (t - c_start[s]);
+                            wv[s] = fold[s] + ((busy[s] && 0.0 < x) ? x : 0.0);
+                        }
                     }
                     int bad_o = 1 << 30;  // order index of the first candidate whose size is missing
                     if (FULL) {
@@ -293,6 +297,44 @@ __global__ void __launch_bounds__(kSimWarpsPerBlock * 32, WarpCfg<S>::min_blocks
                             const bool hit = fb == vmin && vmin != ~0ull;
                             const unsigned bB = __ballot_sync(kFull, hit);
                             mine[0] = hit && (bB & below) == 0;
+                            kind = MSV_FASTEST_FALLBACK;
+                        }
+                    } else if constexpr (SCHED == MSV_ELSA && !FULL) {
+                        // Several slots per lane: Step A scans the slots in order (slot s holds
+                        // order indices [32s, 32s + 32)) and stops at the first slot with a
+                        // satisfying partition, so later slots' waits are computed only when
+                        // needed (Step B needs them all).
+                        kind = MSV_SLACK_SATISFYING;
+                        int s_eval = 0;
+#pragma unroll
+                        for (int s = 0; s < S; ++s) {
+                            const double x = c_est[s] - (t - c_start[s]);
+                            wv[s] = fold[s] + ((busy[s] && 0.0 < x) ? x : 0.0);
+                            s_eval = s + 1;
+                            bool pred;
+                            if constexpr (UNIT) pred = act[s] && (sla > wv[s] + est_n[s]);
+                            else pred = act[s] && (sla > alpha * (wv[s] + beta * est_n[s]));
+                            const unsigned bA = __ballot_sync(kFull, pred);
+                            if (bA) {
+                                ch = s * 32 + __ffs(bA) - 1;
+                                break;
+                            }
+                        }
+                        if (ch < 0) {  // Step B (sched.hpp:132-142): argmin w + est, earliest on ties
+                            (void)s_eval;  // every slot was evaluated (no break)
+                            uint64_t fb[S];
+                            uint64_t vmin = ~0ull;
+#pragma unroll
+                            for (int s = 0; s < S; ++s) {
+                                fb[s] = act[s] ? msv_dbits(wv[s] + est_n[s]) : ~0ull;
+                                vmin = fb[s] < vmin ? fb[s] : vmin;
+                            }
+                            vmin = seg_min_u64<32>(vmin);
+#pragma unroll
+                            for (int s = S - 1; s >= 0; --s) {
+                                const unsigned bB = __ballot_sync(kFull, fb[s] == vmin && vmin != ~0ull);
+                                if (bB) ch = s * 32 + __ffs(bB) - 1;
+                            }
                             kind = MSV_FASTEST_FALLBACK;
                         }
                     } else if constexpr (SCHED == MSV_ELSA) {
