@@ -217,10 +217,9 @@ struct ClassKey {
 };
 
 constexpr int kMaxChunks = 8;           // chunks per wave (pipelined over kAuxStreams streams)
-constexpr int kDefaultChunks = 2;
 constexpr int64_t kChunkScenarios = 1024;  // smallest chunk worth its own launch
 constexpr int kCounterSlots = 1024;      // work-stealing counters per launch (chunk x class)
-constexpr int kAuxStreams = 2;
+constexpr int kAuxStreams = 4;  // chunk c runs on aux stream c % kAuxStreams
 
 // Kernel class of a plan with P partitions. The one-scenario-per-warp kernel (W = 32)
 // serves every plan; the segmented kernel runs G = 32/W scenarios per warp (W lanes
@@ -565,23 +564,24 @@ int grid_build(msv_ctx* ctx, const msv_scenario* sc, int64_t n, const double* ta
             n16 += g->P[i] <= 16;
         }
         const int seg_w = wave_seg_width(n4, n8, n16, ctx->sms);
-        int max_chunks = kDefaultChunks;
-        if (const char* e = getenv("MSV_MAX_CHUNKS")) max_chunks = std::max(1, std::min(kMaxChunks, atoi(e)));
-        // A second chunk pays only when the first still fills the device for about two
-        // rounds of the warp kernel's slots (28 warps per SM): then its trace generation
-        // hides under that simulation and its simulation fills the first one's tail.
-        // Smaller waves run as one chunk (a half-full launch costs more than the overlap).
+        // Chunks pay only when the wave fills the device for about two rounds of the warp
+        // kernel's slots (28 warps per SM): then the big first chunk's simulation hides the
+        // small chunks' trace generation, and their simulations and tail selections fill
+        // its last round. Smaller waves run as one chunk (a half-full launch costs more
+        // than the overlap). Shares 2:1:1:1 on four streams (sweep on the C2 grid: 3:1 on
+        // two streams -1.4 %, one chunk -7 %). MSV_MAX_CHUNKS / MSV_CHUNK_SPLIT override.
         const int64_t warp_slots = (int64_t)ctx->sms * 28;
         int64_t warps_w = 0;  // warps the wave occupies (segmented classes pack 32/W scenarios)
         for (int64_t i = w.s0; i < w.s1; ++i) warps_w += class_of(g->P[i], sc[i].scheduler, seg_w).W;
         warps_w /= 32;
-        int n_chunks = (int)std::max<int64_t>(1, std::min<int64_t>(max_chunks, ns_w / kChunkScenarios));
-        if (!getenv("MSV_MAX_CHUNKS") && warps_w < 2 * warp_slots) n_chunks = 1;
-        // chunk shares (MSV_CHUNK_SPLIT=f0,f1,...: experiment knob; default equal)
-        // two chunks split 3:1 (sweep on the C2 grid: the small second chunk's simulation
-        // fills the first chunk's tail, its trace generation hides under it)
-        std::vector<double> share(n_chunks, 1.0);
-        if (n_chunks == 2) share[0] = 3.0;
+        std::vector<double> share;
+        if (warps_w >= 2 * warp_slots && ns_w >= 4 * kChunkScenarios) share = {2.0, 1.0, 1.0, 1.0};
+        else share = {1.0};
+        if (const char* e = getenv("MSV_MAX_CHUNKS")) {
+            const int mc = std::max(1, std::min(kMaxChunks, atoi(e)));
+            const int nc = (int)std::max<int64_t>(1, std::min<int64_t>(mc, ns_w / kChunkScenarios));
+            share.assign(nc, 1.0);
+        }
         if (const char* e = getenv("MSV_CHUNK_SPLIT")) {
             std::vector<double> f;
             for (const char* c = e; *c;) {
@@ -591,11 +591,9 @@ int grid_build(msv_ctx* ctx, const msv_scenario* sc, int64_t n, const double* ta
                 if (v > 0) f.push_back(v);
                 c = (*end == ',') ? end + 1 : end;
             }
-            if (!f.empty() && (int64_t)f.size() <= ns_w) {
-                share = f;
-                n_chunks = (int)f.size();
-            }
+            if (!f.empty() && (int)f.size() <= kMaxChunks && (int64_t)f.size() <= ns_w) share = f;
         }
+        const int n_chunks = (int)share.size();
         double share_sum = 0.0;
         for (double v : share) share_sum += v;
         // proportional interleave in cost order: each scenario goes to the chunk furthest
