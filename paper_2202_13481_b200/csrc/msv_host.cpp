@@ -136,6 +136,9 @@ struct msv_ctx {
     cudaStream_t aux[4] = {};    // chunk streams of overlapped grid launches
     cudaEvent_t aux_ev[4] = {};
     cudaEvent_t fork_ev = nullptr;
+    cudaStream_t cls[4] = {};    // extra class streams: a chunk's kernel classes run concurrently
+    cudaEvent_t cls_ev[4] = {};
+    cudaEvent_t cls_fork = nullptr;
     std::vector<Profile> profiles;
     std::vector<Dist> dists;
     std::vector<Plan> plans;
@@ -821,7 +824,29 @@ int launch_chunk(msv_grid* g, const msv_grid::Chunk& ch, int counter_base, cudaS
         ctx->launches += 1;
     }
     if (e1) MSV_CUDA_TRY(cudaEventRecord(e1, st));
-    for (size_t c = 0; c < ch.classes.size(); ++c) {
+    // A chunk's kernel classes are independent: the largest runs on the chunk stream, the
+    // others on class streams forked after K1, so their blocks fill the largest one's
+    // last round instead of each class launch ending in its own tail.
+    const size_t ncls = ch.classes.size();
+    static const bool class_streams = !(getenv("MSV_CLASS_STREAMS") && atoi(getenv("MSV_CLASS_STREAMS")) == 0);
+    const bool par = class_streams && ncls > 1;
+    std::vector<size_t> corder(ncls);
+    for (size_t c = 0; c < ncls; ++c) corder[c] = c;
+    std::stable_sort(corder.begin(), corder.end(), [&](size_t a, size_t b) {
+        return ch.classes[a].second.size() > ch.classes[b].second.size();
+    });
+    if (par) {
+        for (int a = 0; a < 4; ++a) {
+            if (!ctx->cls[a]) MSV_CUDA_TRY(cudaStreamCreateWithFlags(&ctx->cls[a], cudaStreamNonBlocking));
+            if (!ctx->cls_ev[a]) MSV_CUDA_TRY(cudaEventCreateWithFlags(&ctx->cls_ev[a], cudaEventDisableTiming));
+        }
+        if (!ctx->cls_fork) MSV_CUDA_TRY(cudaEventCreateWithFlags(&ctx->cls_fork, cudaEventDisableTiming));
+        MSV_CUDA_TRY(cudaEventRecord(ctx->cls_fork, st));
+    }
+    for (size_t ci = 0; ci < ncls; ++ci) {
+        const size_t c = corder[ci];
+        cudaStream_t cs = (par && ci > 0) ? ctx->cls[(ci - 1) % 4] : st;
+        if (par && ci > 0) MSV_CUDA_TRY(cudaStreamWaitEvent(cs, ctx->cls_fork, 0));
         const ClassKey& k = ch.classes[c].first;
         const int32_t nwork = (int32_t)ch.classes[c].second.size();
         msv::SimParams p;
@@ -849,9 +874,15 @@ int launch_chunk(msv_grid* g, const msv_grid::Chunk& ch, int counter_base, cudaS
         int occ_used = occ;
         if (const char* e = getenv("MSV_SIM_BLOCK_SLACK")) occ_used = std::max(1, occ - atoi(e));
         const int blocks = std::max(1, std::min(need, occ_used * ctx->sms));
-        MSV_CUDA_TRY(msv::launch_sim(k.W, k.S, k.sched, g->records, p, blocks, st));
-        debug_sync(st, "sim");
+        MSV_CUDA_TRY(msv::launch_sim(k.W, k.S, k.sched, g->records, p, blocks, cs));
+        debug_sync(cs, "sim");
         ctx->launches += 1;
+    }
+    if (par) {  // join the class streams back into the chunk stream
+        for (size_t ci = 1; ci < ncls && ci <= 4; ++ci) {
+            MSV_CUDA_TRY(cudaEventRecord(ctx->cls_ev[ci - 1], ctx->cls[ci - 1]));
+            MSV_CUDA_TRY(cudaStreamWaitEvent(st, ctx->cls_ev[ci - 1], 0));
+        }
     }
     if (e2) MSV_CUDA_TRY(cudaEventRecord(e2, st));
     if (!g->tail_p.empty() && nl > 0) {
@@ -1037,6 +1068,14 @@ int msv_destroy(msv_ctx* ctx) {
         if (ctx->aux_ev[a]) cudaEventDestroy(ctx->aux_ev[a]);
     }
     if (ctx->fork_ev) cudaEventDestroy(ctx->fork_ev);
+    for (int a = 0; a < 4; ++a) {
+        if (ctx->cls[a]) {
+            cudaStreamSynchronize(ctx->cls[a]);
+            cudaStreamDestroy(ctx->cls[a]);
+        }
+        if (ctx->cls_ev[a]) cudaEventDestroy(ctx->cls_ev[a]);
+    }
+    if (ctx->cls_fork) cudaEventDestroy(ctx->cls_fork);
     cudaStreamDestroy(ctx->stream);
     delete ctx;
     return MSV_OK;
