@@ -712,6 +712,13 @@ int grid_build(msv_ctx* ctx, const msv_scenario* sc, int64_t n, const double* ta
 
     pt.mark("parts");
     // Per-scenario device descriptors.
+    // every latency >= its service time >= the profile's smallest cell (halved: rounding slack)
+    std::vector<double> lat_floor(ctx->profiles.size(), 0.0);
+    for (size_t pi = 0; pi < ctx->profiles.size(); ++pi) {
+        double mn = INFINITY;
+        for (double v : ctx->profiles[pi].lat) mn = v < mn ? v : mn;
+        lat_floor[pi] = (mn > 0.0 && mn < INFINITY) ? 0.5 * mn : 0.0;
+    }
     g->h_scen.resize(n);
     std::vector<msv::TraceJob> tj(n);
     std::vector<msv::TailJob> lj(n);
@@ -724,6 +731,7 @@ int grid_build(msv_ctx* ctx, const msv_scenario* sc, int64_t n, const double* ta
         d.batch = g->B->d_bat.as<int32_t>() + o;
         d.n = g->B->d_nq.as<int64_t>() + i;
         d.duration_ms = s.duration_ms;
+        d.lat_floor = lat_floor[s.profile];
         d.warmup_ms = s.warmup_fraction * s.duration_ms;  // engine.hpp:238
         d.sla = s.sla_ms;
         d.alpha = s.alpha;

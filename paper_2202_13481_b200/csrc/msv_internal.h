@@ -41,6 +41,7 @@ struct DevScen {
     const int64_t* n;           // queries in the trace (written by K1 or the host)
     double duration_ms;
     double warmup_ms;
+    double lat_floor;           // lower bound of every latency (half the profile's smallest cell)
     double sla, alpha, beta;
     const DevPart* parts;       // P entries in (k, id) ascending order
     const uint64_t* route_mask; // P masks (bit b-1: segment of k covers batch b) or null

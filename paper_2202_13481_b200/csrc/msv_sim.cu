@@ -449,8 +449,8 @@ __global__ void __launch_bounds__(kSimWarpsPerBlock * 32, (SegCfg<W, S>::min_blo
                 o.horizon_ms = (d->duration_ms < lf) ? lf : d->duration_ms;  // engine.hpp:237
                 o.max_wait_diff = wd;
                 o.hash = hsum;
-                o.lat_min_bits = kSignBit;  // key range of non-negative latencies: [+0.0, +inf]
-                o.lat_max_bits = 0xFFF0000000000000ull;
+                o.lat_min_bits = msv_dbits(d->lat_floor) | kSignBit;  // latencies lie in [floor, horizon]
+                o.lat_max_bits = msv_dbits(o.horizon_ms) | kSignBit;
                 o.status = status;
                 o.pad = 0;
                 p.out[sidx] = o;

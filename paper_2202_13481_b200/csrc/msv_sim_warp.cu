@@ -477,8 +477,10 @@ __global__ void __launch_bounds__(kSimWarpsPerBlock * 32, WarpCfg<S>::min_blocks
             o.hash = hsum;
             // key range of non-negative latencies: [+0.0, +inf] (K3's first pass
             // splits on the exponent)
-            o.lat_min_bits = kSignBit;
-            o.lat_max_bits = 0xFFF0000000000000ull;
+            // key range of the latencies for K3: [floor, horizon] (a latency is at least the
+            // service time, and at most its finish time <= the horizon)
+            o.lat_min_bits = msv_dbits(d.lat_floor) | kSignBit;
+            o.lat_max_bits = msv_dbits(o.horizon_ms) | kSignBit;
             o.status = status;
             o.pad = 0;
             p.out[sidx] = o;
