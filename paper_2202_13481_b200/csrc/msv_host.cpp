@@ -393,7 +393,7 @@ std::vector<uint64_t> route_masks(const std::vector<DevPart>& parts, const Routi
 
 int64_t trace_capacity(double rate_qps, double duration_ms) {
     const double mean = rate_qps * duration_ms / 1000.0;
-    if (!(mean < 4e9)) return -1;
+    if (!(mean < 2.0e9)) return -1;  // the kernels index a trace with 32-bit ints
     return (int64_t)ceil(mean + 10.0 * sqrt(mean) + 160.0);
 }
 
