@@ -214,8 +214,9 @@ struct SetDevice {
 // Scenario class: W lanes per scenario, S partition slots per lane, scheduler.
 struct ClassKey {
     int W, S, sched;
+    int lazy = 0;  // warp kernel with lazy folds (scenarios offered more than the plan's capacity)
     bool operator<(const ClassKey& o) const {
-        return std::tie(W, S, sched) < std::tie(o.W, o.S, o.sched);
+        return std::tie(W, S, sched, lazy) < std::tie(o.W, o.S, o.sched, o.lazy);
     }
 };
 
@@ -235,7 +236,7 @@ int segmented_mode() {
     return mode;
 }
 
-ClassKey class_of(int P, int sched, int seg_w) {
+ClassKey class_of(int P, int sched, int seg_w, bool overloaded = false) {
     ClassKey c{32, 1, sched};
     if (segmented_mode() == 1) seg_w = 4;
     if (P <= 4 && seg_w <= 4) c.W = 4;
@@ -244,6 +245,10 @@ ClassKey class_of(int P, int sched, int seg_w) {
     else if (P <= 32) c.W = 32;
     else if (P <= 64) c.S = 2;
     else c.S = 4;
+    // Overloaded scenarios grow long queues: the warp kernel's lazy-fold variant keeps them
+    // O(1) per arrival (the plain variant pays O(queue) per pop, and the lazy paths would
+    // cost it registers).
+    if (c.W == 32 && sched == MSV_ELSA && overloaded) c.lazy = 1;
     return c;
 }
 
@@ -516,6 +521,7 @@ int grid_build(msv_ctx* ctx, const msv_scenario* sc, int64_t n, const double* ta
     // Expected work per scenario for longest-first scheduling: queries x (1 + 4 rho^2),
     // rho = offered load over the plan's nominal capacity sum_p 1000 / E_b[latency(k_p, b)].
     std::vector<double> cost(n);
+    std::vector<char> overloaded(n, 0);  // offered load above the plan's nominal capacity
     {
         std::map<std::tuple<int, int, int>, double> cap_qps;
         for (int64_t i = 0; i < n; ++i) {
@@ -541,6 +547,7 @@ int grid_build(msv_ctx* ctx, const msv_scenario* sc, int64_t n, const double* ta
                 it = cap_qps.emplace(key, c).first;
             }
             const double rho = it->second > 0.0 ? s.rate_qps / it->second : 1.0;
+            overloaded[i] = rho > 1.0;
             cost[i] = (s.rate_qps * s.duration_ms / 1000.0) * (1.0 + 4.0 * rho * rho);
         }
     }
@@ -620,7 +627,7 @@ int grid_build(msv_ctx* ctx, const msv_scenario* sc, int64_t n, const double* ta
             g->launch_order.insert(g->launch_order.end(), members[c].begin(), members[c].end());
             ch.l1 = (int64_t)g->launch_order.size();
             std::map<ClassKey, std::vector<int32_t>> cls;
-            for (int32_t i : members[c]) cls[class_of(g->P[i], sc[i].scheduler, seg_w)].push_back(i);  // cost order kept
+            for (int32_t i : members[c]) cls[class_of(g->P[i], sc[i].scheduler, seg_w, overloaded[i])].push_back(i);  // cost order kept
             for (auto& kv : cls) ch.classes.emplace_back(kv.first, std::move(kv.second));
             w.chunks.push_back(std::move(ch));
         }
@@ -875,7 +882,8 @@ int launch_chunk(msv_grid* g, const msv_grid::Chunk& ch, int counter_base, cudaS
             if (g->scen[si].flags & MSV_FLAG_CHECK_WAIT) p.any_check_wait = 1;
         }
         const bool full = g->records || p.any_routing || p.any_bad || p.any_check_wait || p.any_usage;
-        const int occ = msv::sim_max_blocks_per_sm(k.W, k.S, k.sched, g->records, full, g->n_cells);
+        p.lazy = k.lazy;
+        const int occ = msv::sim_max_blocks_per_sm(k.W, k.S, k.sched, g->records, full, k.lazy != 0, g->n_cells);
         if (occ <= 0) return fail(MSV_CUDA, "sim kernel: no occupancy for class");
         const int segs_per_block = msv::kSimWarpsPerBlock * (32 / k.W);
         const int need = (nwork + segs_per_block - 1) / segs_per_block;

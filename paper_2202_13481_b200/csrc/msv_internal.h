@@ -87,6 +87,7 @@ struct SimParams {
     int32_t any_bad;         // some plan has a size the profile lacks
     int32_t any_check_wait;  // some scenario sets MSV_FLAG_CHECK_WAIT
     int32_t any_usage;       // per-partition usage (PartitionUsage) requested
+    int32_t lazy;            // warp kernel: lazy folds for long queues (overloaded scenarios)
 };
 
 // Trace generation job (sample_trace, workload.hpp:97-113).
@@ -172,7 +173,7 @@ cudaError_t launch_trace_gen(const TraceJob* d_jobs, int n_jobs, int log1p_varia
 cudaError_t launch_sim(int W, int S, int sched, bool records, const SimParams& p, int blocks,
                        cudaStream_t stream);
 size_t sim_smem_bytes(int W, int S, int n_cells);
-int sim_max_blocks_per_sm(int W, int S, int sched, bool records, bool full, int n_cells);
+int sim_max_blocks_per_sm(int W, int S, int sched, bool records, bool full, bool lazy, int n_cells);
 cudaError_t launch_tail(const TailJob* d_jobs, int n_jobs, const double* d_p, int n_p,
                         cudaStream_t stream);
 cudaError_t launch_dispatch(const DispatchParams& p, cudaStream_t stream);

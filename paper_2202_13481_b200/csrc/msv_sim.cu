@@ -492,7 +492,7 @@ void* pick_sim(int W, int S, int sched, bool rec, bool full) {
 
 }  // namespace
 
-void* sim_warp_fn(int S, int sched, bool rec, bool full);  // msv_sim_warp.cu
+void* sim_warp_fn(int S, int sched, bool rec, bool full, bool lazy);  // msv_sim_warp.cu
 size_t sim_warp_smem_bytes(int S, int n_cells);
 
 size_t sim_smem_bytes(int W, int S, int n_cells) {
@@ -505,12 +505,12 @@ size_t sim_smem_bytes(int W, int S, int n_cells) {
     return tab + (size_t)kSimWarpsPerBlock * per_warp;
 }
 
-static void* sim_fn_for(int W, int S, int sched, bool rec, bool full) {
-    return W == 32 ? sim_warp_fn(S, sched, rec, full) : pick_sim(W, S, sched, rec, full);
+static void* sim_fn_for(int W, int S, int sched, bool rec, bool full, bool lazy) {
+    return W == 32 ? sim_warp_fn(S, sched, rec, full, lazy) : pick_sim(W, S, sched, rec, full);
 }
 
-int sim_max_blocks_per_sm(int W, int S, int sched, bool records, bool full, int n_cells) {
-    void* fn = sim_fn_for(W, S, sched, records, full);
+int sim_max_blocks_per_sm(int W, int S, int sched, bool records, bool full, bool lazy, int n_cells) {
+    void* fn = sim_fn_for(W, S, sched, records, full, lazy);
     if (!fn) return 0;
     const size_t smem = sim_smem_bytes(W, S, n_cells);
     if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) return 0;
@@ -522,7 +522,7 @@ int sim_max_blocks_per_sm(int W, int S, int sched, bool records, bool full, int 
 
 cudaError_t launch_sim(int W, int S, int sched, bool records, const SimParams& p, int blocks, cudaStream_t stream) {
     const bool full = records || p.any_routing || p.any_bad || p.any_check_wait || p.any_usage;
-    void* fn = sim_fn_for(W, S, sched, records, full);
+    void* fn = sim_fn_for(W, S, sched, records, full, p.lazy != 0);
     if (!fn) return cudaErrorInvalidValue;
     const size_t smem = sim_smem_bytes(W, S, p.n_cells);
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

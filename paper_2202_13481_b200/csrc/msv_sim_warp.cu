@@ -42,13 +42,35 @@ struct WarpSmem {
     int32_t win_b[32];
     uint32_t g_head[S][32];  // overflow list head / tail per lane slot
     uint32_t g_tail[S][32];
+    double dd_hi[S][32];     // overflow mode: double-double sum of the queued latencies
+    double dd_lo[S][32];
 };
 
-template <int S, int SCHED, bool REC, bool FULL>
+// Error-free sum (Knuth two-sum) and a double-double accumulator (RN, no contraction).
+__device__ __forceinline__ void dd_add(double& hi, double& lo, double x) {
+    const double s = hi + x;
+    const double bp = s - hi;
+    const double e = (hi - (s - bp)) + (x - bp);
+    const double t = lo + e;
+    hi = s + t;
+    lo = t - (hi - s);
+}
+
+template <int S, int SCHED, bool REC, bool FULL, bool LAZY>
 __global__ void __launch_bounds__(kSimWarpsPerBlock * 32, WarpCfg<S>::min_blocks)
     sim_warp_kernel(const SimParams p) {
     constexpr int QC = WarpCfg<S>::qcap;
     constexpr bool kFold = (SCHED == MSV_ELSA) || FULL;  // Eq. 1 needed (ELSA, or the check)
+    // Plain ELSA keeps long queues' folds lazily: while a slot's FIFO spills into the
+    // overflow list, a pop no longer refolds the queue (O(queue)); the slot keeps a
+    // double-double sum of its queued latencies instead, which bounds the left fold to
+    // +-(n+4)*2^-52 relative, and the exact fold is recomputed only when a decision
+    // cannot be settled from the bounds (an overloaded scenario becomes O(1) per arrival).
+    // (A separate instantiation, chosen by the host for scenarios offered more than the
+    // plan's nominal capacity: the extra paths cost the plain kernel registers.)
+    constexpr bool kLazy = LAZY && (SCHED == MSV_ELSA) && !FULL;
+    constexpr int32_t kFv = 1 << 30;  // pk bit: fold[s] holds the exact left fold
+    constexpr int kLazyMin = 48;      // queues up to this length are refolded eagerly
     extern __shared__ __align__(16) unsigned char smem[];
     double* s_lat = reinterpret_cast<double*>(smem);
     double* s_util = s_lat + p.n_cells;
@@ -162,6 +184,7 @@ __global__ void __launch_bounds__(kSimWarpsPerBlock * 32, WarpCfg<S>::min_blocks
                         c_meta[s] = W.q_meta[s][h][lane];
                         qh[s] = (h + 1) & (QC - 1);
                         qn[s] -= 1;
+                        const bool spilled = gn[s] > 0;  // overflow mode before this pop
                         if (gn[s] > 0) {  // refill the ring from the overflow list
                             const uint32_t g = W.g_head[s][lane];
                             W.g_head[s][lane] = g_next[g];
@@ -176,7 +199,20 @@ __global__ void __launch_bounds__(kSimWarpsPerBlock * 32, WarpCfg<S>::min_blocks
                         c_start[s] = now;
                         c_est[s] = est;
                         c_comp[s] = now + est;
-                        if (kFold) fold[s] = refold(s);
+                        if (kLazy && spilled && gn[s] > 0) {  // still spilled: drop the head from the sum
+                            double hi = W.dd_hi[s][lane], lo = W.dd_lo[s][lane];
+                            dd_add(hi, lo, -est);
+                            W.dd_hi[s][lane] = hi;
+                            W.dd_lo[s][lane] = lo;
+                            if (qn[s] + (int)gn[s] > kLazyMin) {
+                                pk[s] &= ~kFv;  // long queue: the fold is stale until a decision needs it
+                            } else {
+                                fold[s] = refold(s);  // short spill: refolding is cheap
+                                pk[s] |= kFv;
+                            }
+                        } else if (kFold) {
+                            fold[s] = refold(s);  // the queue fits the ring: cheap exact fold
+                        }
                     } else {
                         busy[s] = false;
                         fold[s] = 0.0;
@@ -278,9 +314,96 @@ __global__ void __launch_bounds__(kSimWarpsPerBlock * 32, WarpCfg<S>::min_blocks
                     }
                     // ---- decision ----
                     int ch = -1;  // chosen order index
-                    int kind;
+                    int kind = MSV_SLACK_SATISFYING;
                     bool mine[S];  // this lane's slot s is the chosen partition
-                    if constexpr (SCHED == MSV_ELSA && S == 1 && !FULL) {
+                    bool bounded = false;
+                    if constexpr (kLazy) {
+                        bool stale = false;
+#pragma unroll
+                        for (int s = 0; s < S; ++s) stale |= gn[s] > 0 && !(pk[s] & kFv);
+                        bounded = __any_sync(kFull, stale);
+                    }
+                    if (bounded) {
+                        // Some slot's fold is stale: decide on bounds, refold only the slots a
+                        // decision cannot be settled without (Step A near sla, Step B near the min).
+                        double vlo[S], vhi[S];
+                        bool stl[S];
+#pragma unroll
+                        for (int s = 0; s < S; ++s) {
+                            const double x = c_est[s] - (t - c_start[s]);
+                            const double xp = (busy[s] && 0.0 < x) ? x : 0.0;
+                            stl[s] = gn[s] > 0 && !(pk[s] & kFv);
+                            double flo = fold[s], fhi = fold[s];
+                            if (stl[s]) {  // |left fold - exact sum| <= (n-1) 2^-53 sum; slack x2
+                                const double hi = W.dd_hi[s][lane], lo = W.dd_lo[s][lane];
+                                const double g = (double)(qn[s] + (int)gn[s] + 4) * 0x1p-52;
+                                flo = __dmul_rd(__dadd_rd(hi, lo), __dadd_rd(1.0, -g));
+                                fhi = __dmul_ru(__dadd_ru(hi, lo), __dadd_ru(1.0, g));
+                            }
+                            // RN additions are monotone: the exact w + est lies in [vlo, vhi]
+                            vlo[s] = (flo + xp) + est_n[s];
+                            vhi[s] = (fhi + xp) + est_n[s];
+                        }
+                        auto exact = [&](int s) {  // refold slot s and make its value exact
+                            fold[s] = refold(s);
+                            pk[s] |= kFv;
+                            stl[s] = false;
+                            const double x = c_est[s] - (t - c_start[s]);
+                            vlo[s] = vhi[s] = (fold[s] + ((busy[s] && 0.0 < x) ? x : 0.0)) + est_n[s];
+                        };
+#pragma unroll
+                        for (int s = 0; s < S; ++s) {  // Step A (sched.hpp:125-130), slots in order
+                            bool pred;
+                            if constexpr (UNIT) {
+                                if (act[s] && stl[s] && sla > vlo[s] && !(sla > vhi[s])) exact(s);
+                                pred = act[s] && (sla > vhi[s]);
+                            } else {
+                                if (act[s] && stl[s]) exact(s);
+                                const double x = c_est[s] - (t - c_start[s]);
+                                const double w = fold[s] + ((busy[s] && 0.0 < x) ? x : 0.0);
+                                pred = act[s] && (sla > alpha * (w + beta * est_n[s]));
+                            }
+                            const unsigned bA = __ballot_sync(kFull, pred);
+                            if (bA) {
+                                ch = s * 32 + __ffs(bA) - 1;
+                                break;
+                            }
+                        }
+                        if (ch < 0) {  // Step B (sched.hpp:132-142): argmin w + est, earliest on ties
+                            uint64_t lm = ~0ull;
+#pragma unroll
+                            for (int s = 0; s < S; ++s)
+                                if (act[s]) lm = msv_dbits(vhi[s]) < lm ? msv_dbits(vhi[s]) : lm;
+                            const uint64_t mhi = seg_min_u64<32>(lm);  // >= the true minimum
+                            bool cnd[S];
+                            int ncand = 0;
+#pragma unroll
+                            for (int s = 0; s < S; ++s) {
+                                cnd[s] = act[s] && msv_dbits(vlo[s]) <= mhi;  // may attain the minimum
+                                ncand += __popc(__ballot_sync(kFull, cnd[s]));
+                            }
+                            if (ncand > 1) {  // overlapping candidates: compare exact values
+                                uint64_t lv = ~0ull;
+#pragma unroll
+                                for (int s = 0; s < S; ++s) {
+                                    if (cnd[s] && stl[s]) exact(s);
+                                    if (cnd[s]) lv = msv_dbits(vhi[s]) < lv ? msv_dbits(vhi[s]) : lv;
+                                }
+                                const uint64_t vmin = seg_min_u64<32>(lv);
+#pragma unroll
+                                for (int s = S - 1; s >= 0; --s) cnd[s] = cnd[s] && msv_dbits(vhi[s]) == vmin;
+                            }
+                            // a single candidate is the argmin whatever its exact value
+#pragma unroll
+                            for (int s = S - 1; s >= 0; --s) {
+                                const unsigned bB = __ballot_sync(kFull, cnd[s]);
+                                if (bB) ch = s * 32 + __ffs(bB) - 1;
+                            }
+                            kind = MSV_FASTEST_FALLBACK;
+                        }
+#pragma unroll
+                        for (int s = 0; s < S; ++s) mine[s] = s * 32 + lane == ch;
+                    } else if constexpr (SCHED == MSV_ELSA && S == 1 && !FULL) {
                         // One slot per lane: the chosen lane is the lowest set bit of the
                         // ballot, i.e. the lane with no set bit below it — no bit scan on the
                         // critical path.
@@ -411,8 +534,10 @@ __global__ void __launch_bounds__(kSimWarpsPerBlock * 32, WarpCfg<S>::min_blocks
                         }
                     }
                     if constexpr (!(SCHED == MSV_ELSA && S == 1 && !FULL)) {
+                        if (!bounded) {
 #pragma unroll
-                        for (int s = 0; s < S; ++s) mine[s] = s * 32 + lane == ch;
+                            for (int s = 0; s < S; ++s) mine[s] = s * 32 + lane == ch;
+                        }
                     }
                     // ---- start or enqueue on the chosen partition (engine.hpp:225-230) ----
 #pragma unroll
@@ -435,12 +560,28 @@ __global__ void __launch_bounds__(kSimWarpsPerBlock * 32, WarpCfg<S>::min_blocks
                                     W.q_meta[s][e][lane] = meta;
                                     qn[s] += 1;
                                 } else {
+                                    if (kLazy) {  // overflow mode: keep the double-double sum
+                                        double hi = 0.0, lo = 0.0;
+                                        if (gn[s] == 0) {  // entering it: sum the ring, the fold is exact
+#pragma unroll 1
+                                            for (int k = 0; k < qn[s]; ++k)
+                                                dd_add(hi, lo, W.q_est[s][(qh[s] + k) & (QC - 1)][lane]);
+                                            pk[s] |= kFv;
+                                        } else {
+                                            hi = W.dd_hi[s][lane];
+                                            lo = W.dd_lo[s][lane];
+                                        }
+                                        dd_add(hi, lo, est);
+                                        W.dd_hi[s][lane] = hi;
+                                        W.dd_lo[s][lane] = lo;
+                                    }
                                     if (gn[s] == 0) W.g_head[s][lane] = (uint32_t)i;
                                     else g_next[W.g_tail[s][lane]] = (uint32_t)i;
                                     W.g_tail[s][lane] = (uint32_t)i;
                                     gn[s] += 1;
                                 }
-                                fold[s] = fold[s] + est;  // appending extends the left fold exactly
+                                // appending extends the left fold exactly (a stale fold stays stale)
+                                fold[s] = fold[s] + est;
                             }
                             if (REC) {
                                 rec[i].partition = pk[s] & 0xff;
@@ -501,17 +642,24 @@ __global__ void __launch_bounds__(kSimWarpsPerBlock * 32, WarpCfg<S>::min_blocks
 }
 
 template <int S, int SCHED>
-void* pick_flags(bool rec, bool full) {
-    if (rec) return (void*)&sim_warp_kernel<S, SCHED, true, true>;
-    return full ? (void*)&sim_warp_kernel<S, SCHED, false, true> : (void*)&sim_warp_kernel<S, SCHED, false, false>;
+void* pick_flags(bool rec, bool full, bool lazy) {
+    if (rec) return (void*)&sim_warp_kernel<S, SCHED, true, true, false>;
+    if (full) return (void*)&sim_warp_kernel<S, SCHED, false, true, false>;
+    if constexpr (SCHED == MSV_ELSA) {
+        if (lazy) return (void*)&sim_warp_kernel<S, SCHED, false, false, true>;
+    }
+    return (void*)&sim_warp_kernel<S, SCHED, false, false, false>;
 }
 
 }  // namespace
 
-void* sim_warp_fn(int S, int sched, bool rec, bool full) {
-    if (S == 1) return sched == MSV_ELSA ? pick_flags<1, MSV_ELSA>(rec, full) : pick_flags<1, MSV_FIFS>(rec, full);
-    if (S == 2) return sched == MSV_ELSA ? pick_flags<2, MSV_ELSA>(rec, full) : pick_flags<2, MSV_FIFS>(rec, full);
-    if (S == 4) return sched == MSV_ELSA ? pick_flags<4, MSV_ELSA>(rec, full) : pick_flags<4, MSV_FIFS>(rec, full);
+void* sim_warp_fn(int S, int sched, bool rec, bool full, bool lazy) {
+    if (S == 1)
+        return sched == MSV_ELSA ? pick_flags<1, MSV_ELSA>(rec, full, lazy) : pick_flags<1, MSV_FIFS>(rec, full, lazy);
+    if (S == 2)
+        return sched == MSV_ELSA ? pick_flags<2, MSV_ELSA>(rec, full, lazy) : pick_flags<2, MSV_FIFS>(rec, full, lazy);
+    if (S == 4)
+        return sched == MSV_ELSA ? pick_flags<4, MSV_ELSA>(rec, full, lazy) : pick_flags<4, MSV_FIFS>(rec, full, lazy);
     return nullptr;
 }
 

@@ -176,6 +176,27 @@ def test_grid_overloaded_elsa(eng, ref):
     assert_grid_equal(eng.run_grid(specs), ref.run_grid(specs))
 
 
+def test_grid_deep_overload_lazy_folds(eng, ref):
+    """Deeply overloaded ELSA scenarios (queues of thousands, far beyond the shared ring)
+    run in the lazy-fold kernel variant: decisions from double-double bounds, exact
+    refolds only when a bound cannot settle them. Results stay bit-identical, including
+    plans with several slots per lane (P > 32) and alpha/beta != 1 (always exact)."""
+    specs = []
+    for name, gpus in (("resnet50", 1), ("mobilenet", 2), ("bert_base", 8)):
+        m = W.model(name)
+        p = W.paris(m, gpus)
+        peak = W.capacity_qps(m, p)
+        specs += [W._spec(m, p, load * peak, 6000, s) for load in (1.05, 1.3, 2.0, 4.0) for s in (1, 2)]
+    m = W.model("mobilenet")
+    p = PartitionPlan(8, 7, [[1] * 7 for _ in range(8)])  # P = 56: two slots per lane
+    specs += [W._spec(m, p, load * W.capacity_qps(m, p), 6000, 3) for load in (1.5, 2.5)]
+    r50 = W.model("resnet50")
+    sla = SlaConfig(r50.sla.sla_target_ms, 1.3, 0.9)
+    specs += [GridSpec(W.paris(r50, 1), r50.table, r50.dist, sla, 2.0 * W.capacity_qps(r50, W.paris(r50, 1)),
+                       6000 / (2.0 * W.capacity_qps(r50, W.paris(r50, 1))) * 1000.0, 7, "elsa")]
+    assert_grid_equal(eng.run_grid(specs), ref.run_grid(specs))
+
+
 def test_grid_class_widths(eng, ref):
     """One scenario class per kernel instantiation: P = 1..4 (W=4), 8, 16, 32, 43 (S=2), 80 (S=4)."""
     m = W.model("mobilenet")
