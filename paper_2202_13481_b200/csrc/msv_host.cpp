@@ -239,7 +239,7 @@ int segmented_mode() {
 ClassKey class_of(int P, int sched, int seg_w, bool overloaded = false) {
     ClassKey c{32, 1, sched};
     if (segmented_mode() == 1) seg_w = 4;
-    if (overloaded && sched == MSV_ELSA) seg_w = 32;  // long queues: the lazy warp kernel (below)
+    if (overloaded && sched == MSV_ELSA && segmented_mode() != 1) seg_w = 32;  // long queues: lazy warp kernel
     if (P <= 4 && seg_w <= 4) c.W = 4;
     else if (P <= 8 && seg_w <= 8) c.W = 8;
     else if (P <= 16 && seg_w <= 16) c.W = 16;
