@@ -17,6 +17,10 @@ namespace {
 
 constexpr int kBins = 2048;
 constexpr int kDigit = 11;
+// The first pass is shared by every percentile (same prefix): its histogram spans the
+// whole kMaxTails x kBins area, i.e. 13-bit digits, so the bin holding a target rank is
+// usually small enough to gather right away (2 passes instead of 3 on the bench grid).
+constexpr int kDigit0 = 13;
 constexpr int kMaxTails = 4;
 constexpr int kTailGather = 1024;  // per percentile
 
@@ -144,9 +148,14 @@ __global__ void __launch_bounds__(kTailThreads)
                             break;
                         }
             }
+            // pass 0: every open percentile rides on histogram 0 -> one wide histogram
+            bool shared0 = pass == 0;
+            for (int q = 0; q < n_p; ++q) shared0 = shared0 && (S.state[q] != 0 || hsrc[q] == 0);
+            const int dig = shared0 ? kDigit0 : kDigit;
+            unsigned int* const hbase = &S.hist[0][0];
             for (int q = 0; q < n_p; ++q) {
                 if (S.state[q] == 0 && hsrc[q] == q)
-                    for (int k = threadIdx.x; k < kBins; k += blockDim.x) S.hist[q][k] = 0;
+                    for (int k = threadIdx.x; k < (1 << dig); k += blockDim.x) hbase[q * kBins + k] = 0;
                 if (S.state[q] == 1 && threadIdx.x == 0) S.fill[q] = 0;
             }
             __syncthreads();
@@ -161,7 +170,7 @@ __global__ void __launch_bounds__(kTailThreads)
                 if (on && st_r[q] == 0 && hsrc[q] != q) st_r[q] = 3;  // rides on another histogram
                 pos_r[q] = on ? S.pos[q] : 0;
                 pre_r[q] = on ? S.prefix[q] : 0;
-                const int d = pos_r[q] < kDigit ? pos_r[q] : kDigit;
+                const int d = pos_r[q] < dig ? pos_r[q] : dig;
                 sh_r[q] = pos_r[q] - d;
                 dmask_r[q] = (1u << d) - 1u;
             }
@@ -185,7 +194,7 @@ __global__ void __launch_bounds__(kTailThreads)
                         if (st_r[q] == 0) {
                             const unsigned bin = hit ? (unsigned)((v[u] >> sh_r[q]) & dmask_r[q]) : 0xffffffffu;
                             const unsigned peers = __match_any_sync(kFull, bin);
-                            if (hit && lane == __ffs(peers) - 1) atomicAdd(&S.hist[q][bin], (unsigned)__popc(peers));
+                            if (hit && lane == __ffs(peers) - 1) atomicAdd(&hbase[q * kBins + bin], (unsigned)__popc(peers));
                         } else {
                             const unsigned m = __ballot_sync(kFull, hit);
                             unsigned slot = 0;
@@ -202,12 +211,12 @@ __global__ void __launch_bounds__(kTailThreads)
                 const int st = S.state[q];
                 if (st == 0) {
                     const int pos = S.pos[q];
-                    const int d = pos < kDigit ? pos : kDigit;
+                    const int d = pos < dig ? pos : dig;
                     const int nb = 1 << d;
                     const int per = (nb + blockDim.x - 1) / blockDim.x;
                     const int b0 = threadIdx.x * per;
                     unsigned int sum = 0;
-                    const unsigned int* H = S.hist[hsrc[q]];
+                    const unsigned int* H = hbase + hsrc[q] * kBins;
                     for (int k = b0; k < b0 + per && k < nb; ++k) sum += H[k];
                     // read before the scan's barriers: the owning thread rewrites S.rank[q] below
                     const long long r = S.rank[q];
