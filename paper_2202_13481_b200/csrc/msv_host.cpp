@@ -400,6 +400,9 @@ std::vector<uint64_t> route_masks(const std::vector<DevPart>& parts, const Routi
 int64_t trace_capacity(double rate_qps, double duration_ms) {
     const double mean = rate_qps * duration_ms / 1000.0;
     if (!(mean < 2.0e9)) return -1;  // the kernels index a trace with 32-bit ints
+    // MSV_TEST_SHORT_CAP=1 (tests only): undersized capacities exercise the re-run path
+    static const bool short_cap = getenv("MSV_TEST_SHORT_CAP") && atoi(getenv("MSV_TEST_SHORT_CAP")) != 0;
+    if (short_cap) return (int64_t)ceil(0.5 * mean) + 1;
     return (int64_t)ceil(mean + 10.0 * sqrt(mean) + 160.0);
 }
 

@@ -404,3 +404,42 @@ def test_chunking_and_classes_do_not_change_results():
         assert r.returncode == 0, r.stderr[-2000:]
         got = np.load(out)
         assert np.array_equal(got.view(np.uint64), want.view(np.uint64)), extra
+
+
+def _retry_grid_results():
+    eng = Engine(0)
+    m = W.model("resnet50")
+    p = W.paris(m, 1)
+    specs = [W._spec(m, p, 0.7 * W.capacity_qps(m, p), 3000, s) for s in range(1, 41)]
+    r = eng.run_grid(specs, usage=True)
+    return r["placement_hash"], r["tail"], r["total"], r["usage"]["busy_ms"]
+
+
+def test_grid_edge_cases(eng, ref):
+    """Empty grids, scenarios without arrivals (rate 0, duration 0), single-query traces,
+    and traces that overflow their Poisson-tail capacity (re-run with a larger one)."""
+    import os
+    import sys
+    assert eng.run_grid([])["total"].shape == (0,)
+    m = W.model("resnet50")
+    p = W.paris(m, 1)
+    # sample_trace's own argument checks (workload.hpp:99-100)
+    for rate, dur in ((0.0, 1000.0), (-1.0, 1000.0), (500.0, -1.0)):
+        with pytest.raises(ParamError):
+            eng.run_grid([GridSpec(p, m.table, m.dist, m.sla, rate, dur, 1)])
+    specs = [GridSpec(p, m.table, m.dist, m.sla, 500.0, 0.0, 2), GridSpec(p, m.table, m.dist, m.sla, 1e-3, 10.0, 5),
+             GridSpec(p, m.table, m.dist, m.sla, 1.0, 1500.0, 3), W._spec(m, p, 900.0, 500, 4)]
+    got, want = eng.run_grid(specs), ref.run_grid(specs)
+    assert_grid_equal(got, want)
+    assert got["total"][0] == 0 and got["total"][1] == 0 and np.isnan(got["tail"][0]).all()
+    # capacity overflow: every trace longer than its (test-shortened) capacity is re-run
+    base = _retry_grid_results()
+    code = ("import sys, numpy as np; sys.path.insert(0, %r); from tests.test_gpu_parity import _retry_grid_results; "
+            "h, t, n, u = _retry_grid_results(); np.save(sys.argv[1], np.concatenate([h.view(np.float64), t.ravel(), "
+            "n.astype(np.float64), u]))" % str(ROOT))
+    out = Path(f"/tmp/msv_retry_{os.getpid()}.npy")
+    r = subprocess.run([sys.executable, "-c", code, str(out)], capture_output=True, text=True,
+                       env=dict(os.environ, MSV_TEST_SHORT_CAP="1"), timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    want = np.concatenate([base[0].view(np.float64), base[1].ravel(), base[2].astype(np.float64), base[3]])
+    assert np.array_equal(np.load(out).view(np.uint64), want.view(np.uint64))
