@@ -267,7 +267,8 @@ def main():
         issue = None
         if prof_k2:
             ach = prof_k2["warp_instructions_per_query"] * queries / sim_s
-            pk = 148 * 4 * clk_mhz * 1e6
+            sms = torch.cuda.get_device_properties(dev).multi_processor_count
+            pk = sms * 4 * clk_mhz * 1e6  # one warp-instruction per scheduler per clock
             issue = {"achieved_warp_inst_per_s": ach, "peak_warp_inst_per_s": pk, "frac": ach / pk,
                      "warp_inst_per_query": prof_k2["warp_instructions_per_query"], "source": prof_src}
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
