@@ -252,10 +252,11 @@ def main():
             pass
         peak = float(peaks.get("hbm_gbs", 6650.0))
         # per-launch DRAM traffic and instruction mix of K2 from the committed ncu capture
-        prof_k2, prof_src = None, None
+        prof_k2, prof_src, prof_all = None, None, {}
         for sp in sorted((ROOT / "profiles").glob("r*/summary.json"), reverse=True):
             try:
-                prof_k2 = json.loads(sp.read_text())["kernels"]["K2 sim_warp_kernel"]
+                prof_all = json.loads(sp.read_text())["kernels"]
+                prof_k2 = prof_all["K2 sim_warp_kernel"]
                 prof_src = str(sp.relative_to(ROOT))
                 break
             except Exception:
@@ -271,6 +272,11 @@ def main():
             pk = sms * 4 * clk_mhz * 1e6  # one warp-instruction per scheduler per clock
             issue = {"achieved_warp_inst_per_s": ach, "peak_warp_inst_per_s": pk, "frac": ach / pk,
                      "warp_inst_per_query": prof_k2["warp_instructions_per_query"], "source": prof_src}
+            # the whole overlapped step: K1 + K2 + K3 instructions per query over the step time
+            wi = sum(prof_all[k]["warp_instructions_per_query"] for k in prof_all
+                     if "warp_instructions_per_query" in prof_all[k] and not k.startswith("K4"))
+            issue["step_warp_inst_per_query"] = wi
+            issue["step_frac"] = wi * total_q * args.steps / (dev_ms_max / 1000.0) / world / pk
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": dev_ms_max / args.steps, "higher_is_better": True,
                 "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
