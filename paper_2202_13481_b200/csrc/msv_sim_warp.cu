@@ -1,20 +1,24 @@
-// K2 for plans of 17..128 partitions: sim_warp_kernel — one scenario per warp.
-//
-// Same semantics as msv_sim.cu (see its header for the per-arrival protocol) with
-// the warp-uniform structure this class allows:
-//   * scenario -> 32-arrival window -> arrival loops, no per-arrival bookkeeping;
-//     each window is staged in shared memory and broadcast by LDS;
-//   * the window's first measured arrival is one ballot;
-//   * Step A = ballot + first set bit; Step B's 64-bit argmin = two REDUX.MIN;
-//     FIFS = REDUX.MIN over (k, id) / (queue length, id) keys;
-//   * the FIFO fold of Eq. 1 is kept exact at all times: extended on append and
-//     recomputed in FIFO order when the head leaves (ELSA), so a dispatch is
-//     branch-free: w = fold + max(0, est - (now - start));
-//   * template flags: UNIT (alpha = beta = 1, per scenario: 1*x == x bit for bit)
-//     and FULL (segment routing / sizes missing from the profile / wait-consistency
-//     check present in the launch; the plain variant carries none of their votes);
-//   * the horizon is the last completion each lane retained.
-// Lane slot s of lane l owns by_ascending_size order index s*32 + l (sched.hpp:96-104).
+// K2 sim_warp_kernel: run() (engine.hpp:115-253) with ELSA (sched.hpp:119-143) or FIFS
+// (sched.hpp:154-170), one scenario per warp, for plans of up to 32*S partitions (S = 1,
+// 2, 4 slots per lane; lane slot s of lane l owns by_ascending_size order index s*32 + l,
+// sched.hpp:96-104). The per-arrival protocol is msv_sim.cu's (see its header); this
+// kernel adds the warp-uniform structure one scenario per warp allows:
+//   * scenario -> 32-arrival window (staged in shared memory) -> arrival loop; the
+//     window's first measured arrival is one ballot;
+//   * the batch's latency row is loaded ahead of the drain; the drain is lane-local;
+//   * Step A = ballot; with one slot the chosen lane is the one with no set ballot bit
+//     below it (no bit scan on the critical path); with several slots the slots are
+//     scanned in order and later slots' waits are computed only when needed;
+//     Step B's 64-bit argmin = two REDUX.MIN + ballot; FIFS = REDUX.MIN over (k, id) /
+//     (queue length, id) keys;
+//   * the FIFO fold of Eq. 1 is exact: extended on append, recomputed from the queue
+//     head when the head leaves (ELSA); the LAZY instantiation (scenarios offered more
+//     than the plan's capacity) bounds long queues' folds with a double-double sum and
+//     refolds only when a decision needs the exact value;
+//   * template flags: UNIT (alpha = beta = 1, per scenario: 1*x == x bit for bit), FULL
+//     (segment routing / missing sizes / wait check / usage / records in the launch; the
+//     plain variant carries none of that work), REC (per-query records), LAZY;
+//   * the horizon is the last completion each slot retained.
 #include <type_traits>
 
 #include "msv_device.cuh"
