@@ -1354,10 +1354,86 @@ int msv_transfer_bytes(msv_ctx* ctx, int64_t* h2d, int64_t* d2h) {
     return MSV_OK;
 }
 
+}  // extern "C"
+
+namespace {
+
+// The kernels stage a grid's profile cells in shared memory (<= kMaxSmemCells). A call
+// whose scenarios use more distinct profile cells than that runs as several grids, one per
+// group of profiles that fits (the reference has no such limit). Returns false when one
+// grid suffices (or a handle is invalid: the single-grid path reports the error).
+bool profile_groups(const msv_ctx* ctx, const msv_scenario* sc, int64_t n, std::vector<std::vector<int64_t>>* groups) {
+    std::map<int32_t, int> group_of;
+    std::vector<int> cells;  // per group
+    int64_t total = 0;
+    for (int64_t i = 0; i < n; ++i) {
+        const int32_t pf = sc[i].profile;
+        if (pf < 0 || pf >= (int32_t)ctx->profiles.size()) return false;
+        if (group_of.count(pf)) continue;
+        const int c = (int)ctx->profiles[pf].lat.size();
+        if (c > msv::kMaxSmemCells) return false;
+        total += c;
+        if (cells.empty() || cells.back() + c > msv::kMaxSmemCells) cells.push_back(0);
+        cells.back() += c;
+        group_of[pf] = (int)cells.size() - 1;
+    }
+    if (total <= msv::kMaxSmemCells) return false;
+    groups->assign(cells.size(), {});
+    for (int64_t i = 0; i < n; ++i) (*groups)[group_of[sc[i].profile]].push_back(i);
+    return true;
+}
+
+int run_grid_core(msv_ctx* ctx, const msv_scenario* scenarios, int64_t n, const double* tail_p, int n_tails,
+                  msv_result* results, msv_usage* usage);
+
+}  // namespace
+
+extern "C" {
+
 int msv_run_grid(msv_ctx* ctx, const msv_scenario* scenarios, int64_t n, const double* tail_p, int n_tails,
                  msv_result* results, msv_usage* usage) {
     if (!ctx || (n > 0 && (!scenarios || !results))) return fail(MSV_PARAM, "null argument");
     SetDevice sd(ctx->device);
+    std::vector<std::vector<int64_t>> groups;
+    if (!profile_groups(ctx, scenarios, n, &groups)) return run_grid_core(ctx, scenarios, n, tail_p, n_tails, results, usage);
+    // validate everything first, so errors name the caller's scenario index
+    std::vector<int64_t> use_off(n + 1, 0);
+    for (int64_t i = 0; i < n; ++i) {
+        int32_t P = 0;
+        const int rc = validate_scenario(ctx, scenarios[i], true, &P);
+        if (rc) {
+            g_err = "scenario " + std::to_string(i) + ": " + g_err;
+            return rc;
+        }
+        use_off[i + 1] = use_off[i] + P;
+    }
+    for (const std::vector<int64_t>& grp : groups) {
+        std::vector<msv_scenario> sub;
+        for (int64_t i : grp) sub.push_back(scenarios[i]);
+        std::vector<msv_result> sub_res(sub.size());
+        int64_t nu = 0;
+        for (int64_t i : grp) nu += use_off[i + 1] - use_off[i];
+        std::vector<msv_usage> sub_use(std::max<int64_t>(nu, 1));
+        const int rc = run_grid_core(ctx, sub.data(), (int64_t)sub.size(), tail_p, n_tails, sub_res.data(),
+                                     usage ? sub_use.data() : nullptr);
+        if (rc) return rc;
+        int64_t u = 0;
+        for (size_t j = 0; j < grp.size(); ++j) {
+            const int64_t i = grp[j];
+            results[i] = sub_res[j];
+            if (usage)
+                for (int64_t q = use_off[i]; q < use_off[i + 1]; ++q) usage[q] = sub_use[u++];
+        }
+    }
+    return MSV_OK;
+}
+
+}  // extern "C"
+
+namespace {
+
+int run_grid_core(msv_ctx* ctx, const msv_scenario* scenarios, int64_t n, const double* tail_p, int n_tails,
+                  msv_result* results, msv_usage* usage) {
     msv_grid* g = nullptr;
     static const bool host_timing = getenv("MSV_HOST_TIMING") != nullptr;
     const auto t0 = std::chrono::steady_clock::now();
@@ -1403,7 +1479,7 @@ int msv_run_grid(msv_ctx* ctx, const msv_scenario* scenarios, int64_t n, const d
         std::vector<msv_result> sub_res(sub.size());
         std::vector<msv_usage> sub_use(std::max<int64_t>(usage_n, 1));
         std::vector<int64_t> again;
-        rc = grid_results(g2, sub_res.data(), sub_use.data(), nullptr, &again);
+        rc = grid_results(g2, sub_res.data(), usage ? sub_use.data() : nullptr, nullptr, &again);
         if (rc) return rc;
         std::vector<int64_t> next_retry, next_caps;
         size_t again_pos = 0;
@@ -1425,11 +1501,59 @@ int msv_run_grid(msv_ctx* ctx, const msv_scenario* scenarios, int64_t n, const d
     return MSV_OK;
 }
 
+}  // namespace
+
+extern "C" {
+
 int msv_run_replay(msv_ctx* ctx, const msv_scenario* scenarios, int64_t n, const int64_t* offsets,
                    const double* arrival_ms, const int32_t* batch, const double* tail_p, int n_tails,
                    msv_result* results, msv_usage* usage, msv_record* records) {
     if (!ctx || (n > 0 && (!scenarios || !results || !offsets))) return fail(MSV_PARAM, "null argument");
     SetDevice sd(ctx->device);
+    std::vector<std::vector<int64_t>> groups;
+    if (profile_groups(ctx, scenarios, n, &groups)) {  // more profile cells than one grid holds
+        std::vector<int64_t> use_off(n + 1, 0);
+        for (int64_t i = 0; i < n; ++i) {
+            int32_t P = 0;
+            const int rc = validate_scenario(ctx, scenarios[i], false, &P);
+            if (rc) {
+                g_err = "scenario " + std::to_string(i) + ": " + g_err;
+                return rc;
+            }
+            use_off[i + 1] = use_off[i] + P;
+        }
+        for (const std::vector<int64_t>& grp : groups) {
+            std::vector<msv_scenario> sub;
+            std::vector<int64_t> off{0};
+            std::vector<double> arr;
+            std::vector<int32_t> bat;
+            int64_t nu = 0;
+            for (int64_t i : grp) {
+                sub.push_back(scenarios[i]);
+                arr.insert(arr.end(), arrival_ms + offsets[i], arrival_ms + offsets[i + 1]);
+                bat.insert(bat.end(), batch + offsets[i], batch + offsets[i + 1]);
+                off.push_back((int64_t)arr.size());
+                nu += use_off[i + 1] - use_off[i];
+            }
+            std::vector<msv_result> sub_res(sub.size());
+            std::vector<msv_usage> sub_use(std::max<int64_t>(nu, 1));
+            std::vector<msv_record> sub_rec(std::max<size_t>(arr.size(), 1));
+            const int rc = msv_run_replay(ctx, sub.data(), (int64_t)sub.size(), off.data(), arr.data(), bat.data(), tail_p,
+                                          n_tails, sub_res.data(), usage ? sub_use.data() : nullptr,
+                                          records ? sub_rec.data() : nullptr);
+            if (rc) return rc;
+            int64_t u = 0;
+            for (size_t j = 0; j < grp.size(); ++j) {
+                const int64_t i = grp[j];
+                results[i] = sub_res[j];
+                if (usage)
+                    for (int64_t q = use_off[i]; q < use_off[i + 1]; ++q) usage[q] = sub_use[u++];
+                if (records)
+                    for (int64_t q = offsets[i]; q < offsets[i + 1]; ++q) records[q] = sub_rec[off[j] + (q - offsets[i])];
+            }
+        }
+        return MSV_OK;
+    }
     msv_grid* g = nullptr;
     int rc = grid_build(ctx, scenarios, n, tail_p, n_tails, offsets, arrival_ms, batch, records != nullptr, &g, nullptr, true);
     if (rc) return rc;

@@ -1,0 +1,136 @@
+"""Randomised differential tests: the device engine vs the compiled reference on random
+inputs (fixed seeds): random profiles (synthetic and hand-made), batch distributions,
+partition plans (1..64 partitions, any mix of sizes), SLA / alpha / beta, loads from
+idle to deep overload, warm-up fractions, both schedulers, and — through run() on host
+traces — simultaneous arrivals, segment routing and the wait-consistency check. Every
+output is compared bit for bit (per-query records, counts, horizons, tails, hashes)."""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from paper_2202_13481_b200 import (BatchDistribution, Engine, GridSpec, PartitionPlan, ProfileTable, SlaConfig,
+                                   SyntheticProfileParams, derive_sla_target, lognormal_batch_pdf, synth_profile)
+from paper_2202_13481_b200 import workloads as W
+from tests import oracle_py as O
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def eng():
+    return Engine(0)
+
+
+@pytest.fixture(scope="module")
+def ref():
+    if not O.REF_LIB.exists():
+        pytest.skip("oracle/_ref not built")
+    return O.Oracle("reference")
+
+
+def _same(a, b):
+    a, b = np.asarray(a), np.asarray(b)
+    if a.dtype.kind == "f":
+        return a.shape == b.shape and np.array_equal(a.view(np.uint64), np.asarray(b, np.float64).view(np.uint64))
+    return np.array_equal(a, b)
+
+
+def _random_table(rng, i):
+    sizes = sorted(rng.choice([1, 2, 3, 4, 7], size=int(rng.integers(2, 6)), replace=False).tolist())
+    b_max = int(rng.choice([4, 8, 16, 32]))
+    if rng.random() < 0.6:
+        p = SyntheticProfileParams(float(rng.uniform(0.3, 12.0)), float(rng.uniform(0.2, 6.0)),
+                                   float(rng.uniform(0.05, 0.5)), float(rng.uniform(0.6, 1.0)))
+        return synth_profile(p, sizes, b_max)
+    n = len(sizes)
+    row = np.cumsum(rng.uniform(0.05, 4.0, size=b_max))
+    lat = np.stack([row * f for f in np.cumprod(rng.uniform(0.3, 1.0, size=n))])
+    util = np.sort(rng.uniform(0.0, 1.0, size=(n, b_max)), axis=1)
+    return ProfileTable(np.array(sizes, np.int32), b_max, lat, util, f"fuzz{i}")
+
+
+def _random_plan(rng, sizes):
+    gpus = int(rng.integers(1, 9))
+    per = []
+    for _ in range(gpus):
+        left, g = 7, []
+        while True:
+            fit = [k for k in sizes if k <= left]
+            if not fit or (g and rng.random() < 0.15):
+                break
+            k = int(rng.choice(fit))
+            g.append(k)
+            left -= k
+        per.append(sorted(g, reverse=True))
+    if sum(len(g) for g in per) == 0:
+        per[0] = [int(sizes[0])]
+    return PartitionPlan(gpus, 7, per)
+
+
+def test_fuzz_grids(eng, ref):
+    rng = np.random.default_rng(20260)
+    specs = []
+    for i in range(400):
+        table = _random_table(rng, i)
+        b = table.b_max
+        dist = lognormal_batch_pdf(float(rng.uniform(0.0, 2.0)), float(rng.uniform(0.3, 1.5)), b) \
+            if rng.random() < 0.7 else BatchDistribution(rng.uniform(0.0, 1.0, size=b) + 1e-3)
+        plan = _random_plan(rng, [int(k) for k in table.sizes])
+        m = W.Model("fuzz", table, dist, SlaConfig(1.0))
+        cap = W.capacity_qps(m, plan)
+        load = float(rng.choice([0.05, 0.3, 0.7, 0.95, 1.1, 1.6, 3.0]))
+        sla_ms = derive_sla_target(table, b, float(rng.uniform(0.6, 3.0)))
+        alpha, beta = (1.0, 1.0) if rng.random() < 0.6 else (float(rng.uniform(0.5, 1.5)), float(rng.uniform(0.5, 1.5)))
+        queries = float(rng.choice([200, 1500, 4000]))
+        rate = load * cap
+        specs.append(GridSpec(plan, table, dist, SlaConfig(sla_ms, alpha, beta), rate, queries / rate * 1000.0,
+                              int(rng.integers(1, 1 << 40)), "elsa" if rng.random() < 0.7 else "fifs",
+                              float(rng.choice([0.0, 0.1, 0.5]))))
+    got, want = eng.run_grid(specs, (0.5, 0.95, 0.99)), ref.run_grid(specs, (0.5, 0.95, 0.99))
+    for k in ("total", "violations", "measured", "measured_violations", "horizon_ms", "placement_hash", "tail",
+              "status"):
+        assert _same(got[k], want[k]), k
+
+
+KEYS = ("partition", "kind", "start_ms", "finish_ms", "busy_ms", "weighted_busy_ms", "queries", "total",
+        "violations", "measured", "measured_violations", "horizon_ms", "max_wait_estimate_diff")
+
+
+def test_fuzz_runs_with_routing_and_checks(eng, ref):
+    rng = np.random.default_rng(777)
+    items, wants = [], []
+    for i in range(120):
+        table = _random_table(rng, 1000 + i)
+        plan = _random_plan(rng, [int(k) for k in table.sizes])
+        n = int(rng.integers(0, 600))
+        gaps = rng.exponential(float(rng.uniform(0.2, 8.0)), size=n)
+        gaps[rng.random(n) < 0.2] = 0.0  # simultaneous arrivals
+        arrival = np.cumsum(gaps)
+        batch = rng.integers(1, table.b_max + 1, size=n).astype(np.int32)
+        duration = float(arrival[-1] * rng.uniform(0.5, 1.2)) if n else 100.0
+        sla = SlaConfig(derive_sla_target(table, table.b_max, float(rng.uniform(0.5, 3.0))),
+                        *((1.0, 1.0) if rng.random() < 0.5 else (float(rng.uniform(0.5, 1.5)), float(rng.uniform(0.5, 1.5)))))
+        routing = None
+        if rng.random() < 0.5:  # contiguous batch segments per size (paris.hpp:23-30 style)
+            ks = [int(k) for k in table.sizes]
+            cuts = sorted(rng.choice(np.arange(1, table.b_max), size=len(ks) - 1, replace=False).tolist()) \
+                if table.b_max > len(ks) else list(range(1, len(ks)))
+            lo, routing = 1, []
+            for j, k in enumerate(ks):
+                hi = cuts[j] if j < len(cuts) else table.b_max
+                routing.append((k, lo, hi))
+                lo = hi + 1
+        check = bool(rng.random() < 0.5)
+        sched = "elsa" if rng.random() < 0.6 else "fifs"
+        warm = float(rng.choice([0.0, 0.1, 0.4]))
+        got = eng.run(plan, sched, arrival, batch, duration, table, sla, warm, routing, check)
+        want = ref.run(plan, sched, arrival, batch, duration, table, sla, warm, routing, check)
+        for k in KEYS:
+            assert _same(got[k], want[k]), (i, k)
+        items.append((plan, sched, arrival, batch, duration, table, sla, warm, routing, check))
+        wants.append(want)
+    # all cases in one call: more profiles than one device table holds -> split grids
+    for i, (got, want) in enumerate(zip(eng.run_many(items), wants)):
+        for k in KEYS:
+            assert _same(got[k], want[k]), ("batched", i, k)
