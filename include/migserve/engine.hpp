@@ -1,8 +1,8 @@
 // Discrete-event simulation of a MIG-partitioned inference server — the same
 // API as the reference's engine.hpp (engine.hpp:23-313). run() executes on the
-// device (msv_run_replay -> sim_kernel): one warp segment simulates the trace with
-// one partition per lane, reproducing the reference's event order, placements and
-// timings bit for bit. Report formatting (CSV/JSON) stays on the host.
+// device (msv_run_replay -> the K2 simulation kernel): one warp simulates the trace
+// with one partition per lane slot, reproducing the reference's event order,
+// placements and timings bit for bit. Report formatting (CSV/JSON) stays on the host.
 #pragma once
 
 #include <algorithm>
