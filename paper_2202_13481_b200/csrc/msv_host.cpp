@@ -312,6 +312,11 @@ struct msv_grid {
     int n_cells = 0;
     std::vector<DevScen> h_scen;  // pointers into the wave buffers
     cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+    // Many-profile grids (more profile cells than the kernels' shared table): one sub-grid
+    // per profile group; this grid only dispatches and scatters.
+    std::vector<std::unique_ptr<msv_grid>> parts;
+    std::vector<std::vector<int64_t>> part_idx;
+    std::vector<int64_t> use_off;
     float t_total = 0, t_trace = 0, t_sim = 0, t_tail = 0;
     int64_t queries = -1;
     std::vector<int64_t> host_n;  // replay: trace lengths
@@ -1043,6 +1048,35 @@ int grid_results(msv_grid* g, msv_result* res, msv_usage* usage, msv_record* rec
 // ---------------------------------------------------------------------------
 // C ABI
 // ---------------------------------------------------------------------------
+namespace {
+
+// The kernels stage a grid's profile cells in shared memory (<= kMaxSmemCells). A call
+// whose scenarios use more distinct profile cells than that runs as several grids, one per
+// group of profiles that fits (the reference has no such limit). Returns false when one
+// grid suffices (or a handle is invalid: the single-grid path reports the error).
+bool profile_groups(const msv_ctx* ctx, const msv_scenario* sc, int64_t n, std::vector<std::vector<int64_t>>* groups) {
+    std::map<int32_t, int> group_of;
+    std::vector<int> cells;  // per group
+    int64_t total = 0;
+    for (int64_t i = 0; i < n; ++i) {
+        const int32_t pf = sc[i].profile;
+        if (pf < 0 || pf >= (int32_t)ctx->profiles.size()) return false;
+        if (group_of.count(pf)) continue;
+        const int c = (int)ctx->profiles[pf].lat.size();
+        if (c > msv::kMaxSmemCells) return false;
+        total += c;
+        if (cells.empty() || cells.back() + c > msv::kMaxSmemCells) cells.push_back(0);
+        cells.back() += c;
+        group_of[pf] = (int)cells.size() - 1;
+    }
+    if (total <= msv::kMaxSmemCells) return false;
+    groups->assign(cells.size(), {});
+    for (int64_t i = 0; i < n; ++i) (*groups)[group_of[sc[i].profile]].push_back(i);
+    return true;
+}
+
+}  // namespace
+
 extern "C" {
 
 const char* msv_last_error(void) { return g_err.c_str(); }
@@ -1254,19 +1288,74 @@ int msv_grid_create(msv_ctx* ctx, const msv_scenario* scenarios, int64_t n, cons
                     msv_grid** out) {
     if (!ctx || !out || (n > 0 && !scenarios)) return fail(MSV_PARAM, "null argument");
     SetDevice sd(ctx->device);
-    return grid_build(ctx, scenarios, n, tail_p, n_tails, nullptr, nullptr, nullptr, false, out);
+    std::vector<std::vector<int64_t>> groups;
+    if (!profile_groups(ctx, scenarios, n, &groups))
+        return grid_build(ctx, scenarios, n, tail_p, n_tails, nullptr, nullptr, nullptr, false, out);
+    std::unique_ptr<msv_grid> top(new msv_grid);
+    top->ctx = ctx;
+    top->n = n;
+    top->tail_p.assign(tail_p, tail_p + std::max(n_tails, 0));
+    top->use_off.assign(n + 1, 0);
+    for (int64_t i = 0; i < n; ++i) {  // validate first: errors name the caller's index
+        int32_t P = 0;
+        const int rc = validate_scenario(ctx, scenarios[i], true, &P);
+        if (rc) {
+            g_err = "scenario " + std::to_string(i) + ": " + g_err;
+            return rc;
+        }
+        top->use_off[i + 1] = top->use_off[i] + P;
+    }
+    top->usage_total = top->use_off[n];
+    for (std::vector<int64_t>& grp : groups) {
+        std::vector<msv_scenario> sub;
+        for (int64_t i : grp) sub.push_back(scenarios[i]);
+        msv_grid* g = nullptr;
+        const int rc = grid_build(ctx, sub.data(), (int64_t)sub.size(), tail_p, n_tails, nullptr, nullptr, nullptr,
+                                  false, &g);
+        if (rc) return rc;
+        top->parts.emplace_back(g);
+        top->part_idx.push_back(std::move(grp));
+    }
+    for (cudaEvent_t& e : top->ev) MSV_CUDA_TRY(cudaEventCreate(&e));
+    *out = top.release();
+    return MSV_OK;
 }
 
 int msv_grid_launch(msv_grid* grid) {
     if (!grid) return fail(MSV_PARAM, "null grid");
     SetDevice sd(grid->ctx->device);
-    return grid_launch(grid);
+    if (grid->parts.empty()) return grid_launch(grid);
+    MSV_CUDA_TRY(cudaEventRecord(grid->ev[0], grid->ctx->stream));
+    for (std::unique_ptr<msv_grid>& part : grid->parts) {
+        part->usage = grid->usage;
+        part->overlap = grid->overlap;
+        const int rc = grid_launch(part.get());
+        if (rc) return rc;
+    }
+    MSV_CUDA_TRY(cudaEventRecord(grid->ev[3], grid->ctx->stream));
+    grid->t_total = -2;  // only the total is defined
+    return MSV_OK;
 }
 
 int msv_grid_results(msv_grid* grid, msv_result* results, msv_usage* usage) {
     if (!grid || (grid->n > 0 && !results)) return fail(MSV_PARAM, "null argument");
     SetDevice sd(grid->ctx->device);
-    return grid_results(grid, results, usage, nullptr, nullptr);
+    if (grid->parts.empty()) return grid_results(grid, results, usage, nullptr, nullptr);
+    for (size_t k = 0; k < grid->parts.size(); ++k) {
+        msv_grid* part = grid->parts[k].get();
+        const std::vector<int64_t>& idx = grid->part_idx[k];
+        std::vector<msv_result> sub(idx.size());
+        std::vector<msv_usage> sub_use(std::max<int64_t>(part->usage_total, 1));
+        const int rc = grid_results(part, sub.data(), usage ? sub_use.data() : nullptr, nullptr, nullptr);
+        if (rc) return rc;
+        int64_t u = 0;
+        for (size_t j = 0; j < idx.size(); ++j) {
+            results[idx[j]] = sub[j];
+            if (usage)
+                for (int64_t q = grid->use_off[idx[j]]; q < grid->use_off[idx[j] + 1]; ++q) usage[q] = sub_use[u++];
+        }
+    }
+    return MSV_OK;
 }
 
 int msv_grid_destroy(msv_grid* grid) {
@@ -1313,6 +1402,15 @@ int msv_grid_set_overlap(msv_grid* g, int on) {
 int64_t msv_grid_queries(msv_grid* g) {
     if (!g) return -1;
     SetDevice sd(g->ctx->device);
+    if (!g->parts.empty()) {
+        int64_t t = 0;
+        for (std::unique_ptr<msv_grid>& part : g->parts) {
+            const int64_t q = msv_grid_queries(part.get());
+            if (q < 0) return -1;
+            t += q;
+        }
+        return t;
+    }
     if (cudaStreamSynchronize(g->ctx->stream) != cudaSuccess) return -1;
     std::vector<int64_t> nq(g->n);
     if (g->n && cudaMemcpy(nq.data(), g->B->d_nq.p, g->n * 8, cudaMemcpyDeviceToHost) != cudaSuccess) return -1;
@@ -1357,31 +1455,6 @@ int msv_transfer_bytes(msv_ctx* ctx, int64_t* h2d, int64_t* d2h) {
 }  // extern "C"
 
 namespace {
-
-// The kernels stage a grid's profile cells in shared memory (<= kMaxSmemCells). A call
-// whose scenarios use more distinct profile cells than that runs as several grids, one per
-// group of profiles that fits (the reference has no such limit). Returns false when one
-// grid suffices (or a handle is invalid: the single-grid path reports the error).
-bool profile_groups(const msv_ctx* ctx, const msv_scenario* sc, int64_t n, std::vector<std::vector<int64_t>>* groups) {
-    std::map<int32_t, int> group_of;
-    std::vector<int> cells;  // per group
-    int64_t total = 0;
-    for (int64_t i = 0; i < n; ++i) {
-        const int32_t pf = sc[i].profile;
-        if (pf < 0 || pf >= (int32_t)ctx->profiles.size()) return false;
-        if (group_of.count(pf)) continue;
-        const int c = (int)ctx->profiles[pf].lat.size();
-        if (c > msv::kMaxSmemCells) return false;
-        total += c;
-        if (cells.empty() || cells.back() + c > msv::kMaxSmemCells) cells.push_back(0);
-        cells.back() += c;
-        group_of[pf] = (int)cells.size() - 1;
-    }
-    if (total <= msv::kMaxSmemCells) return false;
-    groups->assign(cells.size(), {});
-    for (int64_t i = 0; i < n; ++i) (*groups)[group_of[sc[i].profile]].push_back(i);
-    return true;
-}
 
 int run_grid_core(msv_ctx* ctx, const msv_scenario* scenarios, int64_t n, const double* tail_p, int n_tails,
                   msv_result* results, msv_usage* usage);

@@ -68,10 +68,10 @@ def _random_plan(rng, sizes):
     return PartitionPlan(gpus, 7, per)
 
 
-def test_fuzz_grids(eng, ref):
-    rng = np.random.default_rng(20260)
+def _fuzz_specs(seed, n):
+    rng = np.random.default_rng(seed)
     specs = []
-    for i in range(400):
+    for i in range(n):
         table = _random_table(rng, i)
         b = table.b_max
         dist = lognormal_batch_pdf(float(rng.uniform(0.0, 2.0)), float(rng.uniform(0.3, 1.5)), b) \
@@ -87,10 +87,40 @@ def test_fuzz_grids(eng, ref):
         specs.append(GridSpec(plan, table, dist, SlaConfig(sla_ms, alpha, beta), rate, queries / rate * 1000.0,
                               int(rng.integers(1, 1 << 40)), "elsa" if rng.random() < 0.7 else "fifs",
                               float(rng.choice([0.0, 0.1, 0.5]))))
+    return specs
+
+
+def test_fuzz_grids(eng, ref):
+    specs = _fuzz_specs(20260, 400)
     got, want = eng.run_grid(specs, (0.5, 0.95, 0.99)), ref.run_grid(specs, (0.5, 0.95, 0.99))
     for k in ("total", "violations", "measured", "measured_violations", "horizon_ms", "placement_hash", "tail",
               "status"):
         assert _same(got[k], want[k]), k
+
+
+def test_fuzz_device_grid_many_profiles(eng, ref):
+    """A device-resident grid whose profiles exceed one shared table (1,024 cells) is held as
+    several sub-grids: launches, results, usage, queries and timing still cover the whole grid
+    in the caller's order."""
+    specs = _fuzz_specs(4242, 120)
+    assert sum(s.table.latency.size for s in {id(s.table): s for s in specs}.values()) > 1024
+    want = ref.run_grid(specs, (0.5, 0.99))
+    use = eng.run_grid(specs, (0.5, 0.99), usage=True)["usage"]  # the split msv_run_grid path
+    g = eng.grid(specs, (0.5, 0.99))
+    for _ in range(2):
+        g.launch()
+        got = g.results(usage=True)
+        for k in ("total", "violations", "measured", "measured_violations", "horizon_ms", "placement_hash", "tail",
+                  "status"):
+            assert _same(got[k], want[k]), k
+        for k in use:
+            assert _same(got["usage"][k], use[k]), k
+    assert g.queries() == int(want["total"].sum())
+    assert g.timing()["total_ms"] > 0
+    g.set_usage(False)
+    g.launch()
+    assert _same(g.results()["tail"], want["tail"])
+    g.close()
 
 
 KEYS = ("partition", "kind", "start_ms", "finish_ms", "busy_ms", "weighted_busy_ms", "queries", "total",
