@@ -64,7 +64,7 @@ def _stale(target: Path, deps: list[Path]) -> bool:
 
 def build_libmsv(force: bool = False, verbose: bool = False) -> Path:
     BUILD.mkdir(exist_ok=True)
-    headers = sorted(CSRC.glob("*.h")) + sorted((ROOT / "include").rglob("*.h*"))
+    headers = sorted(CSRC.glob("*.h")) + sorted(CSRC.glob("*.cuh")) + sorted((ROOT / "include").rglob("*.h*"))
     objs: list[Path] = []
     log: list[str] = []
     for src in sorted(CSRC.glob("*.cu")):

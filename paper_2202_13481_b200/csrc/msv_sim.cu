@@ -145,6 +145,9 @@ __global__ void __launch_bounds__(kSimWarpsPerBlock * 32, (SegCfg<W, S>::min_blo
                 g_arr = d->arrival;
                 g_bat = d->batch;
                 samples = d->samples;
+                __builtin_assume(__isGlobal(g_arr));
+                __builtin_assume(__isGlobal(g_bat));
+                __builtin_assume(__isGlobal(samples));
                 sla = d->sla;
                 warmup = d->warmup_ms;
                 alpha = d->alpha;

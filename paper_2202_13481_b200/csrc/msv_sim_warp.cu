@@ -107,6 +107,13 @@ __global__ void __launch_bounds__(kSimWarpsPerBlock * 32, WarpCfg<S>::min_blocks
         const bool check_wait = FULL && p.any_check_wait && (d.flags & MSV_FLAG_CHECK_WAIT);
         const int bmax = d.b_max;
         const uint64_t* route_mask = d.route_mask;
+        // global-space accesses (LDG/STG) instead of generic ones on the per-query paths
+        __builtin_assume(__isGlobal(g_arr));
+        __builtin_assume(__isGlobal(g_bat));
+        __builtin_assume(__isGlobal(g_next));
+        __builtin_assume(__isGlobal(samples));
+        if (REC) __builtin_assume(__isGlobal(rec));
+        if (FULL && route_mask) __builtin_assume(__isGlobal(route_mask));
 
         // ---- lane slots ----
         bool act[S], busy[S];
