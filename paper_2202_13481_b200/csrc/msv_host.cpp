@@ -119,8 +119,8 @@ int set_error(int code, const char* what) { return fail(code, what ? what : "");
 
 // Device buffers of one grid launch sequence.
 struct GridBufs {
-    DevBuf d_scen, d_out, d_tjobs, d_tailjobs, d_tails, d_p, d_usage, d_nq, d_tovf, d_parts, d_masks, d_work,
-        d_counter;
+    DevBuf d_scen, d_out, d_tjobs, d_tgroups, d_tailjobs, d_tails, d_p, d_usage, d_nq, d_tovf, d_parts, d_masks,
+        d_work, d_counter;
     DevBuf d_arr, d_bat, d_next, d_samples, d_rec, d_glat, d_gutil;
 };
 
@@ -294,6 +294,7 @@ struct msv_grid {
     // chunk's trace / tail jobs are the contiguous range [l0, l1).
     struct Chunk {
         int64_t l0 = 0, l1 = 0;
+        int64_t g0 = 0, g1 = 0;  // K1 trace groups [g0, g1) in d_tgroups
         std::vector<std::pair<ClassKey, std::vector<int32_t>>> classes;
         std::vector<int64_t> work_off;  // offset of each class's work list in d_work
     };
@@ -303,6 +304,7 @@ struct msv_grid {
         std::vector<Chunk> chunks;
     };
     std::vector<int32_t> launch_order;  // scenario index of each launch slot
+    std::vector<msv::TraceGroup> tgroups;  // K1 groups (launch-slot ranges), chunk by chunk
     bool overlap = true;                // chunks on concurrent streams
     bool usage = true;                  // accumulate per-partition usage (msv_grid_set_usage)
     std::vector<Wave> waves;
@@ -560,6 +562,14 @@ int grid_build(msv_ctx* ctx, const msv_scenario* sc, int64_t n, const double* ta
             cost[i] = (s.rate_qps * s.duration_ms / 1000.0) * (1.0 + 4.0 * rho * rho);
         }
     }
+    // MSV_TRACE_GROUP=0: one K1 warp per trace (no shared random streams), for A/B runs
+    static const bool group_traces = !(getenv("MSV_TRACE_GROUP") && atoi(getenv("MSV_TRACE_GROUP")) == 0);
+    static const int group_max = getenv("MSV_TRACE_GROUP_MAX")
+                                     ? std::max(1, std::min(msv::kTraceGroupMax, atoi(getenv("MSV_TRACE_GROUP_MAX"))))
+                                     : msv::kTraceGroupMax;
+    static const int group_first = getenv("MSV_TRACE_GROUP_FIRST")
+                                       ? std::max(1, std::min(msv::kTraceGroupMax, atoi(getenv("MSV_TRACE_GROUP_FIRST"))))
+                                       : 2;
     int64_t qoff_global = 0;
     for (msv_grid::Wave& w : g->waves) {
         w.q0 = qoff_global;
@@ -615,28 +625,67 @@ int grid_build(msv_ctx* ctx, const msv_scenario* sc, int64_t n, const double* ta
         const int n_chunks = (int)share.size();
         double share_sum = 0.0;
         for (double v : share) share_sum += v;
-        // proportional interleave in cost order: each scenario goes to the chunk furthest
+        // K1 groups: scenarios with the same seed and batch distribution draw the same
+        // random stream (sample_trace's draws do not depend on the rate), so one K1 warp
+        // generates up to kTraceGroupMax of their traces. Groups stay whole inside a chunk
+        // and are dealt in cost order of their first member. A group's warp is latency-
+        // bound (fewer, longer warps), so grouping pays where K1 overlaps other chunks'
+        // simulation: chunked waves only, and the first chunk (which nothing overlaps) in
+        // pairs (C2 bench grid, B200: one warp per trace 8.42, groups of <= 16 8.79, first
+        // chunk in pairs 8.95 G queries/s).
+        std::vector<std::vector<int32_t>> groups;
+        {
+            std::map<std::pair<uint64_t, int32_t>, size_t> open;
+            for (int32_t i : ord) {
+                const double rpm = sc[i].rate_qps / 1000.0;  // the grouped quotient needs a normal range
+                if (!group_traces || !g->generated || n_chunks < 2 || !(rpm >= 0x1p-600 && rpm <= 0x1p600)) {
+                    groups.push_back({i});
+                    continue;
+                }
+                const std::pair<uint64_t, int32_t> key(sc[i].seed, sc[i].dist);
+                auto it = open.find(key);
+                if (it == open.end() || groups[it->second].size() >= (size_t)group_max) {
+                    open[key] = groups.size();
+                    groups.push_back({});
+                    it = open.find(key);
+                }
+                groups[it->second].push_back(i);
+            }
+        }
+        // proportional interleave in cost order: each group goes to the chunk furthest
         // below its share (equal shares: round robin)
         std::vector<std::vector<int32_t>> members(n_chunks);
-        for (size_t j = 0; j < ord.size(); ++j) {
+        std::vector<std::vector<std::pair<int32_t, int32_t>>> cgroups(n_chunks);  // (offset, count) in members
+        int64_t dealt = 0;
+        for (const std::vector<int32_t>& grp : groups) {
+            dealt += (int64_t)grp.size();
             int best = 0;
             double best_def = -1e300;
             for (int c = 0; c < n_chunks; ++c) {
-                const double def = share[c] / share_sum * (double)(j + 1) - (double)members[c].size();
+                const double def = share[c] / share_sum * (double)dealt - (double)members[c].size();
                 if (def > best_def + 1e-12) {
                     best_def = def;
                     best = c;
                 }
             }
-            members[best].push_back(ord[j]);
+            cgroups[best].emplace_back((int32_t)members[best].size(), (int32_t)grp.size());
+            members[best].insert(members[best].end(), grp.begin(), grp.end());
         }
         for (int c = 0; c < n_chunks; ++c) {
             msv_grid::Chunk ch;
             ch.l0 = (int64_t)g->launch_order.size();
             g->launch_order.insert(g->launch_order.end(), members[c].begin(), members[c].end());
             ch.l1 = (int64_t)g->launch_order.size();
+            ch.g0 = (int64_t)g->tgroups.size();
+            const int cap_c = (c == 0 && n_chunks > 1) ? group_first : group_max;
+            for (const auto& og : cgroups[c])
+                for (int32_t o = 0; o < og.second; o += cap_c)
+                    g->tgroups.push_back({(int32_t)(ch.l0 + og.first + o), std::min(cap_c, og.second - o)});
+            ch.g1 = (int64_t)g->tgroups.size();
+            std::vector<int32_t> by_cost = members[c];  // kernel classes keep longest-first order
+            std::stable_sort(by_cost.begin(), by_cost.end(), [&](int32_t a, int32_t b) { return cost[a] > cost[b]; });
             std::map<ClassKey, std::vector<int32_t>> cls;
-            for (int32_t i : members[c]) cls[class_of(g->P[i], sc[i].scheduler, seg_w, overloaded[i])].push_back(i);  // cost order kept
+            for (int32_t i : by_cost) cls[class_of(g->P[i], sc[i].scheduler, seg_w, overloaded[i])].push_back(i);
             for (auto& kv : cls) ch.classes.emplace_back(kv.first, std::move(kv.second));
             w.chunks.push_back(std::move(ch));
         }
@@ -796,6 +845,11 @@ int grid_build(msv_ctx* ctx, const msv_scenario* sc, int64_t n, const double* ta
         MSV_CUDA_TRY(cudaMemcpy(g->B->d_tailjobs.p, lj_l.data(), n * sizeof(msv::TailJob), cudaMemcpyHostToDevice));
         MSV_CUDA_TRY(cudaMemset(g->B->d_tovf.p, 0, n * 4));
     }
+    MSV_CUDA_TRY(g->B->d_tgroups.ensure(std::max<size_t>(g->tgroups.size(), 1) * sizeof(msv::TraceGroup)));
+    if (!g->tgroups.empty())
+        MSV_CUDA_TRY(cudaMemcpy(g->B->d_tgroups.p, g->tgroups.data(), g->tgroups.size() * sizeof(msv::TraceGroup),
+                                cudaMemcpyHostToDevice));
+    ctx->h2d += (int64_t)(g->tgroups.size() * sizeof(msv::TraceGroup));
     pt.mark("descriptors");
     // Work lists of every (wave, chunk, class).
     std::vector<int32_t> work_h;
@@ -843,7 +897,12 @@ int launch_chunk(msv_grid* g, const msv_grid::Chunk& ch, int counter_base, cudaS
     msv_ctx* ctx = g->ctx;
     const int64_t nl = ch.l1 - ch.l0;
     if (g->generated && nl > 0) {
-        MSV_CUDA_TRY(msv::launch_trace_gen(g->B->d_tjobs.as<msv::TraceJob>() + ch.l0, (int)nl, ctx->log1p, st));
+        if (ch.g1 - ch.g0 == nl)  // no shared streams in this chunk: one warp per trace
+            MSV_CUDA_TRY(msv::launch_trace_gen(g->B->d_tjobs.as<msv::TraceJob>() + ch.l0, (int)nl, ctx->log1p, st));
+        else
+            MSV_CUDA_TRY(msv::launch_trace_groups(g->B->d_tjobs.as<msv::TraceJob>(),
+                                                  g->B->d_tgroups.as<msv::TraceGroup>() + ch.g0, (int)(ch.g1 - ch.g0),
+                                                  ctx->log1p, st));
         debug_sync(st, "trace_gen");
         ctx->launches += 1;
     }

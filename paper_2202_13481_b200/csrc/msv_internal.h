@@ -18,6 +18,8 @@ constexpr int kQCap = 8;
 constexpr int kMaxSmemCells = 1024;
 constexpr int kSimWarpsPerBlock = 4;
 constexpr int kTraceWarpsPerBlock = 4;
+constexpr int kTraceGroupMax = 16;    // traces sharing one random stream per K1 warp
+constexpr int kTraceAccStride = 34;   // padded row (double2 reads by 16 lanes: 2 wavefronts)
 constexpr int kTailThreads = 512;
 constexpr int kTailSmemCap = 2048;  // values gathered for the final in-smem select
 // Guide table of BatchDistribution::sample: u in [j/G, (j+1)/G) starts its lower_bound at guide[j].
@@ -166,6 +168,13 @@ struct ParisParams {
 
 // Kernel launchers (msv_kernels.cu). Return cudaGetLastError().
 cudaError_t launch_paris(const ParisParams& p, cudaStream_t stream);
+// K1 over groups: group g covers jobs [first, first + count) (count <= kTraceGroupMax, one
+// seed and distribution per group).
+struct TraceGroup {
+    int32_t first, count;
+};
+cudaError_t launch_trace_groups(const TraceJob* d_jobs, const TraceGroup* d_groups, int n_groups, int log1p_variant,
+                                cudaStream_t stream);
 cudaError_t launch_trace_gen(const TraceJob* d_jobs, int n_jobs, int log1p_variant,
                              cudaStream_t stream);
 // Persistent simulation kernel for P <= W*S (W lanes per scenario, S slots per lane).
