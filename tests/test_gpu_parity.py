@@ -443,3 +443,46 @@ def test_grid_edge_cases(eng, ref):
     assert r.returncode == 0, r.stderr[-2000:]
     want = np.concatenate([base[0].view(np.float64), base[1].ravel(), base[2].astype(np.float64), base[3]])
     assert np.array_equal(np.load(out).view(np.uint64), want.view(np.uint64))
+
+
+def _shared_stream_grid():
+    """Scenarios sharing seeds (and the batch distribution) at different rates, durations
+    and trace lengths: K1 generates each seed's traces from one random stream."""
+    m = W.model("resnet50")
+    plans = [W.paris(m, 1), homogeneous_plan(1, 7, 1, 7), homogeneous_plan(7, 7, 1, 7)]
+    specs = []
+    for s in range(1, 61):
+        for j, load in enumerate((0.2, 0.5, 0.8, 0.95, 1.3)):
+            p = plans[(s + j) % len(plans)]
+            rate = load * W.capacity_qps(m, p)
+            queries = (300, 1200, 2500, 700, 40)[(s * 7 + j) % 5]
+            specs.append(GridSpec(p, m.table, m.dist, m.sla, rate, queries / rate * 1000.0, s))
+    return specs
+
+
+def _shared_stream_results():
+    r = Engine(0).run_grid(_shared_stream_grid(), (0.5, 0.99))
+    return r["placement_hash"], r["tail"], r["total"]
+
+
+def test_shared_random_streams_match_reference(ref):
+    """Chunked waves generate the traces of one seed in one K1 warp (groups of up to 16,
+    pairs in the first chunk); with forced chunks, any group cap and shortened trace
+    capacities (overflow re-runs) every result equals the reference's."""
+    import os
+    import sys
+    specs = _shared_stream_grid()
+    want = ref.run_grid(specs, (0.5, 0.99))
+    code = ("import sys, numpy as np; sys.path.insert(0, %r); from tests.test_gpu_parity import _shared_stream_results; "
+            "h, t, n = _shared_stream_results(); np.save(sys.argv[1], np.concatenate([h.view(np.float64), t.ravel(), "
+            "n.astype(np.float64)]))" % str(ROOT))
+    ref_arr = np.concatenate([want["placement_hash"].view(np.float64), want["tail"].ravel(),
+                              want["total"].astype(np.float64)])
+    for extra in ({"MSV_CHUNK_SPLIT": "2,1,1"}, {"MSV_CHUNK_SPLIT": "1,1", "MSV_TRACE_GROUP_FIRST": "16"},
+                  {"MSV_CHUNK_SPLIT": "1,1", "MSV_TRACE_GROUP_MAX": "3", "MSV_TEST_SHORT_CAP": "1"},
+                  {"MSV_CHUNK_SPLIT": "1"}):
+        out = Path(f"/tmp/msv_groups_{os.getpid()}.npy")
+        r = subprocess.run([sys.executable, "-c", code, str(out)], capture_output=True, text=True,
+                           env=dict(os.environ, **extra), timeout=600)
+        assert r.returncode == 0, r.stderr[-2000:]
+        assert np.array_equal(np.load(out).view(np.uint64), ref_arr.view(np.uint64)), extra
