@@ -220,7 +220,10 @@ typedef struct msv_grid msv_grid;
 int msv_grid_create(msv_ctx* ctx, const msv_scenario* scenarios, int64_t n, const double* tail_p,
                     int n_tails, msv_grid** out);
 /* Runs trace generation, simulation and tail selection for the whole grid on the
- * context stream; no host synchronisation, no host<->device copies. */
+ * context stream; no host synchronisation, no host<->device copies. Back-to-back
+ * launches of one single-wave grid overlap (each chunk waits only for its own previous
+ * run); msv_event_record, or launching another grid in between, restores a full
+ * barrier. msv_grid_results returns the last launch's results. */
 int msv_grid_launch(msv_grid* grid);
 int msv_grid_results(msv_grid* grid, msv_result* results, msv_usage* usage);
 int msv_grid_destroy(msv_grid* grid);

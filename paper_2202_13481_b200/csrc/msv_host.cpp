@@ -136,6 +136,8 @@ struct msv_ctx {
     cudaStream_t aux[4] = {};    // chunk streams of overlapped grid launches
     cudaEvent_t aux_ev[4] = {};
     cudaEvent_t fork_ev = nullptr;
+    uint64_t grid_serial = 0;       // grids created on this context
+    uint64_t last_launch_grid = 0;  // serial of the grid launched last
     cudaStream_t cls[4] = {};    // extra class streams: a chunk's kernel classes run concurrently
     cudaEvent_t cls_ev[4] = {};
     cudaEvent_t cls_fork = nullptr;
@@ -303,6 +305,7 @@ struct msv_grid {
         int64_t q0 = 0, q1 = 0;  // trace slots [q0, q1)
         std::vector<Chunk> chunks;
     };
+    uint64_t serial = 0;                // per-context creation number
     std::vector<int32_t> launch_order;  // scenario index of each launch slot
     std::vector<msv::TraceGroup> tgroups;  // K1 groups (launch-slot ranges), chunk by chunk
     bool overlap = true;                // chunks on concurrent streams
@@ -463,6 +466,7 @@ int grid_build(msv_ctx* ctx, const msv_scenario* sc, int64_t n, const double* ta
     if (rc) return rc;
     pt.mark("tables");
     std::unique_ptr<msv_grid> g(new msv_grid);
+    g->serial = ++ctx->grid_serial;
     g->ctx = ctx;
     if (scratch) g->B = &ctx->scratch;
     g->generated = offsets == nullptr;
@@ -982,12 +986,27 @@ int grid_launch(msv_grid* g) {
     msv_ctx* ctx = g->ctx;
     cudaStream_t st = ctx->stream;
     int rc;
-    // counters are zeroed once per launch; each (chunk, class) owns one
     MSV_CUDA_TRY(cudaEventRecord(g->ev[0], st));
-    MSV_CUDA_TRY(cudaMemsetAsync(g->B->d_counter.p, 0, kCounterSlots * sizeof(int32_t), st));
     size_t total_chunks = 0;
     for (const msv_grid::Wave& w : g->waves) total_chunks += w.chunks.size();
     const bool overlap = g->overlap && total_chunks > 1;
+    // Back-to-back launches of one single-wave grid are pipelined: chunk c only touches
+    // its own scenarios' buffer regions and always runs on aux stream c, so launch i+1's
+    // chunk c needs only launch i's chunk c to be done (stream order) — no fork, and its
+    // trace generation overlaps the other chunks' simulation of launch i. Any other grid
+    // launched in between (it may share the scratch buffers) restores the full fork.
+    static const bool pipeline_env = !(getenv("MSV_PIPELINE") && atoi(getenv("MSV_PIPELINE")) == 0);
+    const bool pipelined = pipeline_env && overlap && g->waves.size() == 1 && ctx->last_launch_grid == g->serial;
+    ctx->last_launch_grid = g->serial;
+    // work counters: each (chunk, class) owns one slot (mod kCounterSlots), zeroed on the
+    // stream that uses it right before the chunk
+    auto zero_counters = [&](int base, size_t n, cudaStream_t s) -> int {
+        const int s0 = base % kCounterSlots;
+        const size_t first = std::min(n, (size_t)(kCounterSlots - s0));
+        MSV_CUDA_TRY(cudaMemsetAsync(g->B->d_counter.as<int32_t>() + s0, 0, first * sizeof(int32_t), s));
+        if (n > first) MSV_CUDA_TRY(cudaMemsetAsync(g->B->d_counter.p, 0, (n - first) * sizeof(int32_t), s));
+        return MSV_OK;
+    };
     if (overlap) {
         for (int a = 0; a < kAuxStreams; ++a) {
             if (!ctx->aux[a]) MSV_CUDA_TRY(cudaStreamCreateWithFlags(&ctx->aux[a], cudaStreamNonBlocking));
@@ -1001,10 +1020,11 @@ int grid_launch(msv_grid* g) {
         const msv_grid::Wave& w = g->waves[wi];
         if (overlap) {
             // fork: every aux stream starts after everything queued on the main stream
-            MSV_CUDA_TRY(cudaEventRecord(ctx->fork_ev, st));
+            if (!pipelined) MSV_CUDA_TRY(cudaEventRecord(ctx->fork_ev, st));
             for (size_t c = 0; c < w.chunks.size(); ++c) {
                 cudaStream_t sc = ctx->aux[c % kAuxStreams];
-                MSV_CUDA_TRY(cudaStreamWaitEvent(sc, ctx->fork_ev, 0));
+                if (!pipelined) MSV_CUDA_TRY(cudaStreamWaitEvent(sc, ctx->fork_ev, 0));
+                if ((rc = zero_counters(counter_base, w.chunks[c].classes.size(), sc))) return rc;
                 if ((rc = launch_chunk(g, w.chunks[c], counter_base, sc, nullptr, nullptr))) return rc;
                 counter_base += (int)w.chunks[c].classes.size();
             }
@@ -1017,6 +1037,7 @@ int grid_launch(msv_grid* g) {
             for (const msv_grid::Chunk& ch : w.chunks) {
                 cudaEvent_t e0 = g->ev[0], e1 = g->ev[1], e2 = g->ev[2], e3 = g->ev[3];
                 if (wi > 0 || &ch != &w.chunks.front()) MSV_CUDA_TRY(cudaEventRecord(e0, st));
+                if ((rc = zero_counters(counter_base, ch.classes.size(), st))) return rc;
                 if ((rc = launch_chunk(g, ch, counter_base, st, e1, e2))) return rc;
                 counter_base += (int)ch.classes.size();
                 MSV_CUDA_TRY(cudaEventRecord(e3, st));
@@ -1492,6 +1513,7 @@ int msv_event_record(msv_ctx* ctx, int slot) {
     SetDevice sd(ctx->device);
     if (!ctx->ev[slot]) MSV_CUDA_TRY(cudaEventCreate(&ctx->ev[slot]));
     MSV_CUDA_TRY(cudaEventRecord(ctx->ev[slot], ctx->stream));
+    ctx->last_launch_grid = 0;  // the next launch forks from the main stream: it starts after this event
     return MSV_OK;
 }
 
