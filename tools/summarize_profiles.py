@@ -5,11 +5,13 @@
         --launches gpurun_out/r01/launches.csv --bench gpurun_out/r01/bench.log \
         --reference gpurun_out/r01/bench_ref.log
 
-Writes <kernel>_raw.csv (ncu --page raw), sim_opcodes.csv (SASS opcode histogram of
-K2 from the source page), launches_bench.csv and summary.json with per-launch figures
-(duration, warp instructions per query, issue utilisation, DRAM bytes per launch and
-per query) and each kernel's share of the launch list. Per-launch times under ncu are
-serialised and cold-cache: the shares, not the absolutes, compare with bench.py.
+The first report holds every kernel of ONE bench step (all chunks); each kernel's
+launches are summed (time, warp instructions, DRAM bytes) and divided by the step's
+simulated queries. Writes <kernel>_raw.csv (ncu --page raw, one row per launch),
+sim_opcodes.csv (SASS opcode histogram of one K2 launch, from a report holding only
+that launch: --opcodes), launches_bench.csv and summary.json, plus each kernel's share
+of the launch list. Times under ncu are serialised and cold-cache: the shares, not the
+absolutes, compare with bench.py.
 """
 from __future__ import annotations
 
@@ -24,7 +26,8 @@ import subprocess
 from pathlib import Path
 
 ROOT = Path(__file__).resolve().parents[1]
-SHORT = {"trace_gen_kernel": "K1 trace_gen_kernel", "sim_warp_kernel": "K2 sim_warp_kernel",
+SHORT = {"trace_gen_kernel": "K1 trace_gen_kernel", "trace_group_kernel": "K1 trace_group_kernel",
+         "sim_warp_kernel": "K2 sim_warp_kernel",
          "sim_kernel": "K2 sim_kernel (segmented)", "tail_kernel": "K3 tail_kernel", "paris_kernel": "K4 paris_kernel"}
 METRICS = {
     "duration_ms": "gpu__time_duration.sum",
@@ -59,8 +62,9 @@ def main():
     ap.add_argument("--launches", type=Path)
     ap.add_argument("--bench", type=Path)
     ap.add_argument("--reference", type=Path)
-    ap.add_argument("--queries-per-launch", type=float, default=None,
-                    help="simulated queries one K1/K2 launch covers (default: from the bench line)")
+    ap.add_argument("--opcodes", type=Path, default=None, help="report holding one K2 launch (source page)")
+    ap.add_argument("--queries-per-step", type=float, default=None,
+                    help="simulated queries of the captured step (default: from the bench line)")
     a = ap.parse_args()
     out = ROOT / "profiles" / a.round
     out.mkdir(parents=True, exist_ok=True)
@@ -74,62 +78,73 @@ def main():
         lines = [l for l in a.reference.read_text().splitlines() if l.startswith("{")]
         if lines:
             (out / "bench_reference_line.json").write_text(json.dumps(json.loads(lines[-1]), indent=1) + "\n")
-    qpl = a.queries_per_launch
-    if qpl is None and bench:
+    qps = a.queries_per_step
+    if qps is None and bench:
         cfg = bench["config"]
-        launches_per_step = bench["gpu_launches"] / bench["steps"]
-        qpl = cfg["scenarios_per_gpu"] * cfg["queries_per_scenario"] / (launches_per_step / 3.0)
-    kernels = {}
-    for rep in a.reps:
-        rows = ncu_csv(rep, "--page", "raw")
-        head, units = rows[0], rows[1]
-        for r in rows[2:]:
-            name = short(r[head.index("Kernel Name")])
-            if name in kernels:
+        qps = cfg["scenarios_per_gpu"] * cfg["queries_per_scenario"]
+    ADD = ("duration_ms", "warp_instructions", "dram_read", "dram_write")
+    kernels, raw = {}, collections.defaultdict(list)
+    rows = ncu_csv(a.reps[0], "--page", "raw")
+    head, units = rows[0], rows[1]
+    for r in rows[2:]:
+        name = short(r[head.index("Kernel Name")])
+        vals = {}
+        for key, m in METRICS.items():
+            if m not in head:
                 continue
-            k = {"kernel": r[head.index("Kernel Name")]}
-            for key, m in METRICS.items():
-                if m not in head:
-                    continue
-                i = head.index(m)
+            i = head.index(m)
+            try:
+                v = float(r[i].replace(",", ""))
+            except ValueError:
+                continue
+            if key.startswith("dram"):
+                v *= UNIT.get(units[i], 1)
+            elif key == "duration_ms":
+                v *= UNIT.get(units[i], 1) if units[i] != "ms" else 1
+            vals[key] = v
+        raw[name].append(r)
+        k = kernels.setdefault(name, {"kernel": r[head.index("Kernel Name")], "launches": 0,
+                                      **{x: 0.0 for x in ADD}, "_w": {}})
+        k["launches"] += 1
+        for x in ADD:
+            k[x] += vals.get(x, 0.0)
+        # duration-weighted means of the rates, instruction-weighted lane occupancy
+        for x, wkey in (("issue_active_pct", "duration_ms"), ("warps_active_per_sm", "duration_ms"),
+                        ("threads_per_instruction", "warp_instructions")):
+            if x in vals:
+                acc = k["_w"].setdefault(x, [0.0, 0.0])
+                acc[0] += vals[x] * vals.get(wkey, 0.0)
+                acc[1] += vals.get(wkey, 0.0)
+        for x in ("registers", "grid"):
+            if x in vals:
+                k.setdefault(x + "_per_launch", []).append(vals[x])
+    for name, k in kernels.items():
+        for x, (num, den) in k.pop("_w").items():
+            k[x] = num / den if den else None
+        k["traffic_bytes_per_step"] = k["dram_read"] + k["dram_write"]
+        if qps:
+            samples = 0.9 if name.startswith("K3") else 1.0  # K3 reads the measured (post-warm-up) latencies
+            k["warp_instructions_per_query"] = k["warp_instructions"] / qps
+            k["traffic_bytes_per_query"] = k["traffic_bytes_per_step"] / (qps * samples)
+        with open(out / f"{name.split()[0].lower()}_{name.split()[1]}_raw.csv", "w", newline="") as f:
+            csv.writer(f).writerows([head, units, *raw[name]])
+    if a.opcodes and a.opcodes.exists():
+        src = ncu_csv(a.opcodes, "--page", "source", "--print-source", "cuda,sass")
+        ops, tot = collections.Counter(), 0
+        for r in src:
+            if len(r) > 8 and r[0] == "" and r[2].startswith("0x"):
                 try:
-                    v = float(r[i].replace(",", ""))
+                    n = int(r[7])
                 except ValueError:
                     continue
-                if key.startswith("dram"):
-                    v *= UNIT.get(units[i], 1)
-                elif key == "duration_ms":
-                    v *= UNIT.get(units[i], 1) if units[i] != "ms" else 1
-                k[key] = v
-            if not k.get("warp_instructions", 0.0) == k.get("warp_instructions", 0.0):
-                continue  # an incomplete capture (NaN counters): take the kernel from another report
-            if "dram_read" in k and "dram_write" in k:
-                k["traffic_bytes_per_launch"] = k["dram_read"] + k["dram_write"]
-                if qpl:
-                    k["traffic_bytes_per_query"] = k["traffic_bytes_per_launch"] / (
-                        qpl * (0.9 if name.startswith("K3") else 1.0))
-            if qpl and "warp_instructions" in k:
-                k["warp_instructions_per_query"] = k["warp_instructions"] / qpl
-            kernels[name] = k
-            with open(out / f"{name.split()[0].lower()}_raw.csv", "w", newline="") as f:
-                csv.writer(f).writerows([head, units, r])
-        if any(short(r[head.index("Kernel Name")]).startswith("K2") for r in rows[2:]):
-            src = ncu_csv(rep, "--page", "source", "--print-source", "cuda,sass")
-            ops, tot = collections.Counter(), 0
-            for r in src:
-                if len(r) > 8 and r[0] == "" and r[2].startswith("0x"):
-                    try:
-                        n = int(r[7])
-                    except ValueError:
-                        continue
-                    s = re.sub(r"^@!?U?P\w+\s+", "", r[3].strip())
-                    ops[s.split()[0] if s else "?"] += n
-                    tot += n
-            with open(out / "sim_opcodes.csv", "w", newline="") as f:
-                w = csv.writer(f)
-                w.writerow(["opcode", "warp_instructions", "share", "per_query"])
-                for o, n in ops.most_common():
-                    w.writerow([o, n, round(n / tot, 5), round(n / qpl, 3) if qpl else ""])
+                t = re.sub(r"^@!?U?P\w+\s+", "", r[3].strip())
+                ops[t.split()[0] if t else "?"] += n
+                tot += n
+        with open(out / "sim_opcodes.csv", "w", newline="") as f:
+            w = csv.writer(f)
+            w.writerow(["opcode", "warp_instructions", "share"])
+            for o, n in ops.most_common():
+                w.writerow([o, n, round(n / tot, 5)])
     shares = {}
     if a.launches and a.launches.exists():
         shutil.copy(a.launches, out / "launches_bench.csv")
@@ -144,10 +159,11 @@ def main():
         shares = {k: {"launches": cnt[k], "total_ms": round(v / 1e6, 3), "share": round(v / s, 4)}
                   for k, v in tot.items()}
     summary = {
-        "note": "ncu --set full --clock-control none captures of `python bench.py --no-cpu-baseline --steps 1 "
-                "--warmup 3` (default grid: 10,240 scenarios x 1e5 queries, two chunks per step) on one B200; "
-                "per-launch figures. ncu times are serialised / cold-cache: compare shares, not absolutes.",
-        "queries_per_launch": qpl,
+        "note": "ncu --set full --clock-control none capture of every kernel of one step of `python bench.py "
+                "--no-cpu-baseline --steps 1 --warmup 3` (10,240 scenarios x 1e5 queries, four chunks) on one "
+                "B200; per kernel: its launches in the step summed, per-query figures over the step's queries. "
+                "ncu times are serialised / cold-cache: compare shares, not absolutes.",
+        "queries_per_step": qps,
         "issue_peak_warp_inst_per_s": "148 SMs x 4 schedulers x SM clock (1 warp-instruction / scheduler / clk)",
         "kernels": kernels,
         "launch_shares_bench": shares,
