@@ -16,4 +16,4 @@ ncu --set full --clock-control none --import-source on -k "$KR" --launch-skip $(
 # one K2 launch for the SASS opcode histogram (source page)
 ncu --set full --clock-control none --import-source on -k regex:sim_warp_kernel --launch-skip 12 --launch-count 1 \
     -o gpurun_out/r01/k2 python bench.py --no-cpu-baseline --steps 1 --warmup 3 > gpurun_out/r01/ncu_k2.log 2>&1
-tail -2 gpurun_out/r01/ncu_step.log gpurun_out/r01/ncu_k2.log
+tail -n 2 gpurun_out/r01/ncu_step.log gpurun_out/r01/ncu_k2.log
