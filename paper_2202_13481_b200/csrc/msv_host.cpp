@@ -121,8 +121,19 @@ int set_error(int code, const char* what) { return fail(code, what ? what : "");
 struct GridBufs {
     DevBuf d_scen, d_out, d_tjobs, d_tgroups, d_tailjobs, d_tails, d_p, d_usage, d_nq, d_tovf, d_parts, d_masks,
         d_work, d_counter;
-    DevBuf d_arr, d_bat, d_next, d_samples, d_rec, d_glat, d_gutil;
+    DevBuf d_arr, d_bat, d_next, d_samples, d_rec, d_glat, d_gutil, d_gcdf, d_gguide;
 };
+
+// guide[j] = first i with !(cdf[i] < j/G): lower_bound's answer for u = j/G, a valid
+// start for every u >= j/G (the cdf is nondecreasing).
+static void append_guide(const std::vector<double>& cdf, std::vector<int16_t>& guide) {
+    for (int j = 0; j < msv::kGuide; ++j) {
+        const double uj = (double)j / (double)msv::kGuide;
+        size_t i = 0;
+        while (i < cdf.size() && cdf[i] < uj) ++i;
+        guide.push_back((int16_t)i);
+    }
+}
 
 struct msv_ctx {
     int device = 0;
@@ -166,15 +177,8 @@ struct msv_ctx {
             d.dev_off = cdf.size();
             cdf.insert(cdf.end(), d.cdf.begin(), d.cdf.end());
             pmf.insert(pmf.end(), d.pmf.begin(), d.pmf.end());
-            // guide[j] = first i with !(cdf[i] < j/G): lower_bound's answer for u = j/G,
-            // a valid start for every u >= j/G (the cdf is nondecreasing).
             d.guide_off = guide.size();
-            for (int j = 0; j < msv::kGuide; ++j) {
-                const double uj = (double)j / (double)msv::kGuide;
-                size_t i = 0;
-                while (i < d.cdf.size() && d.cdf[i] < uj) ++i;
-                guide.push_back((int16_t)i);
-            }
+            append_guide(d.cdf, guide);
         }
         n_cells = (int)lat.size();
         MSV_CUDA_TRY(d_lat.ensure(std::max<size_t>(lat.size(), 1) * 8));
@@ -735,6 +739,27 @@ int grid_build(msv_ctx* ctx, const msv_scenario* sc, int64_t n, const double* ta
         MSV_CUDA_TRY(cudaMemcpy(g->B->d_glat.p, glat.data(), glat.size() * 8, cudaMemcpyHostToDevice));
         MSV_CUDA_TRY(cudaMemcpy(g->B->d_gutil.p, gutil.data(), gutil.size() * 8, cudaMemcpyHostToDevice));
     }
+    // The grid's own copy of its batch distributions (cdf + guide): the context's tables
+    // are re-laid out (and may move) when later calls upload more distributions.
+    std::map<int, std::pair<size_t, size_t>> grid_dist_off;  // dist -> (cdf offset, guide offset)
+    if (g->generated) {
+        std::vector<double> gcdf;
+        std::vector<int16_t> gguide;
+        for (int64_t i = 0; i < n; ++i) {
+            if (grid_dist_off.count(sc[i].dist)) continue;
+            const std::vector<double>& cdf = ctx->dists[sc[i].dist].cdf;
+            grid_dist_off[sc[i].dist] = {gcdf.size(), gguide.size()};
+            gcdf.insert(gcdf.end(), cdf.begin(), cdf.end());
+            append_guide(cdf, gguide);
+        }
+        MSV_CUDA_TRY(g->B->d_gcdf.ensure(std::max<size_t>(gcdf.size(), 1) * 8));
+        MSV_CUDA_TRY(g->B->d_gguide.ensure(std::max<size_t>(gguide.size(), 1) * 2));
+        if (!gcdf.empty())
+            MSV_CUDA_TRY(cudaMemcpy(g->B->d_gcdf.p, gcdf.data(), gcdf.size() * 8, cudaMemcpyHostToDevice));
+        if (!gguide.empty())
+            MSV_CUDA_TRY(cudaMemcpy(g->B->d_gguide.p, gguide.data(), gguide.size() * 2, cudaMemcpyHostToDevice));
+        ctx->h2d += (int64_t)(gcdf.size() * 8 + gguide.size() * 2);
+    }
     // Partition tables per (plan, profile) and routing masks per (plan, profile, routing).
     std::map<std::pair<int, int>, size_t> part_off;
     std::map<std::tuple<int, int, int>, size_t> mask_off;
@@ -820,8 +845,8 @@ int grid_build(msv_ctx* ctx, const msv_scenario* sc, int64_t n, const double* ta
         t.seed = s.seed;
         t.rate_per_ms = s.rate_qps / 1000.0;  // workload.hpp:103
         t.duration_ms = s.duration_ms;
-        t.cdf = g->generated ? ctx->d_cdf.as<double>() + ctx->dists[s.dist].dev_off : nullptr;
-        t.guide = g->generated ? ctx->d_guide.as<int16_t>() + ctx->dists[s.dist].guide_off : nullptr;
+        t.cdf = g->generated ? g->B->d_gcdf.as<double>() + grid_dist_off[s.dist].first : nullptr;
+        t.guide = g->generated ? g->B->d_gguide.as<int16_t>() + grid_dist_off[s.dist].second : nullptr;
         t.b_max = g->generated ? (int32_t)ctx->dists[s.dist].cdf.size() : 0;
         t.pad = 0;
         t.arrival = g->B->d_arr.as<double>() + o;
@@ -997,7 +1022,7 @@ int grid_launch(msv_grid* g) {
     // launched in between (it may share the scratch buffers) restores the full fork.
     static const bool pipeline_env = !(getenv("MSV_PIPELINE") && atoi(getenv("MSV_PIPELINE")) == 0);
     const bool pipelined = pipeline_env && overlap && g->waves.size() == 1 && ctx->last_launch_grid == g->serial;
-    ctx->last_launch_grid = g->serial;
+    ctx->last_launch_grid = overlap ? g->serial : 0;  // a main-stream launch is never pipelined past
     // work counters: each (chunk, class) owns one slot (mod kCounterSlots), zeroed on the
     // stream that uses it right before the chunk
     auto zero_counters = [&](int base, size_t n, cudaStream_t s) -> int {

@@ -486,3 +486,47 @@ def test_shared_random_streams_match_reference(ref):
                            env=dict(os.environ, **extra), timeout=600)
         assert r.returncode == 0, r.stderr[-2000:]
         assert np.array_equal(np.load(out).view(np.uint64), ref_arr.view(np.uint64)), extra
+
+
+def _pipelined_launch_results():
+    """Back-to-back launches of one chunked single-wave grid (pipelined), interleaved with
+    another grid's run and a non-overlapped launch; every read must be the full result."""
+    eng = Engine(0)
+    specs = _shared_stream_grid()
+    g = eng.grid(specs, (0.5, 0.99))
+    g.set_usage(False)
+    outs = []
+    for _ in range(3):
+        g.launch()
+    outs.append(g.results())
+    m = W.model("bert_base")
+    p = W.paris(m, 8)
+    eng.run_grid([W._spec(m, p, 0.5 * W.capacity_qps(m, p), 2000, s) for s in range(1, 9)])
+    g.launch()
+    g.set_overlap(False)
+    g.launch()
+    g.set_overlap(True)
+    g.launch()
+    g.launch()
+    outs.append(g.results())
+    g.launch()
+    outs.append(g.results())
+    return [np.concatenate([o["placement_hash"].view(np.float64), o["tail"].ravel(), o["total"].astype(np.float64)])
+            for o in outs]
+
+
+def test_pipelined_launches_match_reference(ref):
+    import os
+    import sys
+    specs = _shared_stream_grid()
+    want = ref.run_grid(specs, (0.5, 0.99))
+    ref_arr = np.concatenate([want["placement_hash"].view(np.float64), want["tail"].ravel(),
+                              want["total"].astype(np.float64)])
+    code = ("import sys, numpy as np; sys.path.insert(0, %r); from tests.test_gpu_parity import _pipelined_launch_results; "
+            "np.save(sys.argv[1], np.stack(_pipelined_launch_results()))" % str(ROOT))
+    out = Path(f"/tmp/msv_pipe_{os.getpid()}.npy")
+    r = subprocess.run([sys.executable, "-c", code, str(out)], capture_output=True, text=True,
+                       env=dict(os.environ, MSV_CHUNK_SPLIT="2,1,1,1"), timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    for got in np.load(out):
+        assert np.array_equal(got.view(np.uint64), ref_arr.view(np.uint64))
