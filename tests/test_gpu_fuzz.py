@@ -164,3 +164,52 @@ def test_fuzz_runs_with_routing_and_checks(eng, ref):
     for i, (got, want) in enumerate(zip(eng.run_many(items), wants)):
         for k in KEYS:
             assert _same(got[k], want[k]), ("batched", i, k)
+
+
+def _fuzz_shared_stream_specs(seed, n):
+    """Random grids whose scenarios share seeds and distributions (so chunked waves
+    generate several traces per random stream), at random rates, lengths and plans."""
+    rng = np.random.default_rng(seed)
+    tables = [_random_table(rng, 5000 + i) for i in range(4)]
+    dists = [lognormal_batch_pdf(float(rng.uniform(0.0, 2.0)), float(rng.uniform(0.3, 1.5)), t.b_max) for t in tables]
+    specs = []
+    for i in range(n):
+        j = int(rng.integers(0, len(tables)))
+        table, dist = tables[j], dists[j]
+        plan = _random_plan(rng, [int(k) for k in table.sizes])
+        m = W.Model("fuzz", table, dist, SlaConfig(1.0))
+        rate = float(rng.choice([0.1, 0.5, 0.9, 1.2, 2.5])) * W.capacity_qps(m, plan)
+        queries = float(rng.choice([50, 400, 1500, 3000]))
+        sla_ms = derive_sla_target(table, table.b_max, float(rng.uniform(0.6, 3.0)))
+        specs.append(GridSpec(plan, table, dist, SlaConfig(sla_ms), rate, queries / rate * 1000.0,
+                              int(rng.integers(1, 12)), "elsa" if rng.random() < 0.7 else "fifs",
+                              float(rng.choice([0.0, 0.1]))))
+    return specs
+
+
+def _fuzz_shared_results():
+    r = Engine(0).run_grid(_fuzz_shared_stream_specs(99, 500), (0.5, 0.95, 0.99))
+    return np.concatenate([r["placement_hash"].view(np.float64), r["tail"].ravel(), r["total"].astype(np.float64),
+                           r["violations"].astype(np.float64)])
+
+
+def test_fuzz_shared_streams_chunked(ref):
+    """Random shared-stream grids through forced chunks (grouped trace generation) and the
+    default layout: bit-identical to the reference."""
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+    root = Path(__file__).resolve().parent.parent
+    specs = _fuzz_shared_stream_specs(99, 500)
+    w = ref.run_grid(specs, (0.5, 0.95, 0.99))
+    want = np.concatenate([w["placement_hash"].view(np.float64), w["tail"].ravel(), w["total"].astype(np.float64),
+                           w["violations"].astype(np.float64)])
+    code = ("import sys, numpy as np; sys.path.insert(0, %r); from tests.test_gpu_fuzz import _fuzz_shared_results; "
+            "np.save(sys.argv[1], _fuzz_shared_results())" % str(root))
+    for extra in ({"MSV_CHUNK_SPLIT": "2,1,1,1"}, {"MSV_CHUNK_SPLIT": "1,1,1", "MSV_TRACE_GROUP_FIRST": "16"}, {}):
+        out = Path(f"/tmp/msv_fz_{os.getpid()}.npy")
+        r = subprocess.run([sys.executable, "-c", code, str(out)], capture_output=True, text=True,
+                           env=dict(os.environ, **extra), timeout=900)
+        assert r.returncode == 0, r.stderr[-2000:]
+        assert np.array_equal(np.load(out).view(np.uint64), want.view(np.uint64)), extra
