@@ -1,5 +1,7 @@
-// K1 trace_gen_kernel: sample_trace (workload.hpp:97-113) on the device, one warp per
-// trace (warp_sample_trace, msv_trace.cuh).
+// K1: sample_trace (workload.hpp:97-113) on the device. trace_gen_kernel: one warp per
+// trace (warp_sample_trace); trace_group_kernel: one warp per random stream, i.e. per
+// group of traces with the same seed and batch distribution (warp_sample_trace_group);
+// both in msv_trace.cuh.
 #include "msv_trace.cuh"
 
 namespace msv {
