@@ -11,6 +11,7 @@ same comparisons), so the returned rates are bit-identical to the reference's.
 """
 from __future__ import annotations
 
+import copy
 from dataclasses import dataclass, field
 from typing import Sequence
 
@@ -121,8 +122,38 @@ def _mean_tail(tails: np.ndarray, measured: np.ndarray) -> float:
     return 0.0 if used == 0 else s / used
 
 
-def latency_bounded_throughput(eng: Engine, designs: Sequence[Design]) -> list[LbtResult]:
+def _clone(s: _Search) -> _Search:
+    c = copy.copy(s)
+    c.res = copy.copy(s.res)
+    return c
+
+
+def _probe_tree(s: _Search, depth: int) -> list[tuple[int, float]]:
+    """Rates the search may probe in its next `depth` steps: node k's children are 2k+1
+    (probe met the SLA) and 2k+2 (violated it); (node, rate) for every live node."""
+    out, level = [], [(0, s)]
+    for _ in range(depth):
+        nxt = []
+        for k, st in level:
+            if st.phase == _Search.DONE:
+                continue
+            out.append((k, st.rate))
+            for child, tail in ((2 * k + 1, -np.inf), (2 * k + 2, np.inf)):
+                c = _clone(st)
+                c.feed(tail)
+                nxt.append((child, c))
+        level = nxt
+    return out
+
+
+def latency_bounded_throughput(eng: Engine, designs: Sequence[Design], lookahead: int = 3) -> list[LbtResult]:
+    """Every design's bracket/bisection advanced in lockstep. Each round simulates the
+    rates of the next `lookahead` steps of every design's outcome tree (2^L - 1 probes per
+    design, all independent scenarios of one device grid) and then walks the tree with
+    the measured tails: the same probe sequence, comparisons and rates as the reference
+    (metrics.hpp:81-120), in L times fewer rounds. sims_run counts the probes taken."""
     searches = [_Search(d) for d in designs]
+    depth = max(1, int(lookahead))
     while True:
         active = [s for s in searches if s.phase != _Search.DONE]
         if not active:
@@ -131,17 +162,24 @@ def latency_bounded_throughput(eng: Engine, designs: Sequence[Design]) -> list[L
         for s in active:
             by_p.setdefault(s.d.opt.tail_p, []).append(s)
         for p, group in by_p.items():
-            specs = []
+            specs, where = [], []
             for s in group:
                 o = s.d.opt
-                specs += [GridSpec(s.d.plan, s.d.table, s.d.dist, s.d.sla, s.rate, o.duration_ms, seed,
-                                   s.d.scheduler, o.warmup_fraction) for seed in o.seeds]
+                nodes = {}
+                for k, rate in _probe_tree(s, depth):
+                    nodes[k] = (len(specs), rate)
+                    specs += [GridSpec(s.d.plan, s.d.table, s.d.dist, s.d.sla, rate, o.duration_ms, seed,
+                                       s.d.scheduler, o.warmup_fraction) for seed in o.seeds]
+                where.append(nodes)
             r = eng.run_grid(specs, (p,))
-            pos = 0
-            for s in group:
-                k = len(s.d.opt.seeds)
-                s.feed(_mean_tail(r["tail"][pos:pos + k, 0], r["measured"][pos:pos + k]))
-                pos += k
+            for s, nodes in zip(group, where):
+                k, n_seeds = 0, len(s.d.opt.seeds)
+                while k in nodes and s.phase != _Search.DONE:
+                    pos, rate = nodes[k]
+                    assert rate == s.rate  # the tree followed the search's own rule
+                    tail = _mean_tail(r["tail"][pos:pos + n_seeds, 0], r["measured"][pos:pos + n_seeds])
+                    s.feed(tail)
+                    k = 2 * k + (1 if not tail > s.d.sla.sla_target_ms else 2)
 
 
 def best_homogeneous(eng: Engine, table: ProfileTable, dist: BatchDistribution, sla: SlaConfig, total_gpcs: int,
