@@ -8,6 +8,8 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdint>
+#include <limits>
+#include <map>
 #include <numeric>
 #include <string>
 #include <vector>
@@ -174,43 +176,76 @@ struct LbtSearch {
     }
 };
 
-// Advance all searches together; each round is one device grid over every active
-// search's pending (rate x seeds).
+// Advance all searches together. Each round is one device grid over the rates of every
+// active search's next kLbtLookahead steps — its outcome tree: node k's children are
+// 2k+1 (the probe met the SLA) and 2k+2 (it did not) — all independent simulations;
+// the tree is then walked with the measured tails, so each search takes exactly the
+// reference's probes and rates (metrics.hpp:81-120) in kLbtLookahead times fewer rounds.
+constexpr int kLbtLookahead = 3;
+
 inline void run_lockstep(std::vector<LbtSearch>& searches) {
     for (LbtSearch& s : searches) s.start();
     for (;;) {
         std::vector<GridCell> cells;
-        std::vector<std::size_t> active, first;
+        struct Probe {
+            std::size_t search;
+            int node;
+            std::size_t first;
+        };
+        std::vector<Probe> probes;
         for (std::size_t i = 0; i < searches.size(); ++i) {
-            LbtSearch& s = searches[i];
-            if (s.done()) continue;
-            active.push_back(i);
-            first.push_back(cells.size());
-            append_probe(cells, *s.plan, s.scheduler, *s.table, s.cfg, *s.dist, s.rate, s.opt);
+            if (searches[i].done()) continue;
+            std::vector<std::pair<int, LbtSearch>> level{{0, searches[i]}};
+            for (int d = 0; d < kLbtLookahead && !level.empty(); ++d) {
+                std::vector<std::pair<int, LbtSearch>> next;
+                for (auto& [k, st] : level) {
+                    if (st.done()) continue;
+                    probes.push_back({i, k, cells.size()});
+                    append_probe(cells, *st.plan, st.scheduler, *st.table, st.cfg, *st.dist, st.rate, st.opt);
+                    LbtSearch ok = st, bad = st;
+                    ok.feed(-std::numeric_limits<double>::infinity());
+                    bad.feed(std::numeric_limits<double>::infinity());
+                    next.emplace_back(2 * k + 1, std::move(ok));
+                    next.emplace_back(2 * k + 2, std::move(bad));
+                }
+                level = std::move(next);
+            }
         }
-        if (active.empty()) return;
-        // All searches of one call share tail_p only if equal; group by it.
+        if (probes.empty()) return;
+        // one grid per distinct tail_p
         std::vector<GridCellResult> res(cells.size());
         std::vector<double> ps;
-        for (std::size_t a : active)
-            if (std::find(ps.begin(), ps.end(), searches[a].opt.tail_p) == ps.end()) ps.push_back(searches[a].opt.tail_p);
+        for (const Probe& pr : probes)
+            if (std::find(ps.begin(), ps.end(), searches[pr.search].opt.tail_p) == ps.end())
+                ps.push_back(searches[pr.search].opt.tail_p);
         for (double p : ps) {
             std::vector<GridCell> sub;
             std::vector<std::size_t> where;
-            for (std::size_t j = 0; j < active.size(); ++j) {
-                const LbtSearch& s = searches[active[j]];
+            for (const Probe& pr : probes) {
+                const LbtSearch& s = searches[pr.search];
                 if (s.opt.tail_p != p) continue;
                 for (std::size_t q = 0; q < s.opt.seeds.size(); ++q) {
-                    sub.push_back(cells[first[j] + q]);
-                    where.push_back(first[j] + q);
+                    sub.push_back(cells[pr.first + q]);
+                    where.push_back(pr.first + q);
                 }
             }
             const std::vector<GridCellResult> r = run_grid(sub, {p});
             for (std::size_t q = 0; q < r.size(); ++q) res[where[q]] = r[q];
         }
-        for (std::size_t j = 0; j < active.size(); ++j) {
-            LbtSearch& s = searches[active[j]];
-            s.feed(mean_of_probe(res, first[j], s.opt.seeds.size()));
+        std::map<std::pair<std::size_t, int>, std::size_t> at;
+        for (const Probe& pr : probes) at[{pr.search, pr.node}] = pr.first;
+        for (std::size_t i = 0; i < searches.size(); ++i) {
+            LbtSearch& s = searches[i];
+            int node = 0;
+            while (!s.done()) {
+                auto it = at.find({i, node});
+                if (it == at.end()) break;
+                const double tail = mean_of_probe(res, it->second, s.opt.seeds.size());
+                const double sla = s.cfg.sla_target_ms;  // the branch feed() takes
+                const bool bad = s.phase == LbtSearch::Bisect ? !(tail <= sla) : tail > sla;
+                s.feed(tail);
+                node = 2 * node + (bad ? 2 : 1);
+            }
         }
     }
 }

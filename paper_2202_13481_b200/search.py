@@ -178,8 +178,10 @@ def latency_bounded_throughput(eng: Engine, designs: Sequence[Design], lookahead
                     pos, rate = nodes[k]
                     assert rate == s.rate  # the tree followed the search's own rule
                     tail = _mean_tail(r["tail"][pos:pos + n_seeds, 0], r["measured"][pos:pos + n_seeds])
+                    sla = s.d.sla.sla_target_ms  # the branch feed() takes
+                    bad = not (tail <= sla) if s.phase == _Search.BISECT else tail > sla
                     s.feed(tail)
-                    k = 2 * k + (1 if not tail > s.d.sla.sla_target_ms else 2)
+                    k = 2 * k + (2 if bad else 1)
 
 
 def best_homogeneous(eng: Engine, table: ProfileTable, dist: BatchDistribution, sla: SlaConfig, total_gpcs: int,
