@@ -530,3 +530,24 @@ def test_pipelined_launches_match_reference(ref):
     assert r.returncode == 0, r.stderr[-2000:]
     for got in np.load(out):
         assert np.array_equal(got.view(np.uint64), ref_arr.view(np.uint64))
+
+
+def test_grid_extremes(eng, ref):
+    """The largest plan the engine takes (128 partitions, four slots per lane), one
+    partition, no tail percentiles at all, and four at once."""
+    m = W.model("mobilenet")
+    big = PartitionPlan(19, 7, [[1] * 7] * 18 + [[1, 1]])
+    assert big.total_instances() == 128
+    one = PartitionPlan(1, 7, [[7]])
+    specs = []
+    for p, load in ((big, 0.6), (big, 1.4), (one, 0.9), (one, 2.0)):
+        rate = load * W.capacity_qps(m, p)
+        for sched in ("elsa", "fifs"):
+            specs += [W._spec(m, p, rate, 3000, s, sched) for s in (1, 2)]
+    got, want = eng.run_grid(specs, ()), ref.run_grid(specs, ())
+    assert got["tail"].shape == (len(specs), 0)
+    for k in ("total", "violations", "measured", "measured_violations", "horizon_ms", "placement_hash", "status"):
+        assert np.array_equal(np.asarray(got[k]), np.asarray(want[k])), k
+    ps = (0.5, 0.9, 0.99, 0.999)
+    got, want = eng.run_grid(specs, ps), ref.run_grid(specs, ps)
+    assert np.array_equal(got["tail"].view(np.uint64), want["tail"].view(np.uint64))
