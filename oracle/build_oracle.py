@@ -81,6 +81,9 @@ def build_reference(force: bool = False) -> None:
     unit = REF_OUT / "ref_unit_tests"
     if force or _stale(unit, [*tests, *ref_headers, shim / "catch2" / "catch_amalgamated.hpp"]):
         _run(["g++", *flags, f"-I{shim}", str(shim / "shim_main.cpp"), *map(str, tests), "-o", str(unit)])
+    io_ref = REF_OUT / "io_check_ref"  # oracle/io_check.cpp on the reference's CPU engine
+    if force or _stale(io_ref, [HERE / "io_check.cpp", *ref_headers]):
+        _run(["g++", *flags, str(HERE / "io_check.cpp"), "-o", str(io_ref)])
 
 
 def build_dropin(force: bool = False) -> None:
@@ -99,6 +102,11 @@ def build_dropin(force: bool = False) -> None:
         _run(["g++", "-std=c++20", "-O2", "-DNDEBUG", "-pthread", f"-I{ROOT / 'include'}", f"-I{_json_dir()}",
               f"-I{shim}", f"-I{REF / 'tests'}", str(shim / "shim_main.cpp"), *map(str, tests), "-o", str(out),
               f"-L{libmsv.parent}", "-lmsv", f"-Wl,-rpath,{libmsv.parent}", "-Wl,-rpath,$ORIGIN/../../paper_2202_13481_b200"])
+    io_dev = REF_OUT / "io_check_dev"  # the same program on the device engine (drop-in headers)
+    if force or _stale(io_dev, [HERE / "io_check.cpp", *ours, libmsv]):
+        _run(["g++", "-std=c++20", "-O2", "-DNDEBUG", "-pthread", f"-I{ROOT / 'include'}", f"-I{_json_dir()}",
+              str(HERE / "io_check.cpp"), "-o", str(io_dev), f"-L{libmsv.parent}", "-lmsv",
+              f"-Wl,-rpath,{libmsv.parent}", "-Wl,-rpath,$ORIGIN/../../paper_2202_13481_b200"])
 
 
 def build(force: bool = False) -> None:

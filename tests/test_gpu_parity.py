@@ -551,3 +551,16 @@ def test_grid_extremes(eng, ref):
     ps = (0.5, 0.9, 0.99, 0.999)
     got, want = eng.run_grid(specs, ps), ref.run_grid(specs, ps)
     assert np.array_equal(got["tail"].view(np.uint64), want["tail"].view(np.uint64))
+
+
+def test_query_csv_and_report_json_byte_identical():
+    """SURVEY §8 f3 / SPEC acceptance #7: the same program (oracle/io_check.cpp: ELSA and
+    FIFS, routing, warm-up, wait check, overload; per-query CSV + report JSON) built on the
+    reference's CPU engine and on the device engine prints byte-identical output."""
+    ref_exe, dev_exe = ROOT / "oracle" / "_ref" / "io_check_ref", ROOT / "oracle" / "_ref" / "io_check_dev"
+    if not (ref_exe.exists() and dev_exe.exists()):
+        pytest.skip("io_check binaries not built (needs /root/reference at build time)")
+    want = subprocess.run([str(ref_exe)], capture_output=True, timeout=600, check=True).stdout
+    got = subprocess.run([str(dev_exe)], capture_output=True, timeout=600, check=True).stdout
+    assert want.count(b"# case") == 36 and len(want) > 1_000_000
+    assert got == want
