@@ -12,6 +12,9 @@ Outputs (all git-ignored, all travel to the GPU box with the repo snapshot):
                                 repo's include/migserve headers and linked to libmsv.so
                                 (every run()/sample_trace()/tail_latency()/dispatch call
                                 executes on the GPU) — the drop-in check
+  oracle/_ref/msv_cli_ref       paper_2202_13481_b200/cli/msv_cli.cpp (the run/plan/sweep
+                                runner) compiled against the reference headers: the
+                                checker for the product CLI paper_2202_13481_b200/msv
 
 The _ref targets need /root/reference (present in the build container only); on the
 GPU box the prebuilt files are used as they are.
@@ -81,6 +84,10 @@ def build_reference(force: bool = False) -> None:
     unit = REF_OUT / "ref_unit_tests"
     if force or _stale(unit, [*tests, *ref_headers, shim / "catch2" / "catch_amalgamated.hpp"]):
         _run(["g++", *flags, f"-I{shim}", str(shim / "shim_main.cpp"), *map(str, tests), "-o", str(unit)])
+    cli_src = ROOT / "paper_2202_13481_b200" / "cli" / "msv_cli.cpp"
+    cli_ref = REF_OUT / "msv_cli_ref"  # the SPEC's runner on the reference's CPU engine (the CLI checker)
+    if force or _stale(cli_ref, [cli_src, *ref_headers]):
+        _run(["g++", *flags, str(cli_src), "-o", str(cli_ref)])
     io_ref = REF_OUT / "io_check_ref"  # oracle/io_check.cpp on the reference's CPU engine
     if force or _stale(io_ref, [HERE / "io_check.cpp", *ref_headers]):
         _run(["g++", *flags, str(HERE / "io_check.cpp"), "-o", str(io_ref)])

@@ -2,6 +2,8 @@
 
     libmsv.so           csrc/*.cu (sm_100a kernels, -fmad=false) + csrc/*.cpp (host
                         runtime) -> paper_2202_13481_b200/libmsv.so, static cudart.
+    msv                 cli/msv_cli.cpp (the SPEC's run/plan/sweep runner) over include/migserve,
+                        linked to libmsv.so -> paper_2202_13481_b200/msv.
     oracle (test infra) delegated to oracle/build_oracle.py.
 
 Everything is written in-tree so the built files travel to the GPU box with the
@@ -89,8 +91,24 @@ def build_libmsv(force: bool = False, verbose: bool = False) -> Path:
     return LIB
 
 
+CLI = PKG / "msv"
+
+
+def build_cli(force: bool = False) -> Path:
+    """The experiment runner on the device engine: the drop-in headers + libmsv.so."""
+    src = PKG / "cli" / "msv_cli.cpp"
+    deps = [src, LIB, *sorted((ROOT / "include").rglob("*.h*"))]
+    if force or _stale(CLI, deps):
+        tmp = CLI.with_name("msv.tmp")
+        _run(["g++", "-std=c++20", "-O2", "-Wall", "-pthread", f"-I{ROOT / 'include'}", f"-I{json_include_dir()}",
+              str(src), "-o", str(tmp), f"-L{PKG}", "-lmsv", "-Wl,-rpath,$ORIGIN"])
+        os.replace(tmp, CLI)
+    return CLI
+
+
 def build_all(force: bool = False) -> None:
     build_libmsv(force=force)
+    build_cli(force=force)
     sys.path.insert(0, str(ROOT / "oracle"))
     try:
         import build_oracle  # type: ignore
