@@ -38,7 +38,7 @@ inline SchedulerKind scheduler_from_string(const std::string& name) {
 
 struct EngineOptions {
     double warmup_fraction = 0.1;
-    double noise_sigma = 0.0;  // lognormal execution noise; the device engine supports 0 only
+    double noise_sigma = 0.0;  // lognormal execution noise, 0 = exact (engine.hpp:37-38)
     uint64_t noise_seed = 1;
     bool check_wait_consistency = false;
     bool segment_routing = false;
@@ -127,8 +127,6 @@ inline void check_run_args(const PartitionPlan& plan, const SlaConfig& cfg, cons
         throw ParamError("run: warmup_fraction must be in [0,1)");
     if (options.segment_routing && options.routing_segments.empty())
         throw ParamError("run: segment_routing enabled without segments");
-    if (options.noise_sigma > 0.0)
-        throw ParamError("run: execution noise (noise_sigma > 0) is not supported by the device engine");
 }
 
 }  // namespace detail
@@ -175,9 +173,26 @@ inline SimReport run(const PartitionPlan& plan, SchedulerKind scheduler, const Q
     const std::vector<PartitionSize> sizes = plan.flatten();
     std::vector<msv_usage> usage(sizes.size());
     std::vector<msv_record> rec(std::max<std::size_t>(n, 1));
-    device::check(msv_run_replay(ctx, &s, 1, offsets, arr.data(), bat.data(), nullptr, 0, &res, usage.data(),
-                                 rec.data()),
-                  "run");
+    if (options.noise_sigma > 0.0) {
+        // Execution noise (engine.hpp:140-145): the j-th query started runs for
+        // est * exp(sigma*z_j - sigma^2/2), z_j the j-th Rng(noise_seed).normal(). The
+        // multipliers are an input stream (drawn here with the reference's Rng and libm,
+        // n of them: every query starts once); the device starts queries in the global
+        // event order, so query j-th-started takes multiplier j (msv_noise.cu).
+        Rng noise_rng(options.noise_seed);
+        std::vector<double> mult(std::max<std::size_t>(n, 1));
+        for (std::size_t j = 0; j < n; ++j) {
+            const double z = noise_rng.normal();
+            mult[j] = std::exp(options.noise_sigma * z - 0.5 * options.noise_sigma * options.noise_sigma);
+        }
+        device::check(msv_run_noise(ctx, &s, static_cast<int64_t>(n), arr.data(), bat.data(), mult.data(), &res,
+                                    usage.data(), rec.data()),
+                      "run");
+    } else {
+        device::check(msv_run_replay(ctx, &s, 1, offsets, arr.data(), bat.data(), nullptr, 0, &res, usage.data(),
+                                     rec.data()),
+                      "run");
+    }
     SimReport rep;
     rep.queries.resize(n);
     for (std::size_t j = 0; j < n; ++j) {

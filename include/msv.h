@@ -151,6 +151,16 @@ int msv_run_replay(msv_ctx* ctx, const msv_scenario* scenarios, int64_t n, const
                    const double* arrival_ms, const int32_t* batch, const double* tail_p,
                    int n_tails, msv_result* results, msv_usage* usage, msv_record* records);
 
+/* run() with execution noise (EngineOptions::noise_sigma > 0, engine.hpp:140-145) on one
+ * host trace (sorted by arrival), with per-query records. noise_mult[j] = exp(sigma*z_j -
+ * 0.5*sigma*sigma), z_j the j-th Rng(noise_seed).normal() (rng.hpp:27-31), is the
+ * multiplier of the j-th query started; the caller draws them (n of them: every query
+ * starts once) with the reference's Rng and libm, and the device starts queries in the
+ * reference's global event order. P <= 64. No tails (result->tail = NaN). */
+int msv_run_noise(msv_ctx* ctx, const msv_scenario* scenario, int64_t n, const double* arrival_ms,
+                  const int32_t* batch, const double* noise_mult, msv_result* result, msv_usage* usage,
+                  msv_record* records);
+
 /* sample_trace() on the device (workload.hpp:97-113). On MSV_PARAM with *n_out > cap
  * the trace did not fit; retry with cap >= *n_out. */
 int msv_sample_trace(msv_ctx* ctx, int32_t dist, double rate_qps, double duration_ms,

@@ -7,6 +7,7 @@
 #include <string.h>
 
 #include <algorithm>
+#include <limits>
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
@@ -1740,6 +1741,101 @@ int msv_run_replay(msv_ctx* ctx, const msv_scenario* scenarios, int64_t n, const
     rc = grid_launch(g);
     if (rc) return rc;
     return grid_results(g, results, usage, records, nullptr);
+}
+
+// run() with execution noise (engine.hpp:140-145): K5 (msv_noise.cu), one warp.
+int msv_run_noise(msv_ctx* ctx, const msv_scenario* scenario, int64_t n, const double* arrival_ms,
+                  const int32_t* batch, const double* noise_mult, msv_result* result, msv_usage* usage,
+                  msv_record* records) {
+    if (!ctx || !scenario || !result || (n > 0 && (!arrival_ms || !batch || !noise_mult || !records)))
+        return fail(MSV_PARAM, "null argument");
+    if (n < 0 || n >= (int64_t)UINT32_MAX) return fail(MSV_PARAM, "run: trace length out of range");
+    SetDevice sd(ctx->device);
+    const msv_scenario& sc = *scenario;
+    int32_t P = 0;
+    int rc = validate_scenario(ctx, sc, false, &P);
+    if (rc) return rc;
+    if (P > 64) return fail(MSV_PARAM, "run: execution noise on the device supports at most 64 partitions");
+    for (int64_t i = 1; i < n; ++i)
+        if (arrival_ms[i] < arrival_ms[i - 1]) return fail(MSV_PARAM, "run: trace must be sorted by arrival");
+    const Profile& prof = ctx->profiles[sc.profile];
+    const std::vector<DevPart> parts = plan_parts(ctx->plans[sc.plan], prof, 0);
+    std::vector<uint64_t> masks;
+    if (sc.routing >= 0) masks = route_masks(parts, ctx->routings[sc.routing], prof.b_max);
+    const size_t nn = (size_t)std::max<int64_t>(n, 1);
+    DevBuf d_arr, d_bat, d_mult, d_lat, d_util, d_parts, d_masks, d_next, d_rec, d_use, d_out;
+    MSV_CUDA_TRY(d_arr.ensure(nn * 8));
+    MSV_CUDA_TRY(d_bat.ensure(nn * 4));
+    MSV_CUDA_TRY(d_mult.ensure(nn * 8));
+    MSV_CUDA_TRY(d_lat.ensure(prof.lat.size() * 8));
+    MSV_CUDA_TRY(d_util.ensure(prof.util.size() * 8));
+    MSV_CUDA_TRY(d_parts.ensure(parts.size() * sizeof(DevPart)));
+    MSV_CUDA_TRY(d_masks.ensure(std::max<size_t>(masks.size(), 1) * 8));
+    MSV_CUDA_TRY(d_next.ensure(nn * 4));
+    MSV_CUDA_TRY(d_rec.ensure(nn * sizeof(msv_record)));
+    MSV_CUDA_TRY(d_use.ensure((size_t)P * sizeof(msv_usage)));
+    MSV_CUDA_TRY(d_out.ensure(sizeof(DevOut)));
+    cudaStream_t st = ctx->stream;
+    if (n > 0) {
+        MSV_CUDA_TRY(cudaMemcpyAsync(d_arr.p, arrival_ms, (size_t)n * 8, cudaMemcpyHostToDevice, st));
+        MSV_CUDA_TRY(cudaMemcpyAsync(d_bat.p, batch, (size_t)n * 4, cudaMemcpyHostToDevice, st));
+        MSV_CUDA_TRY(cudaMemcpyAsync(d_mult.p, noise_mult, (size_t)n * 8, cudaMemcpyHostToDevice, st));
+    }
+    MSV_CUDA_TRY(cudaMemcpyAsync(d_lat.p, prof.lat.data(), prof.lat.size() * 8, cudaMemcpyHostToDevice, st));
+    MSV_CUDA_TRY(cudaMemcpyAsync(d_util.p, prof.util.data(), prof.util.size() * 8, cudaMemcpyHostToDevice, st));
+    MSV_CUDA_TRY(
+        cudaMemcpyAsync(d_parts.p, parts.data(), parts.size() * sizeof(DevPart), cudaMemcpyHostToDevice, st));
+    if (!masks.empty())
+        MSV_CUDA_TRY(cudaMemcpyAsync(d_masks.p, masks.data(), masks.size() * 8, cudaMemcpyHostToDevice, st));
+    MSV_CUDA_TRY(cudaMemsetAsync(d_rec.p, 0, nn * sizeof(msv_record), st));
+    MSV_CUDA_TRY(cudaMemsetAsync(d_out.p, 0, sizeof(DevOut), st));
+    ctx->h2d += n * 20 + (int64_t)(prof.lat.size() * 16 + parts.size() * sizeof(DevPart) + masks.size() * 8);
+    msv::NoiseParams np{};
+    np.arrival = d_arr.as<double>();
+    np.batch = d_bat.as<int32_t>();
+    np.n = n;
+    np.mult = d_mult.as<double>();
+    np.lat = d_lat.as<double>();
+    np.util = d_util.as<double>();
+    np.parts = d_parts.as<DevPart>();
+    np.route_mask = masks.empty() ? nullptr : d_masks.as<uint64_t>();
+    np.P = P;
+    np.b_max = prof.b_max;
+    np.sched = sc.scheduler;
+    np.sla = sc.sla_ms;
+    np.alpha = sc.alpha;
+    np.beta = sc.beta;
+    np.warmup_ms = sc.warmup_fraction * sc.duration_ms;  // engine.hpp:236
+    np.next = d_next.as<uint32_t>();
+    np.records = d_rec.as<msv_record>();
+    np.usage = d_use.as<msv_usage>();
+    np.out = d_out.as<DevOut>();
+    MSV_CUDA_TRY(msv::launch_noise(np, st));
+    ctx->launches += 1;
+    DevOut o{};
+    MSV_CUDA_TRY(cudaMemcpyAsync(&o, d_out.p, sizeof(DevOut), cudaMemcpyDeviceToHost, st));
+    if (n > 0)
+        MSV_CUDA_TRY(cudaMemcpyAsync(records, d_rec.p, (size_t)n * sizeof(msv_record), cudaMemcpyDeviceToHost, st));
+    if (usage)
+        MSV_CUDA_TRY(cudaMemcpyAsync(usage, d_use.p, (size_t)P * sizeof(msv_usage), cudaMemcpyDeviceToHost, st));
+    MSV_CUDA_TRY(cudaStreamSynchronize(st));
+    ctx->d2h += (int64_t)sizeof(DevOut) + n * (int64_t)sizeof(msv_record) + (usage ? P * (int64_t)sizeof(msv_usage) : 0);
+    if (o.status) return fail(o.status, "run: profile lookup outside the grid (LookupError)");
+    msv_result& r = *result;
+    r = msv_result{};
+    r.total = n;
+    r.violations = o.violations;
+    r.measured = o.measured;
+    r.measured_violations = o.measured_violations;
+    for (double& t : r.tail) t = std::numeric_limits<double>::quiet_NaN();
+    r.horizon_ms = sc.duration_ms < o.horizon_ms ? o.horizon_ms : sc.duration_ms;  // engine.hpp:235
+    r.warmup_ms = np.warmup_ms;
+    r.max_wait_estimate_diff = 0.0;  // the reference skips the check under noise (engine.hpp:208)
+    r.duration_ms = sc.duration_ms;
+    r.placement_hash = o.hash;
+    r.status = MSV_OK;
+    r.n_partitions = P;
+    return MSV_OK;
 }
 
 int msv_sample_trace(msv_ctx* ctx, int32_t dist, double rate_qps, double duration_ms, uint64_t seed, int64_t cap,

@@ -166,7 +166,26 @@ struct ParisParams {
     int32_t* remaining;  // scratch: num_gpus ints per job at gpu_off
 };
 
+// K5: one run() with execution noise (msv_noise.cu), one warp, P <= 64.
+struct NoiseParams {
+    const double* arrival;      // sorted trace (device)
+    const int32_t* batch;
+    int64_t n;
+    const double* mult;         // n noise multipliers exp(sigma*z_j - sigma^2/2), start order
+    const double* lat;          // this profile's cells, row-major [size_idx][batch-1]
+    const double* util;
+    const DevPart* parts;       // P entries in (k, id) order; row relative to lat, -1 = size missing
+    const uint64_t* route_mask; // P masks or null
+    int32_t P, b_max, sched, pad;
+    double sla, alpha, beta, warmup_ms;
+    uint32_t* next;             // n: FIFO links through query indices
+    msv_record* records;        // n
+    msv_usage* usage;           // P, by partition id
+    DevOut* out;                // violations, measured, measured_violations, hash, horizon (last finish), status
+};
+
 // Kernel launchers (msv_kernels.cu). Return cudaGetLastError().
+cudaError_t launch_noise(const NoiseParams& p, cudaStream_t stream);
 cudaError_t launch_paris(const ParisParams& p, cudaStream_t stream);
 // K1 over groups: group g covers jobs [first, first + count) (count <= kTraceGroupMax, one
 // seed and distribution per group).

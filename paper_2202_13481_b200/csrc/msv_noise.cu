@@ -1,0 +1,370 @@
+// K5 sim_noise_kernel: run() (engine.hpp:115-253) with execution noise
+// (EngineOptions::noise_sigma > 0, engine.hpp:140-145): every start draws the next
+// Rng(noise_seed).normal() and runs for est * exp(sigma*z - sigma^2/2) instead of est.
+//
+// The noise-free kernels rely on the drain rule: completions on
+// different partitions commute, so each lane retires its own chain. With noise they do
+// not: the j-th start takes the j-th draw, so starts must happen in the reference's global
+// event order — (time asc, completion before arrival, seq asc), seq = push order
+// (engine.hpp:93-107, :134-137). This kernel keeps that order exactly:
+//   * one warp per scenario, lane slot s of lane l = by_ascending_size index s*32 + l
+//     (sched.hpp:96-104), P <= 64;
+//   * before each arrival (and after the last) the warp repeatedly takes the global
+//     minimum (completion time, seq) over the slots with completion <= t — a shuffle
+//     argmin — and retires it; a queue head started there takes the next multiplier and
+//     the next seq, so a chain of starts inside one drain keeps the heap's order;
+//   * ELSA / FIFS decisions are msv_sim_warp.cu's (ballot Step A in scan order, shuffle
+//     argmin Step B, FIFS key reductions), on the same exact left fold of Eq. 1;
+//   * the multipliers exp(sigma*z_j - sigma^2/2) are an input stream drawn by the caller
+//     with the reference's Rng (rng.hpp:27-31) and libm, like a replayed trace: the device
+//     consumes multiplier j at the j-th start (est * m_j, one RN multiply, engine.hpp:144).
+// Compiled with -fmad=false like every decision path (Appendix A.13).
+#include <math_constants.h>
+
+#include "msv_device.cuh"
+
+namespace msv {
+
+namespace {
+
+constexpr int kNoiseSlots = 2;  // P <= 64
+
+__global__ void __launch_bounds__(32, 1) sim_noise_kernel(const NoiseParams p) {
+    constexpr int S = kNoiseSlots;
+    const int lane = threadIdx.x & 31;
+    const double* __restrict__ arr = p.arrival;
+    const int32_t* __restrict__ bat = p.batch;
+    const double* __restrict__ lat = p.lat;
+    const int64_t n = p.n;
+    const double sla = p.sla, alpha = p.alpha, beta = p.beta, warmup = p.warmup_ms;
+    const bool route = p.route_mask != nullptr;
+
+    bool act[S], busy[S];
+    int32_t row[S], pid[S], kk[S];
+    uint64_t rmask[S];
+    int64_t qh[S], qt[S], qn[S];
+    double fold[S], c_start[S], c_est[S], c_comp[S], bms[S], wbms[S];
+    uint64_t c_seq[S];
+    int64_t cq[S], nq[S];
+#pragma unroll
+    for (int s = 0; s < S; ++s) {
+        const int o = s * 32 + lane;
+        act[s] = o < p.P;
+        const DevPart dp = act[s] ? p.parts[o] : DevPart{0, 0, -1, 0};
+        row[s] = dp.row;
+        pid[s] = dp.pid;
+        kk[s] = dp.k;
+        rmask[s] = (act[s] && route) ? p.route_mask[o] : 0;
+        busy[s] = false;
+        qh[s] = qt[s] = -1;
+        qn[s] = 0;
+        fold[s] = c_start[s] = c_est[s] = c_comp[s] = bms[s] = wbms[s] = 0.0;
+        c_seq[s] = 0;
+        cq[s] = -1;
+        nq[s] = 0;
+    }
+    uint64_t seq = (uint64_t)n;  // arrivals hold seq 0..n-1 (engine.hpp:136-137)
+    int64_t j = 0;               // next noise multiplier
+    int64_t viol = 0, meas = 0, mviol = 0;
+    uint64_t hash = 0;
+    double last_finish = 0.0;
+    int status = 0;
+
+    // Exact left fold of slot s's FIFO (sched.hpp:78-79).
+    auto refold = [&](int s) {
+        double acc = 0.0;
+        int64_t q = qh[s];
+        for (int64_t i = 0; i < qn[s]; ++i) {
+            acc = acc + lat[row[s] + bat[q] - 1];
+            q = p.next[q];
+        }
+        return acc;
+    };
+
+    // Retire, in global (time, seq) order, every completion with time <= t.
+    auto drain = [&](double t) {
+        for (;;) {
+            double bt = CUDART_INF;
+            uint64_t bs = ~0ull;
+            int bsl = -1;
+#pragma unroll
+            for (int s = 0; s < S; ++s)
+                if (busy[s] && c_comp[s] <= t && (c_comp[s] < bt || (c_comp[s] == bt && c_seq[s] < bs))) {
+                    bt = c_comp[s];
+                    bs = c_seq[s];
+                    bsl = s;
+                }
+            int bl = bsl >= 0 ? lane : 32;
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) {
+                const double ot = __shfl_xor_sync(kFull, bt, off);
+                const uint64_t os = __shfl_xor_sync(kFull, bs, off);
+                const int ol = __shfl_xor_sync(kFull, bl, off);
+                if (ot < bt || (ot == bt && os < bs)) {
+                    bt = ot;
+                    bs = os;
+                    bl = ol;
+                }
+            }
+            if (bl == 32) return;  // nothing due by t
+            int started = 0;
+            if (lane == bl) {
+#pragma unroll
+                for (int s = 0; s < S; ++s) {
+                    if (s != bsl) continue;
+                    const double now = c_comp[s];  // engine.hpp:167-187
+                    const int64_t q = cq[s];
+                    const double a = arr[q];
+                    const double l = now - a;
+                    const bool met = l <= sla;
+                    const double ran = now - c_start[s];
+                    bms[s] = bms[s] + ran;
+                    wbms[s] = wbms[s] + ran * p.util[row[s] + bat[q] - 1];
+                    nq[s] += 1;
+                    viol += met ? 0 : 1;
+                    if (a >= warmup) {
+                        meas += 1;
+                        mviol += met ? 0 : 1;
+                    }
+                    last_finish = last_finish < now ? now : last_finish;
+                    hash += msv_query_digest((uint64_t)q, pid[s], c_start[s], now);
+                    p.records[q].finish_ms = now;
+                    if (qn[s] > 0) {  // start the queue head now (engine.hpp:181-185)
+                        const int64_t h = qh[s];
+                        qh[s] = p.next[h];
+                        qn[s] -= 1;
+                        if (qn[s] == 0) qt[s] = -1;
+                        const double est = lat[row[s] + bat[h] - 1];
+                        c_start[s] = now;
+                        c_est[s] = est;
+                        c_comp[s] = now + est * p.mult[j];
+                        c_seq[s] = seq;
+                        cq[s] = h;
+                        p.records[h].start_ms = now;
+                        fold[s] = refold(s);
+                        started = 1;
+                    } else {
+                        busy[s] = false;
+                        fold[s] = 0.0;
+                    }
+                }
+            }
+            if (__shfl_sync(kFull, started, bl)) {
+                j += 1;
+                seq += 1;
+            }
+        }
+    };
+
+    for (int64_t i = 0; i < n && status == 0; ++i) {
+        const double t = arr[i];
+        drain(t);  // completions at <= t precede the arrival (engine.hpp:101-107)
+        const int b = bat[i];
+        if (b < 1 || b > p.b_max) {  // every lookup of this query fails (profile.hpp:123-132)
+            status = MSV_LOOKUP;
+            break;
+        }
+        // candidates (engine.hpp:197-206): routed partitions, else all
+        bool cand[S];
+        unsigned any = 0;
+#pragma unroll
+        for (int s = 0; s < S; ++s) {
+            cand[s] = act[s] && route && ((rmask[s] >> (b - 1)) & 1ull);
+            any |= __ballot_sync(kFull, cand[s]);
+        }
+        if (any == 0) {
+#pragma unroll
+            for (int s = 0; s < S; ++s) cand[s] = act[s];
+        }
+        int csl = -1, cl = 0, kind = 0;
+        if (p.sched == MSV_ELSA) {
+            double w[S], est[S];
+            unsigned okb[S], badb[S];
+#pragma unroll
+            for (int s = 0; s < S; ++s) {
+                const bool good = cand[s] && row[s] >= 0;
+                est[s] = good ? lat[row[s] + b - 1] : 0.0;
+                double x = fold[s];  // t_wait, Eq. 1 (sched.hpp:77-85)
+                if (busy[s]) {
+                    const double r = c_est[s] - (t - c_start[s]);
+                    x = x + (0.0 < r ? r : 0.0);
+                }
+                w[s] = x;
+                okb[s] = __ballot_sync(kFull, good && sla > alpha * (x + beta * est[s]));
+                badb[s] = __ballot_sync(kFull, cand[s] && row[s] < 0);
+            }
+            // Step A: the first candidate in scan order that satisfies the SLA (or whose
+            // lookup fails first) (sched.hpp:124-129)
+#pragma unroll
+            for (int s = 0; s < S; ++s) {
+                if (csl >= 0 || status) continue;
+                const unsigned m = okb[s] | badb[s];
+                if (m) {
+                    const int f = __ffs(m) - 1;
+                    if ((badb[s] >> f) & 1u) {
+                        status = MSV_LOOKUP;
+                    } else {
+                        csl = s;
+                        cl = f;
+                        kind = MSV_SLACK_SATISFYING;
+                    }
+                }
+            }
+            if (csl < 0 && !status) {  // Step B: argmin w + est, earliest in scan order (sched.hpp:131-141)
+                unsigned bad = 0;
+#pragma unroll
+                for (int s = 0; s < S; ++s) bad |= badb[s];
+                if (bad) {
+                    status = MSV_LOOKUP;
+                } else {
+                    double bv = CUDART_INF;
+                    int bo = 1 << 30;
+#pragma unroll
+                    for (int s = 0; s < S; ++s) {
+                        const double v = w[s] + est[s];
+                        if (cand[s] && v < bv) {  // slots ascend in scan order
+                            bv = v;
+                            bo = s * 32 + lane;
+                        }
+                    }
+#pragma unroll
+                    for (int off = 16; off > 0; off >>= 1) {
+                        const double ov = __shfl_xor_sync(kFull, bv, off);
+                        const int oo = __shfl_xor_sync(kFull, bo, off);
+                        if (ov < bv || (ov == bv && oo < bo)) {
+                            bv = ov;
+                            bo = oo;
+                        }
+                    }
+                    csl = bo >> 5;
+                    cl = bo & 31;
+                    kind = MSV_FASTEST_FALLBACK;
+                }
+            }
+        } else {  // FIFS (sched.hpp:154-170): ties by partition id
+            unsigned key = 0;  // idle: max k, then min id
+#pragma unroll
+            for (int s = 0; s < S; ++s)
+                if (cand[s] && !busy[s]) {
+                    const unsigned kv = ((unsigned)kk[s] << 10) | (unsigned)(1023 - pid[s]);
+                    key = kv > key ? kv : key;
+                }
+            const unsigned best = __reduce_max_sync(kFull, key);
+            if (best) {
+                const int want = 1023 - (int)(best & 1023u);
+#pragma unroll
+                for (int s = 0; s < S; ++s) {
+                    const unsigned hit = __ballot_sync(kFull, cand[s] && !busy[s] && pid[s] == want);
+                    if (hit) {
+                        csl = s;
+                        cl = __ffs(hit) - 1;
+                    }
+                }
+                kind = MSV_IDLE_LARGEST;
+            } else {  // shortest queue by count, then min id
+                unsigned long long qk = ~0ull;
+#pragma unroll
+                for (int s = 0; s < S; ++s)
+                    if (cand[s]) {
+                        const unsigned long long v = ((unsigned long long)qn[s] << 10) | (unsigned)pid[s];
+                        qk = v < qk ? v : qk;
+                    }
+#pragma unroll
+                for (int off = 16; off > 0; off >>= 1) {
+                    const unsigned long long o = __shfl_xor_sync(kFull, qk, off);
+                    qk = o < qk ? o : qk;
+                }
+                const int want = (int)(qk & 1023u);
+#pragma unroll
+                for (int s = 0; s < S; ++s) {
+                    const unsigned hit = __ballot_sync(kFull, cand[s] && pid[s] == want);
+                    if (hit) {
+                        csl = s;
+                        cl = __ffs(hit) - 1;
+                    }
+                }
+                kind = MSV_SHORTEST_QUEUE;
+            }
+        }
+        if (status) break;
+        // the chosen partition: est lookup (engine.hpp:224-229), start or enqueue
+        int started = 0, lookup_bad = 0;
+        if (lane == cl) {
+#pragma unroll
+            for (int s = 0; s < S; ++s) {
+                if (s != csl) continue;
+                if (row[s] < 0) {
+                    lookup_bad = 1;
+                    continue;
+                }
+                const double est = lat[row[s] + b - 1];
+                p.records[i].partition = pid[s];
+                p.records[i].kind = kind;
+                if (busy[s]) {
+                    if (qn[s] == 0) {
+                        qh[s] = i;
+                    } else {
+                        p.next[qt[s]] = (uint32_t)i;
+                    }
+                    qt[s] = i;
+                    qn[s] += 1;
+                    fold[s] = fold[s] + est;  // the left fold extends exactly on append
+                } else {
+                    busy[s] = true;
+                    c_start[s] = t;
+                    c_est[s] = est;
+                    c_comp[s] = t + est * p.mult[j];
+                    c_seq[s] = seq;
+                    cq[s] = i;
+                    fold[s] = 0.0;
+                    p.records[i].start_ms = t;
+                    started = 1;
+                }
+            }
+        }
+        if (__shfl_sync(kFull, lookup_bad, cl)) {
+            status = MSV_LOOKUP;
+            break;
+        }
+        if (__shfl_sync(kFull, started, cl)) {
+            j += 1;
+            seq += 1;
+        }
+    }
+    if (status == 0) drain(CUDART_INF);  // run to completion (no horizon cut-off)
+
+    // per-partition usage by id, totals
+#pragma unroll
+    for (int s = 0; s < S; ++s)
+        if (act[s] && p.usage) {
+            p.usage[pid[s]].busy_ms = bms[s];
+            p.usage[pid[s]].weighted_busy_ms = wbms[s];
+            p.usage[pid[s]].queries = nq[s];
+        }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+        viol += __shfl_xor_sync(kFull, viol, off);
+        meas += __shfl_xor_sync(kFull, meas, off);
+        mviol += __shfl_xor_sync(kFull, mviol, off);
+        hash += __shfl_xor_sync(kFull, hash, off);
+        const double o = __shfl_xor_sync(kFull, last_finish, off);
+        last_finish = last_finish < o ? o : last_finish;
+    }
+    if (lane == 0) {
+        p.out->violations = viol;
+        p.out->measured = meas;
+        p.out->measured_violations = mviol;
+        p.out->hash = hash;
+        p.out->horizon_ms = last_finish;  // the host takes max(duration, last_finish)
+        p.out->status = status;
+    }
+}
+
+}  // namespace
+
+cudaError_t launch_noise(const NoiseParams& p, cudaStream_t stream) {
+    sim_noise_kernel<<<1, 32, 0, stream>>>(p);
+    return cudaGetLastError();
+}
+
+}  // namespace msv

@@ -188,10 +188,38 @@ def test_sweep_tree_identical_to_reference(tmp_path, cfg, extra):
     assert len(t["plot_data.csv"].decode().splitlines()) == 1 + 4 * 6
 
 
+NOISE_CASES = [
+    # (config, overrides): ELSA / FIFS / routing / explicit and random plans on 8 GPUs
+    ("bert_8gpu_run.json", ("--set", "engine.noise_sigma=0.3", "--set", "engine.noise_seed=5")),
+    # busier, other sigma, no warm-up, wait check requested (skipped under noise, engine.hpp:208)
+    ("bert_8gpu_run.json", ("--set", "engine.noise_sigma=0.6", "--set", "workload.rate_qps=1100",
+                            "--set", "engine.warmup_fraction=0")),
+    # one 7g partition at overload: long queues, completion chains inside one drain
+    ("paris_vs_gpu7.json", ("--set", "engine.noise_sigma=0.25", "--set", "workload.duration_ms=1500")),
+    # 56 x 1g partitions (both lane slots), FIFS and ELSA
+    ("bert_8gpu_run.json", ("--set", "engine.noise_sigma=0.4", "--set", "workload.rate_qps=900",
+                            "--set", 'designs=[{"plan": "gpu(1)", "scheduler": "fifs"}, {"plan": "gpu(1)", "scheduler": "elsa"}]')),
+]
+
+
+@pytest.mark.gpu
+@need_ref
+@need_dev
+@pytest.mark.parametrize("cfg,extra", NOISE_CASES)
+def test_noise_run_tree_identical_to_reference(tmp_path, cfg, extra):
+    """Execution noise (engine.hpp:140-145) on the device (K5): per-query CSVs and reports
+    byte-identical to the reference engine's."""
+    t = _both(tmp_path, "run", EX / cfg, *extra)
+    res = json.loads(t["resolved_config.json"])
+    assert res["engine"]["noise_sigma"] > 0
+    assert any(json.loads(v)["noise_sigma"] > 0 for k, v in t.items() if k.startswith("reports/") and k.endswith(".json"))
+
+
 @pytest.mark.gpu
 @need_dev
-def test_noise_rejected_on_device(tmp_path):
-    """Execution noise is outside the device scope: ParamError, exit 1."""
-    cfg = write_cfg(tmp_path, {**SMALL, "engine": {"noise_sigma": 0.1}})
+def test_noise_partition_limit(tmp_path):
+    """K5 holds at most 64 partitions (two lane slots): larger plans raise ParamError."""
+    cfg = write_cfg(tmp_path, {**SMALL, "server": {"num_gpus": 10}, "engine": {"noise_sigma": 0.1},
+                               "designs": [{"plan": "gpu(1)", "scheduler": "elsa"}]})
     r = msv(DEV, "run", cfg, "--out", tmp_path / "o")
-    assert r.returncode == 1 and "ParamError" in r.stderr, r.stderr
+    assert r.returncode == 1 and "ParamError" in r.stderr and "64" in r.stderr, r.stderr
