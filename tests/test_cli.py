@@ -223,3 +223,31 @@ def test_noise_partition_limit(tmp_path):
                                "designs": [{"plan": "gpu(1)", "scheduler": "elsa"}]})
     r = msv(DEV, "run", cfg, "--out", tmp_path / "o")
     assert r.returncode == 1 and "ParamError" in r.stderr and "64" in r.stderr, r.stderr
+
+
+@pytest.mark.gpu
+@need_ref
+@need_dev
+def test_noise_randomised_against_reference(tmp_path):
+    """Random noisy runs (plans of 1-63 partitions on 1-9 GPUs, ELSA/FIFS, routing, alpha/beta,
+    sigma 0.05-1, light to overloaded rates): per-query CSVs and reports byte-identical."""
+    import random
+    rng = random.Random(20261019)
+    for case in range(24):
+        gpus = rng.randint(1, 9)
+        plan = rng.choice(["paris", f"random({rng.randint(0, 99)})", f"gpu({rng.choice([1, 2, 3, 7])})"])
+        cfg = {
+            "profile": {"preset": rng.choice(["light", "medium", "heavy"])},
+            "workload": {"rate_qps": rng.choice([50, 200, 800, 2500]) * gpus, "duration_ms": rng.choice([300, 800]),
+                         "seeds": [rng.randint(1, 10**6), rng.randint(1, 10**6)], "sigma": rng.choice([0.5, 1.0, 1.5])},
+            "server": {"num_gpus": gpus},
+            "sla": {"multiplier": rng.choice([1.0, 1.5, 3.0]), "alpha": rng.choice([1.0, 0.8, 1.3]),
+                    "beta": rng.choice([1.0, 0.5, 2.0])},
+            "engine": {"noise_sigma": rng.choice([0.05, 0.3, 1.0]), "noise_seed": rng.randint(0, 10**6),
+                       "warmup_fraction": rng.choice([0.0, 0.1, 0.5])},
+            "designs": [{"plan": plan, "scheduler": "elsa", "segment_routing": rng.random() < 0.3},
+                        {"plan": plan, "scheduler": "fifs", "label": "fifs-design"}],
+        }
+        d = tmp_path / f"c{case}"
+        d.mkdir()
+        _both(d, "run", write_cfg(d, cfg))
