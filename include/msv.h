@@ -273,6 +273,10 @@ int msv_synth_profile(double work_per_sample, double fixed_overhead, double para
                       int32_t* sizes_out, double* latency_ms, double* utilization);
 /* lognormal_batch_pdf(mu, sigma, b_max) (workload.hpp:81-93): pmf and cdf. */
 int msv_lognormal_pdf(double mu, double sigma, int b_max, double* pmf, double* cdf);
+/* Execution-noise multipliers (engine.hpp:140-145): out[j] = exp(sigma*z_j - 0.5*sigma*sigma),
+ * z_j the j-th Rng(seed).normal() (rng.hpp:14-31: mt19937_64, Box-Muller, this host's libm),
+ * the input stream of msv_run_noise. */
+int msv_noise_multipliers(uint64_t seed, double sigma, int64_t n, double* out);
 
 #ifdef __cplusplus
 }

@@ -140,10 +140,11 @@ int64_t ora_sample_trace(const ora_dist* d, double rate_qps, double duration_ms,
     }
 }
 
-int ora_run(const ora_plan* plan_in, int scheduler, const double* arrival, const int32_t* batch, int64_t n,
-            double duration_ms, const ora_profile* prof, double sla, double alpha, double beta,
-            double warmup_fraction, int check_wait, int n_route, const int32_t* route_k, const int32_t* route_first,
-            const int32_t* route_last, ora_records* rec, ora_report* rep) {
+static int run_impl(const ora_plan* plan_in, int scheduler, const double* arrival, const int32_t* batch, int64_t n,
+                    double duration_ms, const ora_profile* prof, double sla, double alpha, double beta,
+                    double warmup_fraction, int check_wait, int n_route, const int32_t* route_k,
+                    const int32_t* route_first, const int32_t* route_last, ora_records* rec, ora_report* rep,
+                    double noise_sigma, uint64_t noise_seed) {
     try {
         PartitionPlan plan = make_plan(plan_in);
         ProfileTable table = make_table(prof);
@@ -153,6 +154,8 @@ int ora_run(const ora_plan* plan_in, int scheduler, const double* arrival, const
         EngineOptions opt;
         opt.warmup_fraction = warmup_fraction;
         opt.check_wait_consistency = check_wait != 0;
+        opt.noise_sigma = noise_sigma;
+        opt.noise_seed = noise_seed;
         if (n_route > 0) {
             opt.segment_routing = true;
             for (int j = 0; j < n_route; ++j)
@@ -189,6 +192,24 @@ int ora_run(const ora_plan* plan_in, int scheduler, const double* arrival, const
     } catch (...) {
         return code_of_current_exception();
     }
+}
+
+int ora_run(const ora_plan* plan_in, int scheduler, const double* arrival, const int32_t* batch, int64_t n,
+            double duration_ms, const ora_profile* prof, double sla, double alpha, double beta,
+            double warmup_fraction, int check_wait, int n_route, const int32_t* route_k, const int32_t* route_first,
+            const int32_t* route_last, ora_records* rec, ora_report* rep) {
+    return run_impl(plan_in, scheduler, arrival, batch, n, duration_ms, prof, sla, alpha, beta, warmup_fraction,
+                    check_wait, n_route, route_k, route_first, route_last, rec, rep, 0.0, 1);
+}
+
+// run() with EngineOptions::noise_sigma / noise_seed (engine.hpp:140-145): the reference only.
+int oraref_run_noise(const ora_plan* plan_in, int scheduler, const double* arrival, const int32_t* batch, int64_t n,
+                     double duration_ms, const ora_profile* prof, double sla, double alpha, double beta,
+                     double warmup_fraction, int n_route, const int32_t* route_k, const int32_t* route_first,
+                     const int32_t* route_last, double noise_sigma, uint64_t noise_seed, ora_records* rec,
+                     ora_report* rep) {
+    return run_impl(plan_in, scheduler, arrival, batch, n, duration_ms, prof, sla, alpha, beta, warmup_fraction, 0,
+                    n_route, route_k, route_first, route_last, rec, rep, noise_sigma, noise_seed);
 }
 
 int ora_tail_latency(const double* samples, int64_t n, double p, double* out) {

@@ -1,12 +1,14 @@
 // C ABI exports of the host-side planning headers (include/migserve/paris.hpp),
 // for bindings that cannot include C++ headers (the Python package, bench.py).
 #include <algorithm>
+#include <cmath>
 #include <exception>
 #include <map>
 #include <string>
 #include <vector>
 
 #include "../../include/migserve/paris.hpp"
+#include "../../include/migserve/rng.hpp"
 #include "../../include/msv.h"
 
 namespace migserve_capi {
@@ -93,4 +95,16 @@ extern "C" int msv_lognormal_pdf(double mu, double sigma, int b_max, double* pmf
     } catch (...) {
         return map_exception();
     }
+}
+
+// The noise multiplier stream of run() (engine.hpp:140-145), drawn with the reference's
+// Rng (rng.hpp) and this host's libm exp/log/cos/sqrt (the reference's own calls).
+extern "C" int msv_noise_multipliers(uint64_t seed, double sigma, int64_t n, double* out) {
+    if (n < 0 || (n > 0 && !out)) return migserve_capi::set_error(MSV_PARAM, "noise_multipliers: bad arguments");
+    migserve::Rng rng(seed);
+    for (int64_t j = 0; j < n; ++j) {
+        const double z = rng.normal();
+        out[j] = std::exp(sigma * z - 0.5 * sigma * sigma);
+    }
+    return MSV_OK;
 }

@@ -422,10 +422,53 @@ class Engine:
 
     def run(self, plan: PartitionPlan, scheduler: str, arrival, batch, duration_ms: float, table: ProfileTable,
             sla: SlaConfig, warmup_fraction: float = 0.1, routing=None, check_wait: bool = False,
-            tail_p: Sequence[float] = ()) -> dict:
-        """run() (engine.hpp:115-253) on one host trace, with per-query records."""
+            tail_p: Sequence[float] = (), noise_sigma: float = 0.0, noise_seed: int = 1) -> dict:
+        """run() (engine.hpp:115-253) on one host trace, with per-query records;
+        noise_sigma > 0: execution noise (engine.hpp:140-145) on K5 (msv_run_noise)."""
+        if noise_sigma > 0.0:
+            return self._run_noise(plan, scheduler, arrival, batch, duration_ms, table, sla, warmup_fraction, routing,
+                                   tail_p, noise_sigma, noise_seed)
         return self.run_many([(plan, scheduler, arrival, batch, duration_ms, table, sla, warmup_fraction, routing,
                                check_wait)], tail_p)[0]
+
+    def _run_noise(self, plan, scheduler, arrival, batch, duration_ms, table, sla, warmup_fraction, routing, tail_p,
+                   noise_sigma, noise_seed) -> dict:
+        arrival, batch = _arr(arrival, np.float64), _arr(batch, np.int32)
+        n = len(arrival)
+        # the reference's heap serves arrivals by (time, trace index): a stable sort
+        order = np.argsort(arrival, kind="stable")
+        arr_s, bat_s = np.ascontiguousarray(arrival[order]), np.ascontiguousarray(batch[order])
+        spec = GridSpec(plan, table, _REPLAY_DIST, sla, 1.0, duration_ms, 0, scheduler, warmup_fraction, routing, False)
+        sc = self.scenarios([spec])
+        mult = np.zeros(max(n, 1))
+        check(self._lib.msv_noise_multipliers(int(noise_seed), float(noise_sigma), n, _ptr(mult, C.c_double)),
+              "noise_multipliers")
+        P = plan.total_instances()
+        res = (N.Result * 1)()
+        use = (N.Usage * max(P, 1))()
+        rec = (N.Record * max(n, 1))()
+        a = arr_s if n else np.zeros(1)
+        b = bat_s if n else np.zeros(1, np.int32)
+        check(self._lib.msv_run_noise(self._h, sc, n, _ptr(a, C.c_double), _ptr(b, C.c_int32),
+                                      _ptr(mult, C.c_double), res, use, rec), "run")
+        agg = results_to_numpy(res, 1, 0, use, P)
+        r = {k: v[0] for k, v in agg.items() if k not in ("usage", "tail")}
+        rr = np.ctypeslib.as_array(rec)[:n] if n else np.zeros(0, rec._type_)
+        inv = np.empty(n, np.int64)
+        inv[order] = np.arange(n)
+        r["partition"] = np.array(rr["partition"], np.int32)[inv]
+        r["start_ms"] = np.array(rr["start_ms"])[inv]
+        r["finish_ms"] = np.array(rr["finish_ms"])[inv]
+        r["kind"] = np.array(rr["kind"], np.int32)[inv]
+        r["busy_ms"] = agg["usage"]["busy_ms"]
+        r["weighted_busy_ms"] = agg["usage"]["weighted_busy_ms"]
+        r["queries"] = agg["usage"]["queries"]
+        if tail_p:
+            lat = r["finish_ms"] - arrival
+            meas = lat[arrival >= r["warmup_ms"]]
+            r["tail"] = (np.array(self.tail_latency(meas, list(tail_p)), dtype=np.float64) if len(meas)
+                         else np.full(len(tail_p), np.nan))
+        return r
 
     def run_many(self, items, tail_p: Sequence[float] = ()) -> list[dict]:
         specs, arrs, bats = [], [], []

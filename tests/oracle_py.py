@@ -166,6 +166,36 @@ class Oracle:
                 "warmup_ms": rep.warmup_ms, "max_wait_estimate_diff": rep.max_wait_estimate_diff,
                 "busy_ms": busy[:P], "weighted_busy_ms": wbusy[:P], "queries": nq[:P]}
 
+    def run_noise(self, plan, scheduler, arrival, batch, duration, table, sla, warmup, routing, sigma, seed):
+        """The reference's run() with execution noise (oracle/_ref only: oraref_run_noise)."""
+        arrival, batch = _a(arrival, np.float64), _a(batch, np.int32)
+        n, P = len(arrival), plan.total_instances()
+        m = max(n, 1)
+        part, start, fin, kind = np.zeros(m, np.int32), np.zeros(m), np.zeros(m), np.zeros(m, np.int32)
+        busy, wbusy, nq = np.zeros(max(P, 1)), np.zeros(max(P, 1)), np.zeros(max(P, 1), np.int64)
+        rec = OraRecords(_p(part, C.c_int32), _p(start, C.c_double), _p(fin, C.c_double), _p(kind, C.c_int32))
+        rep = OraReport(0, 0, 0, 0, 0.0, 0.0, 0.0, _p(busy, C.c_double), _p(wbusy, C.c_double), _p(nq, C.c_int64))
+        if routing is None:
+            nr, rk, rf, rl = -1, None, None, None
+        else:
+            nr = len(routing)
+            rk, rf, rl = (_a([s[i] for s in routing], np.int32) for i in range(3))
+            self._keep += [rk, rf, rl]
+            rk, rf, rl = _p(rk, C.c_int32), _p(rf, C.c_int32), _p(rl, C.c_int32)
+        fn = self.L.oraref_run_noise
+        fn.argtypes = None
+        rc = fn(C.byref(self.plan(plan)), C.c_int(1 if scheduler == "elsa" else 0),
+                _p(arrival if n else np.zeros(1), C.c_double), _p(batch if n else np.zeros(1, np.int32), C.c_int32),
+                C.c_int64(n), C.c_double(duration), C.byref(self.profile(table)), C.c_double(sla.sla_target_ms),
+                C.c_double(sla.alpha), C.c_double(sla.beta), C.c_double(warmup), C.c_int(nr), rk, rf, rl,
+                C.c_double(sigma), C.c_uint64(seed), C.byref(rec), C.byref(rep))
+        if rc:
+            raise self.err(rc)
+        return {"partition": part[:n], "start_ms": start[:n], "finish_ms": fin[:n], "kind": kind[:n],
+                "total": rep.total, "violations": rep.violations, "measured": rep.measured,
+                "measured_violations": rep.measured_violations, "horizon_ms": rep.horizon_ms,
+                "warmup_ms": rep.warmup_ms, "busy_ms": busy[:P], "weighted_busy_ms": wbusy[:P], "queries": nq[:P]}
+
     def tail_latency(self, samples, p):
         s = _a(samples, np.float64)
         out = C.c_double()

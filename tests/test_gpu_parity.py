@@ -564,3 +564,37 @@ def test_query_csv_and_report_json_byte_identical():
     got = subprocess.run([str(dev_exe)], capture_output=True, timeout=600, check=True).stdout
     assert want.count(b"# case") == 36 and len(want) > 1_000_000
     assert got == want
+
+
+# ---------------------------------------------------------------- execution noise (K5)
+def test_run_noise_bit_exact_python_api(eng, ref):
+    """Engine.run(noise_sigma > 0) (K5, msv_run_noise) against the reference's run() with
+    EngineOptions::noise_sigma / noise_seed (engine.hpp:140-145): records, usage, totals equal."""
+    if ref.kind != "reference":
+        pytest.skip("noise parity needs oracle/_ref (the C port has no noise path)")
+    rng = np.random.default_rng(7)
+    cases = _small_cases()
+    for m, gpus in (("mobilenet", 8), ("bert_base", 8), ("resnet50", 1), ("mobilenet", 9)):
+        mod = W.model(m)
+        plan = W.paris(mod, gpus) if gpus <= 8 else homogeneous_plan(1, 63, 9, 7)
+        rate = 0.9 * W.capacity_qps(mod, plan)
+        cases.append((m, mod.table, mod.dist, plan, "elsa", rate, 800.0, 3, mod.sla, None))
+        cases.append((m, mod.table, mod.dist, plan, "fifs", 1.3 * rate, 800.0, 4, mod.sla, None))
+    for name, table, dist, plan, sched, rate, duration, seed, sla, routing in cases:
+        arr, bat = ref.sample_trace(dist, rate, duration, seed)
+        sigma = float(rng.choice([0.05, 0.3, 0.8]))
+        nseed = int(rng.integers(0, 2**63))
+        warm = float(rng.choice([0.0, 0.1, 0.4]))
+        got = eng.run(plan, sched, arr, bat, duration, table, sla, warm, routing, tail_p=(0.95,),
+                      noise_sigma=sigma, noise_seed=nseed)
+        want = ref.run_noise(plan, sched, arr, bat, duration, table, sla, warm, routing, sigma, nseed)
+        for k in ("partition", "kind", "start_ms", "finish_ms", "busy_ms", "weighted_busy_ms", "queries"):
+            assert same(got[k], want[k]), (name, k, np.nonzero(np.asarray(got[k]) != np.asarray(want[k]))[0][:5])
+        for k in ("total", "violations", "measured", "measured_violations", "horizon_ms", "warmup_ms"):
+            assert got[k] == want[k], (name, k, got[k], want[k])
+        lat = want["finish_ms"] - arr
+        meas = lat[arr >= want["warmup_ms"]]
+        if len(meas):
+            assert got["tail"][0] == ref.tail_latency(meas, 0.95)
+        exact = eng.run(plan, sched, arr, bat, duration, table, sla, warm, routing)
+        assert len(arr) < 2 or not same(exact["finish_ms"], got["finish_ms"])  # the noise does something
