@@ -94,3 +94,42 @@ def paris_argmin(p99: np.ndarray, n_candidates: int, seeds_per_candidate: int) -
         if means[c] < means[best]:
             best = c
     return best, means
+
+
+def design_bounds(n: int, world: int) -> list[tuple[int, int]]:
+    """[lo, hi) contiguous design shards, sizes differing by at most one."""
+    base, extra = divmod(n, world)
+    out, lo = [], 0
+    for r in range(world):
+        hi = lo + base + (1 if r < extra else 0)
+        out.append((lo, hi))
+        lo = hi
+    return out
+
+
+def lbt_sharded(designs: Sequence, search_local: Callable[[list], list], rank: int, world: int,
+                device=None) -> list[tuple[float, bool, int]]:
+    """latency_bounded_throughput (metrics.hpp:81-120) of many designs over `world` ranks
+    (SURVEY §8e): each design's whole search — every seed of every probed rate — stays on
+    one rank, so the lockstep rounds need no collective; one all-gather of (qps,
+    infeasible_at_min, sims_run) at the end gives every rank every design's result, in
+    design order. `search_local(designs) -> [(qps, infeasible, sims), ...]` is e.g.
+    `search.latency_bounded_throughput(eng, ds)` mapped to tuples."""
+    bounds = design_bounds(len(designs), world)
+    lo, hi = bounds[rank]
+    local = [tuple(r) for r in search_local(list(designs[lo:hi]))] if hi > lo else []
+    if world == 1:
+        return [(float(q), bool(i), int(n)) for q, i, n in local]
+    import torch
+    import torch.distributed as td
+    width = max(1, max(h - l for l, h in bounds))
+    buf = np.full((width, 3), np.nan)
+    for j, (q, inf, n) in enumerate(local):
+        buf[j] = (q, 1.0 if inf else 0.0, n)
+    t = torch.from_numpy(buf)
+    if device is not None:
+        t = t.to(device)
+    parts = [torch.empty_like(t) for _ in range(world)]
+    td.all_gather(parts, t)
+    rows = np.concatenate([p.cpu().numpy()[: h - l] for p, (l, h) in zip(parts, bounds)])
+    return [(float(r[0]), bool(r[1]), int(r[2])) for r in rows]

@@ -12,6 +12,11 @@ import pytest
 import torch.multiprocessing as mp
 
 
+def O_REF_EXISTS() -> bool:
+    from tests import oracle_py as O
+    return O.REF_LIB.exists()
+
+
 def _free_port() -> int:
     s = socket.socket()
     s.bind(("127.0.0.1", 0))
@@ -79,3 +84,51 @@ def test_paris_argmin_ties_and_empty_seeds():
     p99 = np.array([3.0, 3.0, 2.0, np.nan, 2.0, 2.0, 1.5, 2.5, 2.0])
     best, means = paris_argmin(p99, 3, 3)
     assert means[1] == 2.0 and means[2] == 2.0 and best == 1
+
+
+def _lbt_designs():
+    from paper_2202_13481_b200 import workloads as W
+    from paper_2202_13481_b200.search import Design, LbtOptions
+    m = W.model("resnet50")
+    opt = LbtOptions(duration_ms=1500.0, seeds=(1, 2), rel_tol=0.05)
+    out = []
+    for p in W.fleet_candidates(1)[:5]:
+        for sched in ("elsa", "fifs"):
+            out.append(Design(p, sched, m.table, m.dist, m.sla, opt))
+    return out
+
+
+def _lbt_worker(rank, world, port, out_q):
+    import torch.distributed as td
+    from paper_2202_13481_b200.distributed import lbt_sharded
+    from tests import oracle_py as O
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    td.init_process_group("gloo", rank=rank, world_size=world)
+    ref = O.Oracle("reference")
+    designs = _lbt_designs()
+    res = lbt_sharded(designs, lambda ds: [ref.lbt(d.plan, d.scheduler, d.table, d.sla, d.dist, d.opt) for d in ds],
+                      rank, world)
+    out_q.put((rank, res))
+    td.barrier()
+    td.destroy_process_group()
+
+
+@pytest.mark.skipif(not O_REF_EXISTS(), reason="oracle/_ref not built")
+def test_lbt_sharded_matches_single_process():
+    """Rank-local LBT searches (3 ranks, 10 designs: uneven shards) + one all-gather give every
+    rank the single-process results in design order."""
+    from tests import oracle_py as O
+    ref = O.Oracle("reference")
+    want = [ref.lbt(d.plan, d.scheduler, d.table, d.sla, d.dist, d.opt) for d in _lbt_designs()]
+    world = 3
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_lbt_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    got = dict(q.get(timeout=600) for _ in range(world))
+    for p in procs:
+        p.join(timeout=120)
+    for r in range(world):
+        assert got[r] == [(float(a), bool(b), int(c)) for a, b, c in want], r
