@@ -1798,6 +1798,7 @@ int msv_run_noise(msv_ctx* ctx, const msv_scenario* scenario, int64_t n, const d
     np.lat = d_lat.as<double>();
     np.util = d_util.as<double>();
     np.parts = d_parts.as<DevPart>();
+    np.n_cells = (int32_t)prof.lat.size();
     np.route_mask = masks.empty() ? nullptr : d_masks.as<uint64_t>();
     np.P = P;
     np.b_max = prof.b_max;

@@ -176,7 +176,7 @@ struct NoiseParams {
     const double* util;
     const DevPart* parts;       // P entries in (k, id) order; row relative to lat, -1 = size missing
     const uint64_t* route_mask; // P masks or null
-    int32_t P, b_max, sched, pad;
+    int32_t P, b_max, sched, n_cells;  // n_cells: entries of lat (and util)
     double sla, alpha, beta, warmup_ms;
     uint32_t* next;             // n: FIFO links through query indices
     msv_record* records;        // n

@@ -28,16 +28,36 @@ namespace msv {
 namespace {
 
 constexpr int kNoiseSlots = 2;  // P <= 64
+constexpr int kRing = 64;       // queued estimates per slot cached in shared memory (ELSA)
 
 __global__ void __launch_bounds__(32, 1) sim_noise_kernel(const NoiseParams p) {
     constexpr int S = kNoiseSlots;
     const int lane = threadIdx.x & 31;
     const double* __restrict__ arr = p.arrival;
     const int32_t* __restrict__ bat = p.batch;
-    const double* __restrict__ lat = p.lat;
+    // the profile's latency / utilisation cells in shared memory (per-query lookups)
+    extern __shared__ double s_tab[];
+    for (int c = lane; c < p.n_cells; c += 32) {
+        s_tab[c] = p.lat[c];
+        s_tab[p.n_cells + c] = p.util[c];
+    }
+    __syncwarp();
+    const double* lat = s_tab;
+    const double* util = s_tab + p.n_cells;
     const int64_t n = p.n;
     const double sla = p.sla, alpha = p.alpha, beta = p.beta, warmup = p.warmup_ms;
     const bool route = p.route_mask != nullptr;
+    const bool elsa = p.sched == MSV_ELSA;  // Eq. 1's fold is needed by ELSA only
+    // The first kRing queued estimates of each slot in FIFO order (a ring at rh[s]); the
+    // rest of a longer queue is walked through the query list from rq[s] (queue item kRing).
+    __shared__ double ring[S][kRing][32];
+    int rh[S];
+    int64_t rq[S];
+    // multipliers j in [mj, mj + 32) staged in shared memory; refilled at warp-uniform points
+    __shared__ double mw[32];
+    int64_t mj = -64;
+    double c_arr[S];  // arrival of each slot's running query
+    int32_t c_b[S];   // and its batch
 
     bool act[S], busy[S];
     int32_t row[S], pid[S], kk[S];
@@ -62,19 +82,33 @@ __global__ void __launch_bounds__(32, 1) sim_noise_kernel(const NoiseParams p) {
         c_seq[s] = 0;
         cq[s] = -1;
         nq[s] = 0;
+        rh[s] = 0;
+        rq[s] = -1;
+        c_arr[s] = 0.0;
+        c_b[s] = 1;
     }
     uint64_t seq = (uint64_t)n;  // arrivals hold seq 0..n-1 (engine.hpp:136-137)
     int64_t j = 0;               // next noise multiplier
+    auto stage_mult = [&]() {
+        if (j >= mj + 32) {
+            mj = j;
+            __syncwarp();
+            mw[lane] = mj + lane < n ? p.mult[mj + lane] : 1.0;
+            __syncwarp();
+        }
+    };
     int64_t viol = 0, meas = 0, mviol = 0;
     uint64_t hash = 0;
     double last_finish = 0.0;
     int status = 0;
 
-    // Exact left fold of slot s's FIFO (sched.hpp:78-79).
+    // Exact left fold of slot s's FIFO (sched.hpp:78-79): the cached ring, then the list.
     auto refold = [&](int s) {
         double acc = 0.0;
-        int64_t q = qh[s];
-        for (int64_t i = 0; i < qn[s]; ++i) {
+        const int nr = qn[s] < kRing ? (int)qn[s] : kRing;
+        for (int k = 0; k < nr; ++k) acc = acc + ring[s][(rh[s] + k) & (kRing - 1)][lane];
+        int64_t q = rq[s];
+        for (int64_t i = kRing; i < qn[s]; ++i) {
             acc = acc + lat[row[s] + bat[q] - 1];
             q = p.next[q];
         }
@@ -84,6 +118,11 @@ __global__ void __launch_bounds__(32, 1) sim_noise_kernel(const NoiseParams p) {
     // Retire, in global (time, seq) order, every completion with time <= t.
     auto drain = [&](double t) {
         for (;;) {
+            bool due = false;
+#pragma unroll
+            for (int s = 0; s < S; ++s) due |= busy[s] && c_comp[s] <= t;
+            if (!__any_sync(kFull, due)) return;  // nothing due by t
+            stage_mult();
             double bt = CUDART_INF;
             uint64_t bs = ~0ull;
             int bsl = -1;
@@ -114,12 +153,12 @@ __global__ void __launch_bounds__(32, 1) sim_noise_kernel(const NoiseParams p) {
                     if (s != bsl) continue;
                     const double now = c_comp[s];  // engine.hpp:167-187
                     const int64_t q = cq[s];
-                    const double a = arr[q];
+                    const double a = c_arr[s];
                     const double l = now - a;
                     const bool met = l <= sla;
                     const double ran = now - c_start[s];
                     bms[s] = bms[s] + ran;
-                    wbms[s] = wbms[s] + ran * p.util[row[s] + bat[q] - 1];
+                    wbms[s] = wbms[s] + ran * util[row[s] + c_b[s] - 1];
                     nq[s] += 1;
                     viol += met ? 0 : 1;
                     if (a >= warmup) {
@@ -132,16 +171,27 @@ __global__ void __launch_bounds__(32, 1) sim_noise_kernel(const NoiseParams p) {
                     if (qn[s] > 0) {  // start the queue head now (engine.hpp:181-185)
                         const int64_t h = qh[s];
                         qh[s] = p.next[h];
+                        if (elsa) {  // the ring drops its head and takes queue item kRing
+                            const int vac = rh[s];
+                            rh[s] = (vac + 1) & (kRing - 1);
+                            if (qn[s] > kRing) {
+                                ring[s][vac][lane] = lat[row[s] + bat[rq[s]] - 1];
+                                if (qn[s] > kRing + 1) rq[s] = p.next[rq[s]];
+                            }
+                        }
                         qn[s] -= 1;
                         if (qn[s] == 0) qt[s] = -1;
-                        const double est = lat[row[s] + bat[h] - 1];
+                        const int32_t hb = bat[h];
+                        c_arr[s] = arr[h];
+                        c_b[s] = hb;
+                        const double est = lat[row[s] + hb - 1];
                         c_start[s] = now;
                         c_est[s] = est;
-                        c_comp[s] = now + est * p.mult[j];
+                        c_comp[s] = now + est * mw[j - mj];
                         c_seq[s] = seq;
                         cq[s] = h;
                         p.records[h].start_ms = now;
-                        fold[s] = refold(s);
+                        if (elsa) fold[s] = refold(s);
                         started = 1;
                     } else {
                         busy[s] = false;
@@ -156,10 +206,21 @@ __global__ void __launch_bounds__(32, 1) sim_noise_kernel(const NoiseParams p) {
         }
     };
 
+    double w_t = lane < n ? arr[lane] : 0.0;  // arrivals [i & ~31, +32) one per lane
+    int32_t w_b = lane < n ? bat[lane] : 0;
+    double nx_t = 32 + lane < n ? arr[32 + lane] : 0.0;  // and the next window
+    int32_t nx_b = 32 + lane < n ? bat[32 + lane] : 0;
     for (int64_t i = 0; i < n && status == 0; ++i) {
-        const double t = arr[i];
+        if (i > 0 && (i & 31) == 0) {
+            w_t = nx_t;
+            w_b = nx_b;
+            nx_t = i + 32 + lane < n ? arr[i + 32 + lane] : 0.0;
+            nx_b = i + 32 + lane < n ? bat[i + 32 + lane] : 0;
+        }
+        const double t = __shfl_sync(kFull, w_t, (int)(i & 31));
+        const int b = __shfl_sync(kFull, w_b, (int)(i & 31));
         drain(t);  // completions at <= t precede the arrival (engine.hpp:101-107)
-        const int b = bat[i];
+        stage_mult();
         if (b < 1 || b > p.b_max) {  // every lookup of this query fails (profile.hpp:123-132)
             status = MSV_LOOKUP;
             break;
@@ -301,6 +362,10 @@ __global__ void __launch_bounds__(32, 1) sim_noise_kernel(const NoiseParams p) {
                 p.records[i].partition = pid[s];
                 p.records[i].kind = kind;
                 if (busy[s]) {
+                    if (elsa) {
+                        if (qn[s] < kRing) ring[s][(rh[s] + (int)qn[s]) & (kRing - 1)][lane] = est;
+                        else if (qn[s] == kRing) rq[s] = i;
+                    }
                     if (qn[s] == 0) {
                         qh[s] = i;
                     } else {
@@ -313,9 +378,11 @@ __global__ void __launch_bounds__(32, 1) sim_noise_kernel(const NoiseParams p) {
                     busy[s] = true;
                     c_start[s] = t;
                     c_est[s] = est;
-                    c_comp[s] = t + est * p.mult[j];
+                    c_comp[s] = t + est * mw[j - mj];
                     c_seq[s] = seq;
                     cq[s] = i;
+                    c_arr[s] = t;
+                    c_b[s] = b;
                     fold[s] = 0.0;
                     p.records[i].start_ms = t;
                     started = 1;
@@ -363,7 +430,13 @@ __global__ void __launch_bounds__(32, 1) sim_noise_kernel(const NoiseParams p) {
 }  // namespace
 
 cudaError_t launch_noise(const NoiseParams& p, cudaStream_t stream) {
-    sim_noise_kernel<<<1, 32, 0, stream>>>(p);
+    const size_t smem = (size_t)2 * p.n_cells * sizeof(double);
+    if (smem > 48 * 1024) {
+        const cudaError_t e =
+            cudaFuncSetAttribute(sim_noise_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+    }
+    sim_noise_kernel<<<1, 32, smem, stream>>>(p);
     return cudaGetLastError();
 }
 

@@ -598,3 +598,32 @@ def test_run_noise_bit_exact_python_api(eng, ref):
             assert got["tail"][0] == ref.tail_latency(meas, 0.95)
         exact = eng.run(plan, sched, arr, bat, duration, table, sla, warm, routing)
         assert len(arr) < 2 or not same(exact["finish_ms"], got["finish_ms"])  # the noise does something
+
+
+def test_run_noise_long_queues(eng, ref):
+    """K5 under overload: ELSA queues far longer than the shared-memory ring of queued
+    estimates (msv_noise.cu kRing = 64), so the Eq. 1 refold walks the ring and then the query
+    list; records, usage and totals equal the reference's run() with noise (engine.hpp:140-145)."""
+    if ref.kind != "reference":
+        pytest.skip("noise parity needs oracle/_ref (the C port has no noise path)")
+    for m, gpus, load, q in (("bert_base", 8, 2.5, 8000), ("resnet50", 1, 3.0, 3000), ("mobilenet", 8, 2.5, 10000)):
+        mod = W.model(m)
+        plan = W.paris(mod, gpus)
+        rate = load * W.capacity_qps(mod, plan)
+        duration = q / rate * 1000.0
+        arr, bat = ref.sample_trace(mod.dist, rate, duration, 17)
+        for sigma, nseed in ((0.2, 3), (0.6, 99)):
+            got = eng.run(plan, "elsa", arr, bat, duration, mod.table, mod.sla, 0.1, None, tail_p=(0.99,),
+                          noise_sigma=sigma, noise_seed=nseed)
+            want = ref.run_noise(plan, "elsa", arr, bat, duration, mod.table, mod.sla, 0.1, None, sigma, nseed)
+            for k in ("partition", "kind", "start_ms", "finish_ms", "busy_ms", "weighted_busy_ms", "queries"):
+                assert same(got[k], want[k]), (m, k)
+            for k in ("total", "violations", "measured", "measured_violations", "horizon_ms"):
+                assert got[k] == want[k], (m, k, got[k], want[k])
+        # the queues did outgrow the ring: some query arrived behind > 64 queued on its partition
+        part, start = np.asarray(want["partition"]), np.asarray(want["start_ms"])
+        depth = 0
+        for pid in np.unique(part):
+            a, st = arr[part == pid], start[part == pid]
+            depth = max(depth, int(np.tril(st[None, :] > a[:, None], -1).sum(axis=1).max()))
+        assert depth > 64, (m, depth)
