@@ -121,7 +121,8 @@ __global__ void __launch_bounds__(32, 1) sim_noise_kernel(const NoiseParams p) {
             bool due = false;
 #pragma unroll
             for (int s = 0; s < S; ++s) due |= busy[s] && c_comp[s] <= t;
-            if (!__any_sync(kFull, due)) return;  // nothing due by t
+            const unsigned dm = __ballot_sync(kFull, due);
+            if (dm == 0) return;  // nothing due by t
             stage_mult();
             double bt = CUDART_INF;
             uint64_t bs = ~0ull;
@@ -134,15 +135,19 @@ __global__ void __launch_bounds__(32, 1) sim_noise_kernel(const NoiseParams p) {
                     bsl = s;
                 }
             int bl = bsl >= 0 ? lane : 32;
+            if (__popc(dm) == 1) {
+                bl = __ffs(dm) - 1;  // one lane has due completions: its own minimum is the global one
+            } else {
 #pragma unroll
-            for (int off = 16; off > 0; off >>= 1) {
-                const double ot = __shfl_xor_sync(kFull, bt, off);
-                const uint64_t os = __shfl_xor_sync(kFull, bs, off);
-                const int ol = __shfl_xor_sync(kFull, bl, off);
-                if (ot < bt || (ot == bt && os < bs)) {
-                    bt = ot;
-                    bs = os;
-                    bl = ol;
+                for (int off = 16; off > 0; off >>= 1) {
+                    const double ot = __shfl_xor_sync(kFull, bt, off);
+                    const uint64_t os = __shfl_xor_sync(kFull, bs, off);
+                    const int ol = __shfl_xor_sync(kFull, bl, off);
+                    if (ot < bt || (ot == bt && os < bs)) {
+                        bt = ot;
+                        bs = os;
+                        bl = ol;
+                    }
                 }
             }
             if (bl == 32) return;  // nothing due by t

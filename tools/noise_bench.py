@@ -41,8 +41,13 @@ for m, gpus, sched, load, sigma in (("bert_base", 8, "elsa", 0.5, 0.1), ("bert_b
         ok = all(np.array_equal(np.asarray(got[k]), np.asarray(want[k]))
                  for k in ("partition", "kind", "start_ms", "finish_ms", "busy_ms", "queries"))
         n = len(arr)
+        import ctypes as C
+        mult = np.zeros(n)
+        t0 = time.perf_counter()
+        eng._lib.msv_noise_multipliers(5, float(sigma), n, mult.ctypes.data_as(C.POINTER(C.c_double)))
+        mt = time.perf_counter() - t0
         row = dict(model=m, gpus=gpus, partitions=plan.total_instances(), sched=sched, load=load,
-                   sigma=sigma, queries=n, device_ms=round(dt * 1e3, 2), reference_1core_ms=round(ct * 1e3, 2),
+                   sigma=sigma, queries=n, device_ms=round(dt * 1e3, 2), host_multiplier_draw_ms=round(mt * 1e3, 2), reference_1core_ms=round(ct * 1e3, 2),
                    device_qps=round(n / dt), reference_qps=round(n / ct), speedup=round(ct / dt, 1),
                    records_identical=ok)
         rows.append(row)
