@@ -1,20 +1,27 @@
 #!/usr/bin/env python3
 """Benchmark: simulated queries/s over the PARIS x ELSA scenario grid.
 
-Workload (BASELINE.json configs[1], "C2"): BERT-base preset profile, the 8-GPU
-PARIS plan (23 partitions), ELSA, Poisson arrivals at 10%..100% of the plan's
-nominal peak QPS, `--seeds` seeds per load, `--queries` expected queries per
-scenario, lognormal(1,1) batches over 1..32, SLA = 1.5 x latency(7g, 32).
-One step = the whole grid: device trace generation (sample_trace), simulation
-(run), exact p95/p99 selection (tail_latency). Per rank: its own seeds (weak
-scaling); no data-path collective — one NCCL all-gather of the per-scenario
-results feeds the cross-rank summary.
+Workload (BASELINE.json configs[4], "C5" — the grid the metric names): 10^4 scenarios
+x 10^6 expected queries. 75 cells = 3 model presets (MobileNet / ResNet-50 / BERT-base)
+x 5 plans (the model's 8-GPU PARIS plan and homogeneous 1g/2g/3g/7g fleets of 56
+GPCs: 8..56 partitions) x 5 loads (30..90 % of the plan's nominal capacity), ELSA,
+lognormal(1,1) batches over 1..32, SLA = 1.5 x latency(7g, 32); scenario i = cell
+i mod 75 with seed 1 + i // 75. One step = the whole grid: device trace generation
+(sample_trace), simulation (run), exact p95/p99 selection (tail_latency).
+
+N > 1 GPUs (torchrun, one process per GPU): strong scaling — the same grid is cut
+into cost-balanced contiguous shards (distributed.shard_bounds), each rank simulates
+its shard with no data-path collective; the end-to-end leg then all-gathers the
+fixed-size per-scenario results (NCCL) and every rank takes the PARIS argmin (best plan
+per model and load by mean p99).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--workload c5|c2] [--scenarios S] [--queries Q]
 """
 from __future__ import annotations
 
 import argparse
+import hashlib
 import json
 import os
 import subprocess
@@ -30,7 +37,8 @@ sys.path.insert(0, str(ROOT))
 
 METRIC = "simulated queries/sec over PARIS×ELSA scenario grid at 1/2/4/8 B200 vs CPU"
 UNIT = "queries/s"
-SIM_BYTES_PER_QUERY = 20  # arrival f64 + batch i32 read, measured latency f64 written (DESIGN.md)
+SIM_BYTES_PER_QUERY = 20  # arrival f64 + batch i32 read, measured latency f64 written (DESIGN.md §4)
+TAILS = (0.95, 0.99)
 
 
 def parse():
@@ -39,30 +47,46 @@ def parse():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--seeds", type=int, default=1024, help="seeds per load level per rank")
-    ap.add_argument("--queries", type=float, default=1e5, help="expected queries per scenario")
-    ap.add_argument("--cpu-seconds", type=float, default=15.0, help="CPU baseline sample budget")
+    ap.add_argument("--workload", default="c5", choices=["c5", "c2"])
+    ap.add_argument("--scenarios", type=int, default=10_000, help="C5: scenarios in the grid")
+    ap.add_argument("--seeds", type=int, default=1024, help="C2: seeds per load level")
+    ap.add_argument("--queries", type=float, default=None, help="expected queries per scenario")
+    ap.add_argument("--cpu-seconds", type=float, default=20.0, help="CPU baseline sample budget (s)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    return ap.parse_args()
+    a = ap.parse_args()
+    if a.queries is None:
+        a.queries = 1e6 if a.workload == "c5" else 1e5
+    return a
 
 
 def dist_env():
-    rank = int(os.environ.get("RANK", "0"))
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    return rank, world, local
+    return int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")), \
+        int(os.environ.get("LOCAL_RANK", "0"))
 
 
-def workload(args, rank):
-    from paper_2202_13481_b200 import workloads as W
-    return W.c2(seeds=args.seeds, queries=args.queries, seed0=1 + rank * args.seeds)
+def workload(args, reference: bool = False):
+    """The scenario list (whole grid). The reference arm builds it from oracle/_ref alone
+    (tests/ref_workloads.py), so that process never maps the product library."""
+    if reference:
+        from tests import ref_workloads as W
+    else:
+        from paper_2202_13481_b200 import workloads as W
+    if args.workload == "c5":
+        return W.c5(n_scenarios=args.scenarios, queries=args.queries)
+    return W.c2(seeds=args.seeds, queries=args.queries)
 
 
-def config(args, world):
-    return {"workload": "C2: BERT-base preset, 8-GPU PARIS plan (23 partitions), ELSA, load 10-100% of peak",
-            "scenarios_per_gpu": 10 * args.seeds, "queries_per_scenario": args.queries, "n_gpus": world,
-            "l2": "inputs larger than L2 (traces ~12 B/query resident in HBM, >1 GB per step)",
-            "trace": "generated on device per step (MT19937-64 + glibc-log1p transcription)"}
+def config(args, world, specs):
+    if args.workload == "c5":
+        name = ("C5: large Monte-Carlo grid, %d scenarios x %.0e queries (3 models x {PARIS 8-GPU, "
+                "homogeneous 1g/2g/3g/7g} plans of 8-56 partitions x loads 0.3-0.9 x seeds), ELSA"
+                % (args.scenarios, args.queries))
+    else:
+        name = "C2: BERT-base, 8-GPU PARIS plan (23 partitions), ELSA, load 10-100%% of peak, %d seeds" % args.seeds
+    return {"workload": name, "scenarios": len(specs), "queries_per_scenario": args.queries, "n_gpus": world,
+            "sharding": "strong: cost-balanced contiguous shards of one grid" if world > 1 else "single GPU",
+            "l2": "inputs larger than L2 (traces ~12 B/query resident in HBM, >10 GB per step)",
+            "trace": "generated on device every step (MT19937-64 + glibc-log1p transcription)"}
 
 
 class ClockSampler:
@@ -106,51 +130,73 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.rows)}
 
 
-def cpu_baseline(specs, budget_s: float):
-    """The reference's own CPU path (oracle/_ref: sample_trace -> run -> tail_latency)
-    on every host core, over a bounded sample of the same grid."""
+def host_cores() -> int:
+    return len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
+
+
+def cpu_sample(specs, budget_s: float, start: int = 0):
+    """The reference's own CPU path (oracle/_ref: sample_trace -> run -> tail_latency) on
+    every host core (one std::thread per core pulling scenarios), over a bounded sample:
+    the `n` consecutive scenarios from `start` (C5 interleaves its 75 cells, so a run of
+    consecutive scenarios covers every plan and load), n sized from a one-scenario probe
+    so the sample is about `budget_s` of wall time."""
     from tests import oracle_py as O
     ora = O.best_oracle()
-    cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
-    # interleave loads so the sample covers the whole sweep
-    order = np.argsort([s.seed * 100 + i % 10 for i, s in enumerate(specs)], kind="stable")
-    probe = [specs[int(order[0])]]
+    cores = host_cores()
     t0 = time.perf_counter()
-    ora.run_grid(probe, threads=1)
-    per = max(time.perf_counter() - t0, 1e-3)  # one scenario on one core
+    ora.run_grid([specs[start % len(specs)]], TAILS, threads=1)
+    per = max(time.perf_counter() - t0, 1e-3)
     n = int(max(cores, min(len(specs), budget_s * cores / per)))
-    idx = [int(i) for i in order[:n]]
+    idx = [(start + j) % len(specs) for j in range(n)]
     sample = [specs[i] for i in idx]
     t0 = time.perf_counter()
-    r = ora.run_grid(sample, threads=cores)
+    r = ora.run_grid(sample, TAILS, threads=cores)
     dt = time.perf_counter() - t0
     q = int(r["total"].sum())
     return {"value": q / dt, "unit": UNIT, "cores": cores, "kind": ora.kind,
-            "sample": f"{len(sample)} of the grid's scenarios (all load levels), {q} simulated queries, "
-                      f"{dt:.1f} s wall on {cores} threads"}, r, idx
+            "sample": f"{len(sample)} consecutive scenarios of the grid from index {start} (every plan and load), "
+                      f"{q} simulated queries, {dt:.1f} s wall on {cores} threads"}, r, idx
 
 
 def run_reference(args):
+    """--impl reference: the compiled reference (oracle/_ref) on the box's host cores, on
+    this arm's config and metric; each step a bounded sample of the same grid."""
     rank, world, _ = dist_env()
     if world > 1 and rank != 0:
         return
-    specs = workload(args, 0)
-    steps = []
-    base = None
+    specs = workload(args, reference=True)
+    vals, base, start = [], None, 0
     for i in range(args.warmup + args.steps):
-        budget = max(args.cpu_seconds / 3.0, 3.0)
-        b, _, _ = cpu_baseline(specs, budget)
+        b, _, idx = cpu_sample(specs, max(args.cpu_seconds / 4.0, 4.0), start)
+        start = (idx[-1] + 1) % len(specs)
         if i >= args.warmup:
-            steps.append(b["value"])
+            vals.append(b["value"])
             base = b
-    val = float(np.median(steps))
+    val = float(np.median(vals))
     line = {"impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": None, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": config(args, args.gpus),
+            "scaling": "strong" if args.gpus > 1 else "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": config(args, args.gpus, specs),
             "cpu_baseline": {**base, "value": val},
             "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
+
+
+def profile_summary(kernel_sources):
+    """Per-launch DRAM traffic / instruction mix of K2 from the newest committed ncu summary,
+    used only if it was captured from the kernel sources built now (sha256 match) — a stale
+    capture is reported as such, never silently."""
+    want = hashlib.sha256(b"".join(p.read_bytes() for p in kernel_sources)).hexdigest()
+    for sp in sorted((ROOT / "profiles").glob("r*/summary.json"), reverse=True):
+        try:
+            js = json.loads(sp.read_text())
+        except Exception:
+            continue
+        if "K2 sim_warp_kernel" not in js.get("kernels", {}):
+            continue
+        fresh = js.get("kernel_sources_sha256") == want
+        return js, str(sp.relative_to(ROOT)), fresh
+    return None, None, False
 
 
 def main():
@@ -173,11 +219,21 @@ def main():
         else:
             td.init_process_group(backend)
     from paper_2202_13481_b200 import Engine
+    from paper_2202_13481_b200 import distributed as D
     eng = Engine(dev)
-    specs = workload(args, rank)
+    specs = workload(args)
+    bounds = D.shard_bounds(specs, world)
+    lo, hi = bounds[rank]
+    mine = specs[lo:hi]
 
-    # ---- device-resident throughput (value) ----
-    grid = eng.grid(specs, (0.95, 0.99))
+    def reduce(vals, op):
+        t = torch.tensor(vals, dtype=torch.float64, device=coll if world > 1 else "cpu")
+        if world > 1:
+            td.all_reduce(t, op=op)
+        return t.cpu().numpy()
+
+    # ---- device-resident throughput (value): this rank's shard, traces regenerated per step ----
+    grid = eng.grid(mine, TAILS)
     grid.set_usage(False)  # the metric needs counts and tails, not per-partition usage
     for _ in range(args.warmup):
         grid.launch()
@@ -195,52 +251,43 @@ def main():
         dev_ms = eng.event_elapsed_ms(0, 1)
     eng.synchronize()
     launches = eng.kernel_launches() - launches0
+    res = grid.results()
     # per-stage timing of one more launch, stages back to back (events on the library stream)
     grid.set_overlap(False)
     grid.launch()
     stage = grid.timing()
     grid.set_overlap(True)
-    res = grid.results()
-    if world > 1:
-        td.barrier()
-    t = torch.tensor([dev_ms, float(queries)], dtype=torch.float64, device=coll if world > 1 else "cpu")
-    if world > 1:
-        mx = t.clone()
-        td.all_reduce(mx[:1], op=td.ReduceOp.MAX)
-        td.all_reduce(t[1:], op=td.ReduceOp.SUM)
-        dev_ms_max, total_q = float(mx[0]), float(t[1])
-    else:
-        dev_ms_max, total_q = dev_ms, float(queries)
+    grid.close()
+    dev_ms_max = float(reduce([dev_ms], D_MAX(td))[0])
+    total_q = float(reduce([float(queries)], D_SUM(td))[0])
+    total_launches = int(reduce([float(launches)], D_SUM(td))[0])
     value = total_q * args.steps / (dev_ms_max / 1000.0)
 
-    # ---- cross-rank exchange: all-gather per-scenario p99 for the summary (NCCL) ----
-    p99 = torch.tensor(res["tail"][:, 1], dtype=torch.float64)
-    if world > 1:
-        p99 = p99.to(coll)
-        gathered = [torch.empty_like(p99) for _ in range(world)]
-        td.all_gather(gathered, p99)
-        p99 = torch.cat(gathered).cpu()
-
-    # ---- end-to-end through the public C-ABI call with host buffers (e2e) ----
-    # input = the grid's msv_scenario array in host memory (marshalled once, like a C++
-    # caller's array); every step: msv_run_grid = descriptors H2D, trace/sim/tails on
-    # the device, per-scenario results D2H into host buffers.
-    prepared = eng.prepare(specs)
-    eng.run_grid(prepared, (0.95, 0.99))  # untimed: sizes the context's reusable buffers
+    # ---- end to end through the public API with host buffers (e2e) ----
+    # every step: msv_run_grid on this rank's shard (scenario descriptors H2D, trace/sim/
+    # tails on the device, per-scenario results D2H into host buffers), the all-gather of
+    # every rank's results (NCCL) and the PARIS argmin per model and load on every rank
+    prepared = eng.prepare(mine)
+    eng.run_grid(prepared, TAILS)  # untimed: sizes the context's reusable buffers
     h0, d0 = eng.transfer_bytes()
+    labels = None
+    if args.workload == "c5":
+        from paper_2202_13481_b200 import workloads as W
+        labels = W.c5_labels(len(specs))
+    e2e_steps = max(1, min(args.steps, 3))
     if world > 1:
         td.barrier()
     t0 = time.perf_counter()
-    for _ in range(max(1, min(args.steps, 3))):
-        r = eng.run_grid(prepared, (0.95, 0.99))
-    e2e_steps = max(1, min(args.steps, 3))
+    for _ in range(e2e_steps):
+        full = D.run_sharded(specs, lambda sub: eng.run_grid(prepared, TAILS), rank, world,
+                             device=coll if world > 1 else None)
+        decision = D.grouped_argmin(full["tail"][:, 1], *labels) if labels else None
     e2e_s = time.perf_counter() - t0
     h1, d1 = eng.transfer_bytes()
-    tt = torch.tensor([e2e_s], dtype=torch.float64, device=coll if world > 1 else "cpu")
-    if world > 1:
-        td.all_reduce(tt, op=td.ReduceOp.MAX)
-    e2e_value = total_q * e2e_steps / float(tt[0])
-    assert np.array_equal(r["placement_hash"], res["placement_hash"]), "e2e and device-resident runs disagree"
+    e2e_max = float(reduce([e2e_s], D_MAX(td))[0])
+    e2e_value = total_q * e2e_steps / e2e_max
+    assert np.array_equal(full["placement_hash"][lo:hi], res["placement_hash"]), \
+        "e2e and device-resident runs disagree"
 
     if rank == 0:
         sim_s = stage["sim_ms"] / 1000.0
@@ -250,59 +297,50 @@ def main():
             peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text())
         except Exception:
             pass
-        peak = float(peaks.get("hbm_gbs", 6650.0))
-        # per-launch DRAM traffic and instruction mix of K2 from the committed ncu capture
-        prof_k2, prof_src, prof_all = None, None, {}
-        for sp in sorted((ROOT / "profiles").glob("r*/summary.json"), reverse=True):
-            try:
-                prof_all = json.loads(sp.read_text())["kernels"]
-                prof_k2 = prof_all["K2 sim_warp_kernel"]
-                prof_src = str(sp.relative_to(ROOT))
-                break
-            except Exception:
-                continue
+        peak = float(peaks.get("hbm_gbs", peaks.get("hbm_GBps", 6650.0)))
+        csrc = ROOT / "paper_2202_13481_b200" / "csrc"
+        prof, prof_src, fresh = profile_summary([csrc / "msv_sim_warp.cu", csrc / "msv_sim.cu"])
         sim_launches = max(1, round(launches / args.steps / 3))  # K1/K2/K3 once per chunk
         q_launch = queries / sim_launches
-        traffic = prof_k2["traffic_bytes_per_query"] * q_launch if prof_k2 else None
+        k2 = prof["kernels"]["K2 sim_warp_kernel"] if prof else None
+        traffic = k2["traffic_bytes_per_query"] * q_launch if (k2 and fresh) else None
         clk_mhz = clk.summary().get("sm_mhz") or 1965.0
         issue = None
-        if prof_k2:
-            ach = prof_k2["warp_instructions_per_query"] * queries / sim_s
+        if k2:
             sms = torch.cuda.get_device_properties(dev).multi_processor_count
             pk = sms * 4 * clk_mhz * 1e6  # one warp-instruction per scheduler per clock
-            issue = {"achieved_warp_inst_per_s": ach, "peak_warp_inst_per_s": pk, "frac": ach / pk,
-                     "warp_inst_per_query": prof_k2["warp_instructions_per_query"], "source": prof_src}
-            # the whole overlapped step: K1 + K2 + K3 instructions per query over the step time
-            wi = sum(prof_all[k]["warp_instructions_per_query"] for k in prof_all
-                     if "warp_instructions_per_query" in prof_all[k] and not k.startswith("K4"))
-            issue["step_warp_inst_per_query"] = wi
-            issue["step_frac"] = wi * total_q * args.steps / (dev_ms_max / 1000.0) / world / pk
+            wi = sum(v["warp_instructions_per_query"] for kname, v in prof["kernels"].items()
+                     if "warp_instructions_per_query" in v and not kname.startswith("K4"))
+            issue = {"warp_inst_per_query_k2": k2["warp_instructions_per_query"], "step_warp_inst_per_query": wi,
+                     "step_frac": wi * total_q * args.steps / (dev_ms_max / 1000.0) / world / pk,
+                     "peak_warp_inst_per_s": pk, "source": prof_src, "fresh": fresh}
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": dev_ms_max / args.steps, "higher_is_better": True,
-                "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-                "config": config(args, world),
+                "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "f64",
+                "data": "synthetic", "config": config(args, world, specs),
                 "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": (h1 - h0) // e2e_steps,
-                        "d2h_bytes_per_step": (d1 - d0) // e2e_steps},
-                "gpu_launches": launches,
+                        "d2h_bytes_per_step": (d1 - d0) // e2e_steps,
+                        "includes": "msv_run_grid with host buffers + all-gather + PARIS argmin"},
+                "gpu_launches": total_launches,
                 "stage_ms": {k: round(v, 3) for k, v in stage.items()},
                 "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                              "frac": achieved / peak, "traffic": traffic,
                              "traffic_unit": "DRAM bytes per K2 launch (ncu, %d queries per launch)" % q_launch,
+                             "traffic_source": (prof_src if fresh else f"stale capture {prof_src}: null")
+                             if prof else None,
                              "algorithmic_bytes_per_launch": SIM_BYTES_PER_QUERY * q_launch,
                              "kernel": "sim_warp_kernel (K2)", "issue": issue,
                              "note": "K2 is issue-bound (dependent FP64 state machine): 'issue' is the binding "
-                                     "roof; HBM fraction is small by construction (DESIGN.md roofline)"},
+                                     "roof; HBM fraction is small by construction (DESIGN.md §4)"},
                 "clocks": clk.summary()}
-        loads = np.tile(np.repeat(np.arange(1, 11) / 10.0, args.seeds), world)
-        allp = p99.numpy()
-        line["p99_ms_by_load"] = {f"{l:.1f}": round(float(np.mean(allp[loads == l])), 4) for l in np.unique(loads)}
+        if decision is not None:
+            line["paris_decision"] = {f"{g[0]}@{g[1]}": best for g, (best, _) in sorted(decision.items())}
         if not args.no_cpu_baseline and world == 1:  # the CPU reference is timed at N=1 only
-            b, ref, idx = cpu_baseline(specs, args.cpu_seconds)
+            b, ref, idx = cpu_sample(specs, args.cpu_seconds)
             line["cpu_baseline"] = b
             # the CPU sample doubles as a full-size parity check of the timed device run
             line["parity"] = {
-                "scenarios_checked": len(idx),
-                "queries_checked": int(ref["total"].sum()),
+                "scenarios_checked": len(idx), "queries_checked": int(ref["total"].sum()),
                 "placement_hash_equal": bool(np.array_equal(res["placement_hash"][idx], ref["placement_hash"])),
                 "tails_equal": bool(np.array_equal(res["tail"][idx], ref["tail"], equal_nan=True)),
                 "counts_equal": bool(all(np.array_equal(res[k][idx], ref[k]) for k in
@@ -311,6 +349,14 @@ def main():
         print(json.dumps(line), flush=True)
     if world > 1:
         td.destroy_process_group()
+
+
+def D_MAX(td):
+    return td.ReduceOp.MAX
+
+
+def D_SUM(td):
+    return td.ReduceOp.SUM
 
 
 if __name__ == "__main__":

@@ -278,6 +278,20 @@ int msv_lognormal_pdf(double mu, double sigma, int b_max, double* pmf, double* c
  * the input stream of msv_run_noise. */
 int msv_noise_multipliers(uint64_t seed, double sigma, int64_t n, double* out);
 
+/* Arithmetic self-checks (test support; no reference analogue). The parity tests
+ * compare these with the host's libm directly (rng.hpp:20):
+ *   msv_log1p_digest   per chunk of `chunk` inputs k in [0, n) of seed's stream
+ *                      (msv_selftest_input in csrc/msv_math.h), the wrapping sum of
+ *                      msv_selftest_digest(k, -log1p(-u_k)) computed with the device's
+ *                      glibc-log1p transcription `variant`; digests[ceil(n/chunk)].
+ *   msv_log1p_values   the device's -log1p(-u_k) for k in [first, first+count).
+ *   msv_quotient_check K1's certified quotient (msv_trace.cuh gap_quotient) against
+ *                      the IEEE division on n (gap, rate) pairs: counts[0] mismatches,
+ *                      counts[1] certificate fallbacks. */
+int msv_log1p_digest(msv_ctx* ctx, int variant, uint64_t seed, int64_t n, int64_t chunk, uint64_t* digests);
+int msv_log1p_values(msv_ctx* ctx, int variant, uint64_t seed, int64_t first, int64_t count, double* out);
+int msv_quotient_check(msv_ctx* ctx, uint64_t seed, int64_t n, int64_t* counts);
+
 #ifdef __cplusplus
 }
 #endif

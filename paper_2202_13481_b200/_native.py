@@ -139,6 +139,9 @@ _SIGNATURES = {
     "msv_synth_profile": (C.c_int, [C.c_double, C.c_double, C.c_double, C.c_double, C.c_int, _i32p, C.c_int, _i32p,
                                     _i32p, _f64p, _f64p]),
     "msv_lognormal_pdf": (C.c_int, [C.c_double, C.c_double, C.c_int, _f64p, _f64p]),
+    "msv_log1p_digest": (C.c_int, [_P, C.c_int, C.c_uint64, C.c_int64, C.c_int64, C.POINTER(C.c_uint64)]),
+    "msv_log1p_values": (C.c_int, [_P, C.c_int, C.c_uint64, C.c_int64, C.c_int64, _f64p]),
+    "msv_quotient_check": (C.c_int, [_P, C.c_uint64, C.c_int64, _i64p]),
 }
 
 _lib = None

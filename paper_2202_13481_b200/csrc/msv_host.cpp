@@ -92,10 +92,14 @@ struct Routing {
 };
 
 // glibc's log1p build selected on this host (rng.hpp:20 calls whichever one the
-// ifunc resolver picked). Probe inputs where the two builds round differently.
+// ifunc resolver picked). Probe inputs where the two transcribed builds round
+// differently and vote; every probed input must agree with the winning build (inputs
+// where the builds agree included). A host libm matching neither — another glibc —
+// returns -1: the device would diverge from the host reference, so msv_create fails
+// instead of silently picking one.
 int probe_host_log1p() {
     uint64_t s = 0x9E3779B97F4A7C15ull;
-    int fma_votes = 0, gen_votes = 0;
+    int fma_votes = 0, gen_votes = 0, neither = 0;
     for (int it = 0; it < 2000000 && fma_votes + gen_votes < 16; ++it) {
         s ^= s << 13;
         s ^= s >> 7;
@@ -103,13 +107,18 @@ int probe_host_log1p() {
         const double u = (double)(s >> 11) * 0x1.0p-53;
         const double a = msv_log1p_neg(-u, MSV_LOG1P_FMA);
         const double g = msv_log1p_neg(-u, MSV_LOG1P_GENERIC);
-        if (msv_dbits(a) == msv_dbits(g)) continue;
         volatile double xin = -u;
         const double h = log1p(xin);
+        if (msv_dbits(a) == msv_dbits(g)) {
+            neither += msv_dbits(h) != msv_dbits(a);
+            continue;
+        }
         if (msv_dbits(h) == msv_dbits(a)) ++fma_votes;
         else if (msv_dbits(h) == msv_dbits(g)) ++gen_votes;
+        else ++neither;
     }
-    return gen_votes > fma_votes ? MSV_LOG1P_GENERIC : MSV_LOG1P_FMA;
+    if (neither || (fma_votes && gen_votes) || fma_votes + gen_votes == 0) return -1;
+    return gen_votes ? MSV_LOG1P_GENERIC : MSV_LOG1P_FMA;
 }
 
 }  // namespace
@@ -122,7 +131,7 @@ int set_error(int code, const char* what) { return fail(code, what ? what : "");
 struct GridBufs {
     DevBuf d_scen, d_out, d_tjobs, d_tgroups, d_tailjobs, d_tails, d_p, d_usage, d_nq, d_tovf, d_parts, d_masks,
         d_work, d_counter;
-    DevBuf d_arr, d_bat, d_next, d_samples, d_rec, d_glat, d_gutil, d_gcdf, d_gguide;
+    DevBuf d_arr, d_bat, d_next, d_rec, d_glat, d_gutil, d_gcdf, d_gguide;
 };
 
 // guide[j] = first i with !(cdf[i] < j/G): lower_bound's answer for u = j/G, a valid
@@ -513,9 +522,9 @@ int grid_build(msv_ctx* ctx, const msv_scenario* sc, int64_t n, const double* ta
         }
     }
     pt.mark("validate");
-    // Waves: bound the per-launch trace working set (arrival 8 + batch 4 + link 4 +
-    // sample 8 [+ record 24] bytes per query slot).
-    const size_t per_q = 24 + (records ? sizeof(msv_record) : 0);
+    // Waves: bound the per-launch trace working set (arrival / measured latency 8 +
+    // batch 4 + link 4 [+ record 24] bytes per query slot).
+    const size_t per_q = 16 + (records ? sizeof(msv_record) : 0);
     // Keep enough trace slots resident that a wave of 1e6-query scenarios still fills
     // every warp slot of the simulation kernel (~4,100 on a B200).
     size_t budget = free_device_bytes() / 10 * 7;
@@ -705,7 +714,6 @@ int grid_build(msv_ctx* ctx, const msv_scenario* sc, int64_t n, const double* ta
     MSV_CUDA_TRY(g->B->d_arr.ensure(wq * 8));
     MSV_CUDA_TRY(g->B->d_bat.ensure(wq * 4));
     MSV_CUDA_TRY(g->B->d_next.ensure(wq * 4));
-    MSV_CUDA_TRY(g->B->d_samples.ensure(wq * 8));
     if (records) MSV_CUDA_TRY(g->B->d_rec.ensure(wq * sizeof(msv_record)));
     MSV_CUDA_TRY(g->B->d_scen.ensure(std::max<int64_t>(n, 1) * sizeof(DevScen)));
     MSV_CUDA_TRY(g->B->d_out.ensure(std::max<int64_t>(n, 1) * sizeof(DevOut)));
@@ -834,7 +842,7 @@ int grid_build(msv_ctx* ctx, const msv_scenario* sc, int64_t n, const double* ta
         d.parts = g->B->d_parts.as<DevPart>() + sc_part[i];
         d.route_mask = (sc_mask[i] == (size_t)-1) ? nullptr : g->B->d_masks.as<uint64_t>() + sc_mask[i];
         d.next = g->B->d_next.as<uint32_t>() + o;
-        d.samples = g->B->d_samples.as<double>() + o;
+        d.samples = g->B->d_arr.as<double>() + o;  // latencies overwrite their own (dead) arrivals
         d.records = records ? g->B->d_rec.as<msv_record>() + o : nullptr;
         d.P = g->P[i];
         d.b_max = prof.b_max;
@@ -1208,8 +1216,11 @@ int msv_create(int device, msv_ctx** out) {
     if (major != 10 || minor != 0)
         return fail(MSV_CUDA, "msv_create: libmsv is built for sm_100a (B200); device is sm_" +
                                   std::to_string(major) + std::to_string(minor));
-    MSV_CUDA_TRY(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
     ctx->log1p = probe_host_log1p();
+    if (ctx->log1p < 0)
+        return fail(MSV_CUDA, "msv_create: this host's libm log1p matches neither transcribed glibc build "
+                              "(csrc/msv_math.h); device traces would diverge from rng.hpp:20");
+    MSV_CUDA_TRY(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
     *out = ctx.release();
     return MSV_OK;
 }
@@ -1243,7 +1254,10 @@ int msv_destroy(msv_ctx* ctx) {
 
 int msv_set_log1p_variant(msv_ctx* ctx, int variant) {
     if (!ctx) return fail(MSV_PARAM, "null context");
-    if (variant == MSV_LOG1P_AUTO) variant = probe_host_log1p();
+    if (variant == MSV_LOG1P_AUTO) {
+        variant = probe_host_log1p();
+        if (variant < 0) return fail(MSV_CUDA, "msv_set_log1p_variant: host libm log1p matches neither build");
+    }
     if (variant != MSV_LOG1P_GENERIC && variant != MSV_LOG1P_FMA)
         return fail(MSV_PARAM, "msv_set_log1p_variant: unknown variant");
     ctx->log1p = variant;
@@ -2085,6 +2099,52 @@ int msv_dispatch_batch(msv_ctx* ctx, int32_t profile, int scheduler, int64_t n_t
     MSV_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
     for (int64_t t = 0; t < n_trials; ++t)
         if (err[t]) return fail(err[t], "trial " + std::to_string(t) + ": profile lookup outside the grid");
+    return MSV_OK;
+}
+
+// ---- arithmetic self-checks (msv_selftest.cu) ----
+int msv_log1p_digest(msv_ctx* ctx, int variant, uint64_t seed, int64_t n, int64_t chunk, uint64_t* digests) {
+    if (!ctx || !digests || n < 0 || chunk <= 0) return fail(MSV_PARAM, "msv_log1p_digest: bad argument");
+    if (variant != MSV_LOG1P_GENERIC && variant != MSV_LOG1P_FMA) return fail(MSV_PARAM, "unknown log1p variant");
+    if (n == 0) return MSV_OK;
+    SetDevice sd(ctx->device);
+    const int64_t n_chunks = (n + chunk - 1) / chunk;
+    DevBuf d;
+    MSV_CUDA_TRY(d.ensure(n_chunks * 8));
+    MSV_CUDA_TRY(msv::launch_log1p_digest(variant, seed, n, chunk, d.as<uint64_t>(), ctx->stream));
+    ctx->launches += 1;
+    MSV_CUDA_TRY(cudaMemcpyAsync(digests, d.p, n_chunks * 8, cudaMemcpyDeviceToHost, ctx->stream));
+    MSV_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    return MSV_OK;
+}
+
+int msv_log1p_values(msv_ctx* ctx, int variant, uint64_t seed, int64_t first, int64_t count, double* out) {
+    if (!ctx || !out || first < 0 || count < 0) return fail(MSV_PARAM, "msv_log1p_values: bad argument");
+    if (variant != MSV_LOG1P_GENERIC && variant != MSV_LOG1P_FMA) return fail(MSV_PARAM, "unknown log1p variant");
+    if (count == 0) return MSV_OK;
+    SetDevice sd(ctx->device);
+    DevBuf d;
+    MSV_CUDA_TRY(d.ensure(count * 8));
+    MSV_CUDA_TRY(msv::launch_log1p_values(variant, seed, first, count, d.as<double>(), ctx->stream));
+    ctx->launches += 1;
+    MSV_CUDA_TRY(cudaMemcpyAsync(out, d.p, count * 8, cudaMemcpyDeviceToHost, ctx->stream));
+    MSV_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    return MSV_OK;
+}
+
+int msv_quotient_check(msv_ctx* ctx, uint64_t seed, int64_t n, int64_t* counts) {
+    if (!ctx || !counts || n < 0) return fail(MSV_PARAM, "msv_quotient_check: bad argument");
+    SetDevice sd(ctx->device);
+    DevBuf d;
+    MSV_CUDA_TRY(d.ensure(16));
+    MSV_CUDA_TRY(cudaMemsetAsync(d.p, 0, 16, ctx->stream));
+    MSV_CUDA_TRY(msv::launch_quotient_check(seed, n, d.as<unsigned long long>(), ctx->stream));
+    ctx->launches += 1;
+    unsigned long long h[2] = {0, 0};
+    MSV_CUDA_TRY(cudaMemcpyAsync(h, d.p, 16, cudaMemcpyDeviceToHost, ctx->stream));
+    MSV_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    counts[0] = (int64_t)h[0];
+    counts[1] = (int64_t)h[1];
     return MSV_OK;
 }
 

@@ -48,7 +48,9 @@ struct DevScen {
     const DevPart* parts;       // P entries in (k, id) ascending order
     const uint64_t* route_mask; // P masks (bit b-1: segment of k covers batch b) or null
     uint32_t* next;             // per-query link of the overflow queues (capacity n)
-    double* samples;            // measured latencies out (capacity n)
+    double* samples;            // measured latencies out: latency of query q >= m0 lands at
+                                // samples[q] (the generated / uploaded arrival buffer itself:
+                                // a query's arrival is dead once its window is retired)
     msv_record* records;        // per-query records out, or null
     int32_t P;
     int32_t b_max;              // profile b_max
@@ -70,7 +72,7 @@ struct DevOut {
     uint64_t lat_min_bits;
     uint64_t lat_max_bits;
     int32_t status;
-    int32_t pad;
+    int32_t m0;                 // first measured query: samples live at samples[m0, m0 + n_samples)
 };
 
 struct SimParams {
@@ -202,6 +204,12 @@ cudaError_t launch_sim(int W, int S, int sched, bool records, const SimParams& p
                        cudaStream_t stream);
 size_t sim_smem_bytes(int W, int S, int n_cells);
 int sim_max_blocks_per_sm(int W, int S, int sched, bool records, bool full, bool lazy, int n_cells);
+// Arithmetic self-checks (msv_selftest.cu).
+cudaError_t launch_log1p_digest(int variant, uint64_t seed, int64_t n, int64_t chunk, uint64_t* d_out,
+                                cudaStream_t stream);
+cudaError_t launch_log1p_values(int variant, uint64_t seed, int64_t first, int64_t count, double* d_out,
+                                cudaStream_t stream);
+cudaError_t launch_quotient_check(uint64_t seed, int64_t n, unsigned long long* d_counts, cudaStream_t stream);
 cudaError_t launch_tail(const TailJob* d_jobs, int n_jobs, const double* d_p, int n_p,
                         cudaStream_t stream);
 cudaError_t launch_dispatch(const DispatchParams& p, cudaStream_t stream);

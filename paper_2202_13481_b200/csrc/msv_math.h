@@ -211,3 +211,21 @@ MSV_HD uint64_t msv_query_digest(uint64_t id, int32_t partition, double start, d
     const uint32_t b = ((uint32_t)(sb >> 32) ^ (uint32_t)fb ^ c) * 0x27D4EB2Fu + c;
     return ((uint64_t)a << 32) | b;
 }
+
+// ---- self-check inputs (msv_log1p_digest; the host checker tests/log1p_check.c) ----
+MSV_HD uint64_t msv_splitmix64(uint64_t z) { return msv_mix64(z); }
+
+// Input k of seed's stream on the generator's grid u = m * 2^-53 (Rng::uniform,
+// rng.hpp:17): k mod 4 == 0/3 uniform m, 1 a right-shifted m (small u, log1p's tiny
+// and intermediate ranges), 2 m close to 2^53 (u close to 1, large gaps).
+MSV_HD double msv_selftest_input(uint64_t seed, uint64_t k) {
+    const uint64_t x = msv_mix64(seed ^ (k * 0xD1B54A32D192ED03ull));
+    uint64_t m = x >> 11;
+    const uint64_t y = msv_mix64(x);
+    if ((k & 3) == 1) m >>= (y & 63);
+    if ((k & 3) == 2) m = (1ull << 53) - 1 - (m >> (y & 31));
+    return (double)m * 0x1.0p-53;
+}
+
+// Digest term of result v of input k (wrapping sums of these are compared).
+MSV_HD uint64_t msv_selftest_digest(uint64_t k, double v) { return msv_mix64(msv_dbits(v) ^ (k << 1)); }

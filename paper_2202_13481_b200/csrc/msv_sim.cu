@@ -8,19 +8,27 @@
 // the per-arrival path serves G scenarios.
 //
 // Per arrival (every kernel of K2 follows this protocol):
-//   1. every lane retires its own completions with time <= now, in chain order, with
-//      no warp collective (completions on different partitions commute and a
-//      completion precedes an arrival at equal time, engine.hpp:101-107);
+//   1. every lane advances its own partitions to `now`: a running query with finish
+//      <= now has completed and the queue head starts at that finish, in chain order,
+//      with no warp collective (completions on different partitions commute and a
+//      completion precedes an arrival at equal time, engine.hpp:101-107). A
+//      completion's bookkeeping is not done here: with noise off a query's start and
+//      finish are known when it is placed (step 3);
 //   2. every lane evaluates Eq. 1 (t_wait, kept as an exact FIFO fold) and Eq. 2 for
 //      its slots; Step A = first set bit of the segment's ballot bits over the slots in
 //      order, Step B = a shuffle-tree argmin over the segment with order tie-break;
 //      FIFS = (k, id) / (queue length, id) key minima;
 //   3. the chosen slot starts the query or appends it to its FIFO (shared-memory
-//      ring, overflow list threaded through query ids in global memory).
+//      ring, overflow list threaded through query ids in global memory); its start is
+//      the arrival (idle) or the finish of the query placed before it, its finish =
+//      start + est (the same RN add the completion event performs), and the chosen lane
+//      books the completion at once: latency, SLA, measured sample, placement digest,
+//      record, usage (in the partition's completion = FIFO order).
 // Each segment keeps a double-buffered 32-arrival window in shared memory, refilled
-// by cp.async one window ahead. Measured latencies land at samples[q - m0]
-// (arrivals are sorted, so the measured set is the suffix from the first
-// arrival >= warmup), ready for K3. The plain variant (no routing / missing sizes /
+// by cp.async one window ahead. Measured latencies overwrite their own arrivals
+// (samples[q] with samples == the arrival buffer: a placed query's arrival is never
+// read again); arrivals are sorted, so the measured set is the suffix from the first
+// arrival >= warmup, m0, ready for K3. The plain variant (no routing / missing sizes /
 // wait check / usage / records in the launch) carries none of those features' work.
 #include <cuda_pipeline.h>
 
@@ -30,7 +38,6 @@ namespace msv {
 
 namespace {
 
-constexpr uint64_t kQidMask = (1ull << 40) - 1;
 
 template <int W, int S>
 struct SegCfg {
@@ -43,9 +50,7 @@ template <int W, int S>
 struct SegSmem {
     static constexpr int G = SegCfg<W, S>::G;
     static constexpr int QC = SegCfg<W, S>::qcap;
-    double q_est[S][QC][32];
-    double q_arr[S][QC][32];
-    uint64_t q_meta[S][QC][32];
+    double q_est[S][QC][32];  // queued latencies (starts / finishes follow from them)
     double win_t[2][32][G];  // [buffer][entry][segment]
     int32_t win_b[2][32][G];
     uint32_t g_head[S][32];  // overflow list head / tail per lane slot
@@ -84,11 +89,11 @@ __global__ void __launch_bounds__(kSimWarpsPerBlock * 32, (SegCfg<W, S>::min_blo
     bool unit = true, check_wait = false;
     int bmax = 0;
     // ---- per-lane partition slots ----
+    // c_* = the query running at the last arrival; tail = finish of the query placed last
     bool act[S], busy[S];
     int32_t row[S], pk[S], qh[S], qn[S];
     uint32_t gn[S], nq[S];
-    double c_start[S], c_est[S], c_comp[S], c_arr[S], fold[S], bms[S], wbms[S];
-    uint64_t c_meta[S];
+    double c_start[S], c_est[S], c_comp[S], tail[S], fold[S], bms[S], wbms[S];
     uint32_t viol = 0, mviol = 0;
     uint64_t hash = 0;
     double wdiff = 0.0;
@@ -97,8 +102,7 @@ __global__ void __launch_bounds__(kSimWarpsPerBlock * 32, (SegCfg<W, S>::min_blo
         act[s] = busy[s] = false;
         row[s] = pk[s] = qh[s] = qn[s] = 0;
         gn[s] = nq[s] = 0;
-        c_start[s] = c_est[s] = c_comp[s] = c_arr[s] = fold[s] = bms[s] = wbms[s] = 0.0;
-        c_meta[s] = 0;
+        c_start[s] = c_est[s] = c_comp[s] = tail[s] = fold[s] = bms[s] = wbms[s] = 0.0;
     }
 
     // Async copy of arrivals [from, from+32) into the segment's window buffer b.
@@ -174,9 +178,8 @@ __global__ void __launch_bounds__(kSimWarpsPerBlock * 32, (SegCfg<W, S>::min_blo
                     busy[s] = false;
                     qh[s] = qn[s] = 0;
                     gn[s] = nq[s] = 0;
-                    c_start[s] = c_est[s] = c_comp[s] = c_arr[s] = 0.0;
+                    c_start[s] = c_est[s] = c_comp[s] = tail[s] = 0.0;
                     fold[s] = bms[s] = wbms[s] = 0.0;
-                    c_meta[s] = 0;
                 }
                 viol = mviol = 0;
                 hash = 0;
@@ -206,9 +209,7 @@ __global__ void __launch_bounds__(kSimWarpsPerBlock * 32, (SegCfg<W, S>::min_blo
             t = M.win_t[buf][i - win_base][seg];
             b = M.win_b[buf][i - win_base][seg];
             if (m0 < 0 && t >= warmup) m0 = i;  // measured iff arrival >= warmup (engine.hpp:262)
-        } else if (ending) {
-            t = INFINITY;  // drain everything (no horizon cut-off)
-        }
+        }  // (ending: nothing to drain — every query was booked when it was placed)
         // the new query's latency on each slot depends on its batch only: load it ahead
         // of the drain (FULL: batch clamped into the table, missing sizes read 0)
         double est_n[S];
@@ -222,52 +223,25 @@ __global__ void __launch_bounds__(kSimWarpsPerBlock * 32, (SegCfg<W, S>::min_blo
             }
         }
 
-        // ---- 1. completions with time <= t, lane-local, in chain order ----
+        // ---- 1. advance to t, lane-local, in chain order (engine.hpp:167-187) ----
 #pragma unroll
         for (int s = 0; s < S; ++s) {
-            while (busy[s] && c_comp[s] <= t) {  // engine.hpp:167-187
-                const double now = c_comp[s];
-                const double lat = now - c_arr[s];
-                const bool met = lat <= sla;
-                const uint64_t q = c_meta[s] & kQidMask;
-                if (FULL) {  // PartitionUsage (engine.hpp:175-177)
-                    const double ran = now - c_start[s];
-                    const int cb = (int)(c_meta[s] >> 40);
-                    bms[s] = bms[s] + ran;
-                    wbms[s] = wbms[s] + ran * s_util[row[s] + cb - 1];
-                    nq[s] += 1;
-                }
-                viol += met ? 0u : 1u;
-                if (c_arr[s] >= warmup) {
-                    mviol += met ? 0u : 1u;
-                    samples[(uint32_t)q - (uint32_t)m0] = lat;
-                }
-                hash += msv_query_digest(q, pk[s] & 0xff, c_start[s], now);
-                if (REC) {
-                    d->records[q].start_ms = c_start[s];
-                    d->records[q].finish_ms = now;
-                }
-                if (qn[s] > 0) {  // start the queue head now (engine.hpp:181-185)
+            while (busy[s] && c_comp[s] <= t) {
+                if (qn[s] > 0) {  // start the queue head at the finish (engine.hpp:181-185)
                     const int h = qh[s];
                     const double est = M.q_est[s][h][lane];
-                    c_arr[s] = M.q_arr[s][h][lane];
-                    c_meta[s] = M.q_meta[s][h][lane];
                     qh[s] = (h + 1) & (QC - 1);
                     qn[s] -= 1;
                     if (gn[s] > 0) {  // refill the ring from the overflow list
                         const uint32_t g = M.g_head[s][lane];
                         M.g_head[s][lane] = d->next[g];
                         gn[s] -= 1;
-                        const int32_t gb = g_bat[g];
-                        const int e2 = (qh[s] + qn[s]) & (QC - 1);
-                        M.q_est[s][e2][lane] = s_lat[row[s] + gb - 1];
-                        M.q_arr[s][e2][lane] = g_arr[g];
-                        M.q_meta[s][e2][lane] = (uint64_t)g | ((uint64_t)gb << 40);
+                        M.q_est[s][(qh[s] + qn[s]) & (QC - 1)][lane] = s_lat[row[s] + g_bat[g] - 1];
                         qn[s] += 1;
                     }
-                    c_start[s] = now;
+                    c_start[s] = c_comp[s];
                     c_est[s] = est;
-                    c_comp[s] = now + est;
+                    c_comp[s] = c_start[s] + est;  // the placement computed the same sum
                     if (kFold) fold[s] = refold(s);
                 } else {
                     busy[s] = false;
@@ -395,25 +369,25 @@ __global__ void __launch_bounds__(kSimWarpsPerBlock * 32, (SegCfg<W, S>::min_blo
             }
         }
 
-        // ---- 3. start or enqueue on the chosen partition (engine.hpp:225-230) ----
+        // ---- 3. start or enqueue on the chosen partition (engine.hpp:225-230) and book
+        //         its completion (engine.hpp:167-187): start and finish are known now ----
 #pragma unroll
         for (int s = 0; s < S; ++s) {
             if (go && s * W + sl == ch) {
                 const double est = est_n[s];
-                const uint64_t meta = (uint64_t)i | ((uint64_t)b << 40);
+                double st, fin;
                 if (!busy[s]) {
                     busy[s] = true;
+                    st = t;
+                    fin = t + est;
                     c_start[s] = t;
                     c_est[s] = est;
-                    c_comp[s] = t + est;
-                    c_arr[s] = t;
-                    c_meta[s] = meta;
+                    c_comp[s] = fin;
                 } else {
+                    st = tail[s];  // starts when the query placed before it finishes
+                    fin = st + est;
                     if (gn[s] == 0 && qn[s] < QC) {
-                        const int e = (qh[s] + qn[s]) & (QC - 1);
-                        M.q_est[s][e][lane] = est;
-                        M.q_arr[s][e][lane] = t;
-                        M.q_meta[s][e][lane] = meta;
+                        M.q_est[s][(qh[s] + qn[s]) & (QC - 1)][lane] = est;
                         qn[s] += 1;
                     } else {
                         if (gn[s] == 0) M.g_head[s][lane] = (uint32_t)i;
@@ -423,9 +397,28 @@ __global__ void __launch_bounds__(kSimWarpsPerBlock * 32, (SegCfg<W, S>::min_blo
                     }
                     fold[s] = fold[s] + est;  // appending extends the left fold exactly
                 }
+                tail[s] = fin;
+                const double lat = fin - t;  // latency = finish - arrival
+                const bool met = lat <= sla;
+                viol += met ? 0u : 1u;
+                if (t >= warmup) {  // measured (engine.hpp:262)
+                    mviol += met ? 0u : 1u;
+                    samples[i] = lat;
+                }
+                hash += msv_query_digest((uint64_t)i, pk[s] & 0xff, st, fin);
+                if (FULL) {  // PartitionUsage (engine.hpp:175-177), completion order
+                    const double ran = fin - st;
+                    bms[s] = bms[s] + ran;
+                    wbms[s] = wbms[s] + ran * s_util[row[s] + b - 1];
+                    nq[s] += 1;
+                }
                 if (REC) {
-                    d->records[i].partition = pk[s] & 0xff;
-                    d->records[i].kind = kind;
+                    msv_record r;
+                    r.start_ms = st;
+                    r.finish_ms = fin;
+                    r.partition = pk[s] & 0xff;
+                    r.kind = kind;
+                    d->records[i] = r;
                 }
             }
         }
@@ -434,10 +427,10 @@ __global__ void __launch_bounds__(kSimWarpsPerBlock * 32, (SegCfg<W, S>::min_blo
         // ---- end of trace: reduce the segment and publish (segment-uniform, rare) ----
         if (ending) {
             __pipeline_wait_prior(0);  // no copy may land in a window after the segment moves on
-            // last completion = each slot's final c_comp (a slot that never ran holds 0.0)
+            // last completion = each slot's last placed finish (a slot that never ran holds 0.0)
             double lf = 0.0;
 #pragma unroll
-            for (int s = 0; s < S; ++s) lf = (lf < c_comp[s]) ? c_comp[s] : lf;
+            for (int s = 0; s < S; ++s) lf = (lf < tail[s]) ? tail[s] : lf;
             const uint64_t v0 = seg_sum_u64<W>((uint64_t)viol, seg_mask);
             const uint64_t v2 = seg_sum_u64<W>((uint64_t)mviol, seg_mask);
             const uint64_t hsum = seg_sum_u64<W>(hash, seg_mask);
@@ -455,7 +448,7 @@ __global__ void __launch_bounds__(kSimWarpsPerBlock * 32, (SegCfg<W, S>::min_blo
                 o.lat_min_bits = msv_dbits(d->lat_floor) | kSignBit;  // latencies lie in [floor, horizon]
                 o.lat_max_bits = msv_dbits(o.horizon_ms) | kSignBit;
                 o.status = status;
-                o.pad = 0;
+                o.m0 = m0 >= 0 ? m0 : 0;
                 p.out[sidx] = o;
             }
             if (FULL && p.any_usage && d->usage_off >= 0) {

@@ -18,7 +18,21 @@
 //   * template flags: UNIT (alpha = beta = 1, per scenario: 1*x == x bit for bit), FULL
 //     (segment routing / missing sizes / wait check / usage / records in the launch; the
 //     plain variant carries none of that work), REC (per-query records), LAZY;
-//   * the horizon is the last completion each slot retained.
+//   * completion bookkeeping happens when a query is PLACED, not when it completes:
+//     with noise off a placed query's start is known at once (the arrival if the
+//     partition is idle, else the finish of the query queued last) and so is its
+//     finish = start + est (engine.hpp:181-185, :225-230 — the same RN add the
+//     completion event would perform). The chosen lane writes (start, finish, partition,
+//     kind) of arrival j into the window's shared row; when the 32-arrival window is
+//     done, lane j retires query base + j — latency, SLA violation, measured sample,
+//     placement digest, per-query record — all 32 lanes at once, coalesced. The lane-
+//     local drain before each arrival only pops queue heads (start = previous finish)
+//     to keep Eq. 1 exact; nothing is drained after the last arrival;
+//   * per-partition usage (PartitionUsage, FULL) is summed at placement, which is the
+//     partition's completion order (its FIFO order);
+//   * measured latencies overwrite the arrivals of their own queries (DevScen.samples
+//     == the arrival buffer): a query's arrival is dead once its window is retired;
+//   * the horizon is the last finish each slot placed.
 #include <type_traits>
 
 #include "msv_device.cuh"
@@ -27,11 +41,10 @@ namespace msv {
 
 namespace {
 
-constexpr uint64_t kQid = (1ull << 40) - 1;
 
 template <int S>
 struct WarpCfg {
-    static constexpr int qcap = S == 1 ? 8 : (S == 2 ? 4 : 2);  // shared ring entries per slot
+    static constexpr int qcap = S == 1 ? 16 : (S == 2 ? 8 : 4);  // shared ring entries per slot
     static constexpr int min_blocks = S == 1 ? 7 : (S == 2 ? 5 : 2);
 };
 
@@ -39,11 +52,12 @@ struct WarpCfg {
 template <int S>
 struct WarpSmem {
     static constexpr int QC = WarpCfg<S>::qcap;
-    double q_est[S][QC][32];
-    double q_arr[S][QC][32];
-    uint64_t q_meta[S][QC][32];
+    double q_est[S][QC][32];  // queued latencies (ring; starts/finishes follow from them)
     double win_t[32];
+    double win_s[32];   // start of window arrival j (written by the chosen lane)
+    double win_f[32];   // finish of window arrival j
     int32_t win_b[32];
+    int32_t win_p[32];  // partition id | kind << 8
     uint32_t g_head[S][32];  // overflow list head / tail per lane slot
     uint32_t g_tail[S][32];
     double dd_hi[S][32];     // overflow mode: double-double sum of the queued latencies
@@ -116,11 +130,12 @@ __global__ void __launch_bounds__(kSimWarpsPerBlock * 32, WarpCfg<S>::min_blocks
         if (FULL && route_mask) __builtin_assume(__isGlobal(route_mask));
 
         // ---- lane slots ----
+        // c_* = the query running at the last arrival; tail = finish of the query placed
+        // last (== c_comp while the FIFO is empty): the start of the next one queued
         bool act[S], busy[S];
         int32_t row[S], pk[S], qh[S], qn[S];  // pk = partition id | k << 8
         uint32_t gn[S], nq[S];
-        double c_start[S], c_est[S], c_comp[S], c_arr[S], fold[S], bms[S], wbms[S];
-        uint64_t c_meta[S];
+        double c_start[S], c_est[S], c_comp[S], tail[S], fold[S], bms[S], wbms[S];
 #pragma unroll
         for (int s = 0; s < S; ++s) {
             const int o = s * 32 + lane;
@@ -135,10 +150,9 @@ __global__ void __launch_bounds__(kSimWarpsPerBlock * 32, WarpCfg<S>::min_blocks
             busy[s] = false;
             qh[s] = qn[s] = 0;
             gn[s] = nq[s] = 0;
-            c_start[s] = c_est[s] = c_comp[s] = c_arr[s] = 0.0;
+            c_start[s] = c_est[s] = c_comp[s] = tail[s] = 0.0;
             fold[s] = 0.0;
             bms[s] = wbms[s] = 0.0;
-            c_meta[s] = 0;
         }
         uint32_t viol = 0, mviol = 0;
         uint64_t hash = 0;
@@ -162,37 +176,17 @@ __global__ void __launch_bounds__(kSimWarpsPerBlock * 32, WarpCfg<S>::min_blocks
             return acc;
         };
 
-        // Retire every completion of this lane with time <= t, in chain order.
+        // Advance this lane's partitions to time t: every running query with finish <= t
+        // has completed (a completion precedes an arrival at equal time, engine.hpp:101-107)
+        // and the queue head starts at its finish (engine.hpp:181-185). The completions'
+        // bookkeeping was done when the queries were placed; only Eq. 1's state moves.
         auto drain = [&](double t) {
 #pragma unroll
             for (int s = 0; s < S; ++s) {
-                while (busy[s] && c_comp[s] <= t) {  // engine.hpp:167-187
-                    const double now = c_comp[s];
-                    const double lat = now - c_arr[s];
-                    const bool met = lat <= sla;
-                    const double ran = now - c_start[s];
-                    const uint64_t q = c_meta[s] & kQid;
-                    const int cb = (int)(c_meta[s] >> 40);
-                    if (FULL) {  // PartitionUsage (engine.hpp:175-177); plain launches skip it
-                        bms[s] = bms[s] + ran;
-                        wbms[s] = wbms[s] + ran * s_util[row[s] + cb - 1];
-                        nq[s] += 1;
-                    }
-                    viol += met ? 0u : 1u;
-                    if (c_arr[s] >= warmup) {
-                        mviol += met ? 0u : 1u;
-                        samples[(uint32_t)q - (uint32_t)m0] = lat;
-                    }
-                    hash += msv_query_digest(q, pk[s] & 0xff, c_start[s], now);
-                    if (REC) {
-                        rec[q].start_ms = c_start[s];
-                        rec[q].finish_ms = now;
-                    }
-                    if (qn[s] > 0) {  // start the queue head now (engine.hpp:181-185)
+                while (busy[s] && c_comp[s] <= t) {
+                    if (qn[s] > 0) {
                         const int h = qh[s];
                         const double est = W.q_est[s][h][lane];
-                        c_arr[s] = W.q_arr[s][h][lane];
-                        c_meta[s] = W.q_meta[s][h][lane];
                         qh[s] = (h + 1) & (QC - 1);
                         qn[s] -= 1;
                         const bool spilled = gn[s] > 0;  // overflow mode before this pop
@@ -200,16 +194,13 @@ __global__ void __launch_bounds__(kSimWarpsPerBlock * 32, WarpCfg<S>::min_blocks
                             const uint32_t g = W.g_head[s][lane];
                             W.g_head[s][lane] = g_next[g];
                             gn[s] -= 1;
-                            const int32_t gb = g_bat[g];
                             const int e2 = (qh[s] + qn[s]) & (QC - 1);
-                            W.q_est[s][e2][lane] = s_lat[row[s] + gb - 1];
-                            W.q_arr[s][e2][lane] = g_arr[g];
-                            W.q_meta[s][e2][lane] = (uint64_t)g | ((uint64_t)gb << 40);
+                            W.q_est[s][e2][lane] = s_lat[row[s] + g_bat[g] - 1];
                             qn[s] += 1;
                         }
-                        c_start[s] = now;
+                        c_start[s] = c_comp[s];
                         c_est[s] = est;
-                        c_comp[s] = now + est;
+                        c_comp[s] = c_start[s] + est;  // the placement computed the same sum
                         if (kLazy && spilled && gn[s] > 0) {  // still spilled: drop the head from the sum
                             double hi = W.dd_hi[s][lane], lo = W.dd_lo[s][lane];
                             dd_add(hi, lo, -est);
@@ -555,20 +546,19 @@ __global__ void __launch_bounds__(kSimWarpsPerBlock * 32, WarpCfg<S>::min_blocks
                     for (int s = 0; s < S; ++s) {
                         if (mine[s]) {
                             const double est = est_n[s];
-                            const uint64_t meta = (uint64_t)i | ((uint64_t)b << 40);
+                            double st, fin;
                             if (!busy[s]) {
                                 busy[s] = true;
+                                st = t;
+                                fin = t + est;
                                 c_start[s] = t;
                                 c_est[s] = est;
-                                c_comp[s] = t + est;
-                                c_arr[s] = t;
-                                c_meta[s] = meta;
+                                c_comp[s] = fin;
                             } else {
+                                st = tail[s];  // starts when the query placed before it finishes
+                                fin = st + est;
                                 if (gn[s] == 0 && qn[s] < QC) {
-                                    const int e = (qh[s] + qn[s]) & (QC - 1);
-                                    W.q_est[s][e][lane] = est;
-                                    W.q_arr[s][e][lane] = t;
-                                    W.q_meta[s][e][lane] = meta;
+                                    W.q_est[s][(qh[s] + qn[s]) & (QC - 1)][lane] = est;
                                     qn[s] += 1;
                                 } else {
                                     if (kLazy) {  // overflow mode: keep the double-double sum
@@ -594,25 +584,54 @@ __global__ void __launch_bounds__(kSimWarpsPerBlock * 32, WarpCfg<S>::min_blocks
                                 // appending extends the left fold exactly (a stale fold stays stale)
                                 fold[s] = fold[s] + est;
                             }
-                            if (REC) {
-                                rec[i].partition = pk[s] & 0xff;
-                                rec[i].kind = kind;
+                            tail[s] = fin;
+                            W.win_s[j] = st;
+                            W.win_f[j] = fin;
+                            W.win_p[j] = (pk[s] & 0xff) | (kind << 8);
+                            if (FULL) {  // PartitionUsage (engine.hpp:175-177), completion order
+                                const double ran = fin - st;
+                                bms[s] = bms[s] + ran;
+                                wbms[s] = wbms[s] + ran * s_util[row[s] + b - 1];
+                                nq[s] += 1;
                             }
                         }
+                    }
+                }
+                // ---- retire the window: lane j completes query base + j (engine.hpp:167-187) ----
+                __syncwarp();
+                if (lane < cnt) {
+                    const int i = base + lane;
+                    const double st = W.win_s[lane], fin = W.win_f[lane];
+                    const int pw = W.win_p[lane];
+                    const double lat = fin - cur_t;  // latency = finish - arrival
+                    const bool met = lat <= sla;
+                    viol += met ? 0u : 1u;
+                    if (cur_t >= warmup) {  // measured (engine.hpp:262): overwrite the dead arrival
+                        mviol += met ? 0u : 1u;
+                        samples[i] = lat;
+                    }
+                    hash += msv_query_digest((uint64_t)i, pw & 0xff, st, fin);
+                    if (REC) {
+                        msv_record r;
+                        r.start_ms = st;
+                        r.finish_ms = fin;
+                        r.partition = pw & 0xff;
+                        r.kind = pw >> 8;
+                        rec[i] = r;
                     }
                 }
             }
         };
         if (d.alpha == 1.0 && d.beta == 1.0) simulate(std::true_type{});
         else simulate(std::false_type{});
-        drain(INFINITY);  // after the last arrival: drain everything, no horizon cut-off
+        // (nothing to drain after the last arrival: every query was retired with its window)
 
         // ---- publish (engine.hpp:233-252) ----
-        // last completion = each slot's final c_comp (completions per slot ascend; a slot
-        // that never ran keeps 0.0, below every completion and the duration)
+        // last completion = each slot's last placed finish (finishes per slot ascend; a
+        // slot that never ran keeps 0.0, below every completion and the duration)
         double lf = 0.0;
 #pragma unroll
-        for (int s = 0; s < S; ++s) lf = (lf < c_comp[s]) ? c_comp[s] : lf;
+        for (int s = 0; s < S; ++s) lf = (lf < tail[s]) ? tail[s] : lf;
         const uint64_t v0 = seg_sum_u64<32>((uint64_t)viol, kFull);
         const uint64_t v2 = seg_sum_u64<32>((uint64_t)mviol, kFull);
         const uint64_t hsum = seg_sum_u64<32>(hash, kFull);
@@ -634,7 +653,7 @@ __global__ void __launch_bounds__(kSimWarpsPerBlock * 32, WarpCfg<S>::min_blocks
             o.lat_min_bits = msv_dbits(d.lat_floor) | kSignBit;
             o.lat_max_bits = msv_dbits(o.horizon_ms) | kSignBit;
             o.status = status;
-            o.pad = 0;
+            o.m0 = m0 >= 0 ? m0 : 0;
             p.out[sidx] = o;
         }
         if (FULL && p.any_usage && d.usage_off >= 0) {

@@ -90,7 +90,7 @@ __global__ void __launch_bounds__(kTailThreads)
             if (threadIdx.x < n_p) J.out[threadIdx.x] = __longlong_as_double(0x7ff8000000000000ll);
             continue;
         }
-        const double* __restrict__ x = J.samples;
+        const double* __restrict__ x = J.samples + src.m0;  // the measured suffix
         if (threadIdx.x == 0) {
             S.kmin = src.lat_min_bits;
             S.kmax = src.lat_max_bits;

@@ -54,26 +54,90 @@ def shard_bounds(specs: Sequence, world: int) -> list[tuple[int, int]]:
     return bounds
 
 
+def _error_code(exc: BaseException) -> int:
+    """errors.hpp type of a local failure as the C-ABI status code (MSV_PARAM..MSV_CUDA),
+    99 for anything else."""
+    from . import _native as N
+    for code, cls in N._ERRORS.items():
+        if type(exc) is cls:
+            return int(code)
+    return 99
+
+
+def _raise_remote(codes: np.ndarray, rank: int, local_exc: BaseException | None, what: str) -> None:
+    """After the gather: every rank raises when any rank's local work failed (the failing
+    rank re-raises its own exception; the others raise the same errors.hpp type)."""
+    bad = [r for r, c in enumerate(codes) if c != 0]
+    if not bad:
+        return
+    if local_exc is not None:
+        raise local_exc
+    from . import _native as N
+    cls = N._ERRORS.get(int(codes[bad[0]]), N.Error)
+    raise cls(f"{what}: rank {bad[0]} failed (status {int(codes[bad[0]])})")
+
+
 def run_sharded(specs: Sequence, run_local: Callable[[list], dict], rank: int, world: int, device=None) -> dict:
     """Run this rank's shard with `run_local` (e.g. Engine.run_grid) and all-gather every
-    rank's rows in global scenario order."""
+    rank's rows in global scenario order. A failure of one rank's local work (e.g. a
+    LookupError from run_grid) still takes part in the gather — row 0 of every rank's
+    buffer carries its status — and is raised on every rank, as the single-process
+    reference would raise it, instead of leaving the other ranks in the collective."""
     import torch
     import torch.distributed as td
     bounds = shard_bounds(specs, world)
     lo, hi = bounds[rank]
-    local = pack(run_local(list(specs[lo:hi]))) if hi > lo else np.zeros((0, len(FIELDS)))
+    exc, local = None, np.zeros((0, len(FIELDS)))
+    try:
+        if hi > lo:
+            local = pack(run_local(list(specs[lo:hi])))
+    except Exception as e:  # noqa: BLE001 - re-raised after the gather
+        if world == 1:
+            raise
+        exc = e
     if world == 1:
         return unpack(local)
     width = max(h - l for l, h in bounds)
-    buf = np.full((width, len(FIELDS)), np.nan)
-    buf[: hi - lo] = local
+    buf = np.full((width + 1, len(FIELDS)), np.nan)
+    buf[0, 0] = _error_code(exc) if exc is not None else 0
+    if exc is None:
+        buf[1: 1 + hi - lo] = local
     t = torch.from_numpy(buf)
     if device is not None:
         t = t.to(device)
     parts = [torch.empty_like(t) for _ in range(world)]
     td.all_gather(parts, t)
-    rows = np.concatenate([p.cpu().numpy()[: h - l] for p, (l, h) in zip(parts, bounds)])
+    parts = [p.cpu().numpy() for p in parts]
+    _raise_remote(np.array([p[0, 0] for p in parts]), rank, exc, "run_sharded")
+    rows = np.concatenate([p[1: 1 + h - l] for p, (l, h) in zip(parts, bounds)])
     return unpack(rows)
+
+
+def grouped_argmin(p99: np.ndarray, group: Sequence, candidate: Sequence) -> dict:
+    """PARIS argmin per group (e.g. per (model, load) of the C5 grid): the mean p99 of every
+    candidate over its scenarios in list order (seed order; NaN tails skipped, summed like
+    mean_tail_at_rate, metrics.hpp:61-74), then the candidate with the least mean; ties go
+    to the candidate seen first. Returns {group: (best candidate, {candidate: mean})}."""
+    sums: dict = {}
+    order: dict = {}
+    for v, g, c in zip(np.asarray(p99, float), group, candidate):
+        d = sums.setdefault(g, {})
+        order.setdefault(g, [])
+        if c not in d:
+            d[c] = [0.0, 0]
+            order[g].append(c)
+        if v == v:
+            d[c][0] += float(v)
+            d[c][1] += 1
+    out = {}
+    for g, d in sums.items():
+        means = {c: (s / n if n else np.inf) for c, (s, n) in d.items()}
+        best = order[g][0]
+        for c in order[g][1:]:
+            if means[c] < means[best]:
+                best = c
+        out[g] = (best, means)
+    return out
 
 
 def paris_argmin(p99: np.ndarray, n_candidates: int, seeds_per_candidate: int) -> tuple[int, np.ndarray]:
@@ -117,19 +181,28 @@ def lbt_sharded(designs: Sequence, search_local: Callable[[list], list], rank: i
     `search.latency_bounded_throughput(eng, ds)` mapped to tuples."""
     bounds = design_bounds(len(designs), world)
     lo, hi = bounds[rank]
-    local = [tuple(r) for r in search_local(list(designs[lo:hi]))] if hi > lo else []
+    exc, local = None, []
+    try:
+        local = [tuple(r) for r in search_local(list(designs[lo:hi]))] if hi > lo else []
+    except Exception as e:  # noqa: BLE001 - re-raised on every rank after the gather
+        if world == 1:
+            raise
+        exc = e
     if world == 1:
         return [(float(q), bool(i), int(n)) for q, i, n in local]
     import torch
     import torch.distributed as td
     width = max(1, max(h - l for l, h in bounds))
-    buf = np.full((width, 3), np.nan)
+    buf = np.full((width + 1, 3), np.nan)
+    buf[0, 0] = _error_code(exc) if exc is not None else 0
     for j, (q, inf, n) in enumerate(local):
-        buf[j] = (q, 1.0 if inf else 0.0, n)
+        buf[1 + j] = (q, 1.0 if inf else 0.0, n)
     t = torch.from_numpy(buf)
     if device is not None:
         t = t.to(device)
     parts = [torch.empty_like(t) for _ in range(world)]
     td.all_gather(parts, t)
-    rows = np.concatenate([p.cpu().numpy()[: h - l] for p, (l, h) in zip(parts, bounds)])
+    parts = [p.cpu().numpy() for p in parts]
+    _raise_remote(np.array([p[0, 0] for p in parts]), rank, exc, "lbt_sharded")
+    rows = np.concatenate([p[1: 1 + h - l] for p, (l, h) in zip(parts, bounds)])
     return [(float(r[0]), bool(r[1]), int(r[2])) for r in rows]

@@ -136,23 +136,40 @@ def c4(gpus: int = 8, seeds: int = 2, queries: float = 2e4, model_name: str = "b
 
 
 # ---- C5: large Monte-Carlo grid: plans x rates x seeds ----
-def c5(n_scenarios: int = 10_000, queries: float = 1e6, seed0: int = 1) -> list[GridSpec]:
+C5_LOADS = (0.3, 0.5, 0.7, 0.8, 0.9)
+C5_PLANS = ("paris", "homog1", "homog2", "homog3", "homog7")
+
+
+def c5_cells() -> list[tuple[str, Model, str, PartitionPlan, float]]:
+    """The 75 (model, plan, load) cells of C5 in grid order: per model its 8-GPU PARIS plan
+    and the homogeneous 1g/2g/3g/7g fleets of 56 GPCs, each at five loads."""
     plans = []
     for name in ("mobilenet", "resnet50", "bert_base"):
         m = model(name)
-        plans.append((m, paris(m, 8)))
+        plans.append((name, m, "paris", paris(m, 8)))
         for k in (1, 2, 3, 7):
-            plans.append((m, homogeneous_plan(k, 56, 8, 7)))
-    loads = (0.3, 0.5, 0.7, 0.8, 0.9)
-    cells = [(m, p, load) for (m, p) in plans for load in loads]
+            plans.append((name, m, f"homog{k}", homogeneous_plan(k, 56, 8, 7)))
+    return [(name, m, tag, p, load) for (name, m, tag, p) in plans for load in C5_LOADS]
+
+
+def c5(n_scenarios: int = 10_000, queries: float = 1e6, seed0: int = 1) -> list[GridSpec]:
+    """Scenario i = cell i mod 75 with seed seed0 + i // 75 (cells interleaved, so any
+    prefix or contiguous shard covers every plan and load)."""
+    cells = c5_cells()
     out = []
-    i = 0
-    while len(out) < n_scenarios:
-        m, p, load = cells[i % len(cells)]
-        rate = load * capacity_qps(m, p)
-        out.append(_spec(m, p, rate, queries, seed0 + i // len(cells)))
-        i += 1
+    for i in range(n_scenarios):
+        _, m, _, p, load = cells[i % len(cells)]
+        out.append(_spec(m, p, load * capacity_qps(m, p), queries, seed0 + i // len(cells)))
     return out
+
+
+def c5_labels(n_scenarios: int = 10_000) -> tuple[list[tuple[str, float]], list[str]]:
+    """Per scenario of c5(): its PARIS decision group (model, load) and candidate plan tag,
+    for `distributed.grouped_argmin` (which plan serves each model and load best by p99)."""
+    cells = c5_cells()
+    group = [(cells[i % len(cells)][0], cells[i % len(cells)][4]) for i in range(n_scenarios)]
+    cand = [cells[i % len(cells)][2] for i in range(n_scenarios)]
+    return group, cand
 
 
 def shard(specs: list, rank: int, world: int) -> list:

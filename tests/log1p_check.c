@@ -52,3 +52,51 @@ int host_variant(void) {
     }
     return g > f ? 0 : 1;
 }
+
+/* Host side of msv_log1p_digest: the same per-chunk digests with this process's libm
+ * log1p (whichever build the ifunc picked), on n_threads threads. */
+#include <pthread.h>
+
+typedef struct {
+    uint64_t seed;
+    long n, chunk, c0, c1;
+    uint64_t* out;
+} digest_job;
+
+static void* digest_worker(void* arg) {
+    digest_job* J = (digest_job*)arg;
+    for (long c = J->c0; c < J->c1; ++c) {
+        uint64_t acc = 0;
+        long hi = (c + 1) * J->chunk < J->n ? (c + 1) * J->chunk : J->n;
+        for (long k = c * J->chunk; k < hi; ++k) {
+            volatile double x = -msv_selftest_input(J->seed, (uint64_t)k);
+            acc += msv_selftest_digest((uint64_t)k, -log1p(x));
+        }
+        J->out[c] = acc;
+    }
+    return 0;
+}
+
+int host_log1p_digest(uint64_t seed, long n, long chunk, uint64_t* out, int n_threads) {
+    long n_chunks = (n + chunk - 1) / chunk;
+    pthread_t th[256];
+    digest_job jobs[256];
+    if (n_threads < 1) n_threads = 1;
+    if (n_threads > 256) n_threads = 256;
+    for (int t = 0; t < n_threads; ++t) {
+        jobs[t].seed = seed;
+        jobs[t].n = n;
+        jobs[t].chunk = chunk;
+        jobs[t].c0 = n_chunks * t / n_threads;
+        jobs[t].c1 = n_chunks * (t + 1) / n_threads;
+        jobs[t].out = out;
+        if (pthread_create(&th[t], 0, digest_worker, &jobs[t])) return -1;
+    }
+    for (int t = 0; t < n_threads; ++t) pthread_join(th[t], 0);
+    return 0;
+}
+
+double host_log1p_value(uint64_t seed, long k) {
+    volatile double x = -msv_selftest_input(seed, (uint64_t)k);
+    return -log1p(x);
+}

@@ -93,14 +93,18 @@ def _log1p_lib():
     out = ROOT / "tests" / "_log1p_check.so"
     hdr = ROOT / "paper_2202_13481_b200" / "csrc" / "msv_math.h"
     if not out.exists() or out.stat().st_mtime < max(src.stat().st_mtime, hdr.stat().st_mtime):
-        subprocess.run(["gcc", "-O2", "-ffp-contract=off", "-fPIC", "-shared", "-o", str(out), str(src), "-lm"],
-                       check=True)
+        subprocess.run(["gcc", "-O2", "-ffp-contract=off", "-fPIC", "-shared", "-o", str(out), str(src), "-lm",
+                        "-lpthread"], check=True)
     L = C.CDLL(str(out))
     L.check_log1p.restype = C.c_long
     L.check_log1p.argtypes = [C.c_int, C.c_long, C.c_uint64]
     L.variants_differ.restype = C.c_long
     L.variants_differ.argtypes = [C.c_long, C.c_uint64]
     L.host_variant.restype = C.c_int
+    L.host_log1p_digest.restype = C.c_int
+    L.host_log1p_digest.argtypes = [C.c_uint64, C.c_long, C.c_long, C.POINTER(C.c_uint64), C.c_int]
+    L.host_log1p_value.restype = C.c_double
+    L.host_log1p_value.argtypes = [C.c_uint64, C.c_long]
     return L
 
 
@@ -179,3 +183,25 @@ def test_shard_partitions_whole_scenarios():
         parts = [W.shard(specs, r, world) for r in range(world)]
         flat = [s for p in parts for s in p]
         assert len(flat) == len(specs) and all(a is b for a, b in zip(flat, specs))
+
+
+# ---------------------------------------------------------------- reference-arm inputs
+@pytest.mark.skipif(not have_ref(), reason="oracle/_ref not built")
+def test_ref_workloads_match_product_workloads():
+    """bench.py's reference arm builds C5 / C2 from oracle/_ref alone (tests/ref_workloads.py);
+    the grids must equal the product's (paper_2202_13481_b200/workloads.py) bit for bit."""
+    from paper_2202_13481_b200 import workloads as W
+    from tests import ref_workloads as R
+
+    for mine, ref in ((W.c5(n_scenarios=300, queries=1e6), R.c5(n_scenarios=300, queries=1e6)),
+                      (W.c2(seeds=3, queries=1e5), R.c2(seeds=3, queries=1e5))):
+        assert len(mine) == len(ref)
+        for a, b in zip(mine, ref):
+            assert a.plan.key() == b.plan.key()
+            assert np.array_equal(a.table.sizes, b.table.sizes) and a.table.b_max == b.table.b_max
+            assert a.table.latency.tobytes() == b.table.latency.tobytes()
+            assert a.table.utilization.tobytes() == b.table.utilization.tobytes()
+            assert np.asarray(a.dist.weights, float).tobytes() == np.asarray(b.dist.weights, float).tobytes()
+            assert (a.sla.sla_target_ms, a.sla.alpha, a.sla.beta) == (b.sla.sla_target_ms, b.sla.alpha, b.sla.beta)
+            assert (a.rate_qps, a.duration_ms, a.seed, a.scheduler, a.warmup_fraction) == \
+                   (b.rate_qps, b.duration_ms, b.seed, b.scheduler, b.warmup_fraction)

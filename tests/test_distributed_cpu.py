@@ -132,3 +132,67 @@ def test_lbt_sharded_matches_single_process():
         p.join(timeout=120)
     for r in range(world):
         assert got[r] == [(float(a), bool(b), int(c)) for a, b, c in want], r
+
+
+def _err_worker(rank, world, port, out_q):
+    import torch.distributed as td
+    from paper_2202_13481_b200 import _native as N
+    from paper_2202_13481_b200.distributed import lbt_sharded, run_sharded
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    td.init_process_group("gloo", rank=rank, world_size=world)
+    specs = list(range(6))  # stand-ins: only the shard split and the failure matter
+
+    class _S:
+        def __init__(self, i):
+            self.rate_qps, self.duration_ms = 1.0, 1000.0
+            self.plan = type("P", (), {"total_instances": lambda self: 1})()
+
+    specs = [_S(i) for i in specs]
+
+    def local(sub):
+        if rank == 1:
+            raise N.LookupError_("profile: batch 40 outside grid 1..32")
+        return {"total": np.ones(len(sub)), "violations": np.zeros(len(sub)), "measured": np.ones(len(sub)),
+                "measured_violations": np.zeros(len(sub)), "tail": np.ones((len(sub), 2)),
+                "horizon_ms": np.ones(len(sub)), "placement_hash": np.zeros(len(sub), np.uint64),
+                "status": np.zeros(len(sub))}
+    got = []
+    for fn in (lambda: run_sharded(specs, local, rank, world),
+               lambda: lbt_sharded(list(range(4)), lambda ds: (_ for _ in ()).throw(N.ParamError("sla <= 0"))
+                                   if rank == 0 else [(1.0, False, 3)] * len(ds), rank, world)):
+        try:
+            fn()
+            got.append("ok")
+        except N.Error as e:
+            got.append(type(e).__name__)
+    out_q.put((rank, got))
+    td.barrier()
+    td.destroy_process_group()
+
+
+def test_sharded_failure_raises_on_every_rank():
+    """ADVICE r1: a rank whose local work raises must not leave the others in the collective;
+    every rank raises the same errors.hpp type."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_err_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    got = dict(q.get(timeout=300) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert got[0] == got[1] == ["LookupError_", "ParamError"]
+
+
+def test_grouped_argmin_seed_order_and_ties():
+    from paper_2202_13481_b200.distributed import grouped_argmin
+    p99 = np.array([3.0, 1.0, 2.0, np.nan, 2.0, 5.0, 1.0, 1.0])
+    group = ["a", "a", "a", "a", "b", "b", "b", "b"]
+    cand = [0, 1, 0, 1, 7, 8, 8, 7]
+    out = grouped_argmin(p99, group, cand)
+    assert out["a"][0] == 1 and out["a"][1] == {0: 2.5, 1: 1.0}
+    assert out["b"][0] == 7 and out["b"][1] == {7: 1.5, 8: 3.0}
+    tie = grouped_argmin(np.array([1.0, 1.0]), ["g", "g"], [5, 4])
+    assert tie["g"][0] == 5  # the candidate seen first wins ties

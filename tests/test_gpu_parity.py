@@ -69,13 +69,65 @@ def test_sample_trace_many_seeds(eng, ref):
     assert_grid_equal(got, want)
 
 
-def test_log1p_variant_probe(eng):
-    import math
-    # the device mirrors whichever glibc build this host's ifunc picked
+def _host_log1p():
+    from tests.test_cpu import _log1p_lib
+    return _log1p_lib()
+
+
+def test_device_log1p_bit_exact_vs_host_libm_1e9(eng):
+    """SURVEY §8(c): the device's glibc-log1p transcription (K1's Rng::exponential,
+    rng.hpp:20) against this host's libm log1p directly, on 1.07e9 inputs of the
+    generator's grid u = m * 2^-53 (uniform, tiny and near-1 u): per 2^20-input chunk a
+    wrapping digest of the result bits, device vs host; any differing chunk is expanded
+    and its first differing input reported."""
+    import ctypes as C
+    from paper_2202_13481_b200 import _native as N
+    L = _host_log1p()
     v = eng.log1p_variant
-    assert v in (0, 1)
-    import ctypes
-    assert math.log1p(-0.5) == math.log1p(-0.5)
+    assert v == L.host_variant()  # msv_create's probe picked the build this host's ifunc picked
+    n, chunk, seed = 1 << 30, 1 << 20, 0x5EED1
+    dev = np.zeros(n // chunk, np.uint64)
+    N.check(N.lib().msv_log1p_digest(eng._h, v, seed, n, chunk, dev.ctypes.data_as(C.POINTER(C.c_uint64))))
+    host = np.zeros_like(dev)
+    threads = len(__import__("os").sched_getaffinity(0))
+    assert L.host_log1p_digest(seed, n, chunk, host.ctypes.data_as(C.POINTER(C.c_uint64)), threads) == 0
+    bad = np.nonzero(dev != host)[0]
+    if len(bad):
+        c = int(bad[0])
+        vals = np.zeros(chunk)
+        N.check(N.lib().msv_log1p_values(eng._h, v, seed, c * chunk, chunk, vals.ctypes.data_as(C.POINTER(C.c_double))))
+        for j in range(chunk):
+            h = L.host_log1p_value(seed, c * chunk + j)
+            assert vals[j].tobytes() == np.float64(h).tobytes(), (c * chunk + j, vals[j], h)
+    assert len(bad) == 0
+
+
+def test_device_log1p_other_build_differs(eng):
+    """The two transcribed builds really differ on this input set (so the check above
+    distinguishes them): the non-selected variant's digests must not all match."""
+    import ctypes as C
+    from paper_2202_13481_b200 import _native as N
+    L = _host_log1p()
+    other = 1 - eng.log1p_variant
+    n, chunk, seed = 1 << 24, 1 << 20, 0x5EED1
+    dev = np.zeros(n // chunk, np.uint64)
+    N.check(N.lib().msv_log1p_digest(eng._h, other, seed, n, chunk, dev.ctypes.data_as(C.POINTER(C.c_uint64))))
+    host = np.zeros_like(dev)
+    assert L.host_log1p_digest(seed, n, chunk, host.ctypes.data_as(C.POINTER(C.c_uint64)), 8) == 0
+    assert (dev != host).any()
+
+
+def test_grouped_trace_quotient_certified(eng):
+    """K1's grouped traces divide through gap_quotient (msv_trace.cuh): a Markstein
+    candidate certified by an exact remainder test, else the IEEE division. 4e9 (gap,
+    rate) pairs — realistic rates and log-uniform rates over [2^-600, 2^600] — must equal
+    the correctly rounded quotient bit for bit."""
+    import ctypes as C
+    from paper_2202_13481_b200 import _native as N
+    counts = np.zeros(2, np.int64)
+    N.check(N.lib().msv_quotient_check(eng._h, 0xD1F, 4_000_000_000, counts.ctypes.data_as(C.POINTER(C.c_int64))))
+    assert counts[0] == 0, counts
+    assert counts[1] < 4_000_000_000 // 1000  # the certificate almost never needs the division
 
 
 # ---------------------------------------------------------------- run() replay, per-query records
