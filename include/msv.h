@@ -113,6 +113,15 @@ typedef struct {
 const char* msv_last_error(void);
 int msv_abi_version(void);
 int msv_create(int device, msv_ctx** out);
+/* A context over several GPUs (member 0 = device_ids[0]; a device may repeat). Uploads
+ * go to it as usual; msv_run_grid, msv_run_replay and the msv_grid_* calls cut their
+ * scenarios into contiguous cost-balanced shards, run one per member concurrently and
+ * gather the per-scenario results in scenario order (the reference's
+ * best_homogeneous fans out with std::async, metrics.hpp:183-209). Timing,
+ * synchronize and counters cover every member; single-scenario calls use member 0. */
+int msv_create_multi(const int* device_ids, int n_devices, msv_ctx** out);
+/* Devices of a context's members (returns the member count; fills up to cap ids). */
+int msv_context_devices(msv_ctx* ctx, int* device_ids, int cap);
 int msv_destroy(msv_ctx* ctx);
 /* Which glibc log1p build the device mirrors for Rng::exponential (rng.hpp:20).
  * AUTO (default) probes the host libm at msv_create(). */

@@ -99,6 +99,8 @@ _SIGNATURES = {
     "msv_last_error": (C.c_char_p, []),
     "msv_abi_version": (C.c_int, []),
     "msv_create": (C.c_int, [C.c_int, C.POINTER(_P)]),
+    "msv_create_multi": (C.c_int, [_i32p, C.c_int, C.POINTER(_P)]),
+    "msv_context_devices": (C.c_int, [_P, _i32p, C.c_int]),
     "msv_destroy": (C.c_int, [_P]),
     "msv_set_log1p_variant": (C.c_int, [_P, C.c_int]),
     "msv_get_log1p_variant": (C.c_int, [_P, C.POINTER(C.c_int)]),
@@ -160,6 +162,8 @@ def lib() -> C.CDLL:
             raise ImportError(f"{LIB_PATH} is missing: run `python -c 'import __graft_entry__ as g; g.build()'`")
         L = C.CDLL(str(LIB_PATH))
         for name, (res, args) in _SIGNATURES.items():
+            if os.environ.get("MSV_LIB") and not hasattr(L, name):
+                continue  # an older A/B build lacks newer entry points
             fn = getattr(L, name)
             fn.restype = res
             fn.argtypes = args

@@ -51,6 +51,26 @@ __device__ __forceinline__ void sts_u32(uint32_t a, uint32_t v) {
     asm volatile("st.shared.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
 }
 
+// (0.0 < x) ? x : 0.0 — Eq. 1's max(0, est - (now - start)) as the reference writes it
+// (std::max(0.0, x), sched.hpp:83): one compare and a 64-bit select (the compiler's own
+// lowering of the pattern goes through fmax with NaN fix-ups and register moves).
+__device__ __forceinline__ double pos_part(double x) {
+    double r;
+    asm("{\n\t.reg .pred p;\n\tsetp.gt.f64 p, %1, 0d0000000000000000;\n\tselp.f64 %0, %1, 0d0000000000000000, p;\n\t}"
+        : "=d"(r)
+        : "d"(x));
+    return r;
+}
+
+// c ? a : b on doubles as one predicated 64-bit select.
+__device__ __forceinline__ double sel_f64(bool c, double a, double b) {
+    double r;
+    asm("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %3, 0;\n\tselp.f64 %0, %1, %2, p;\n\t}"
+        : "=d"(r)
+        : "d"(a), "d"(b), "r"((int)c));
+    return r;
+}
+
 // Order-preserving map of IEEE doubles onto uint64 (total order of finite values).
 __device__ __forceinline__ uint64_t order_key(uint64_t b) { return (b & kSignBit) ? ~b : (b | kSignBit); }
 __device__ __forceinline__ uint64_t order_unkey(uint64_t k) { return (k & kSignBit) ? (k & ~kSignBit) : ~k; }

@@ -8,6 +8,7 @@
 
 #include <algorithm>
 #include <limits>
+#include <atomic>
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
@@ -16,6 +17,7 @@
 #include <numeric>
 #include <string>
 #include <utility>
+#include <thread>
 #include <vector>
 
 #include "msv_internal.h"
@@ -40,6 +42,10 @@ int fail(int code, std::string msg) {
         if (e_ != cudaSuccess) return fail(MSV_CUDA, std::string(#x ": ") + cudaGetErrorString(e_)); \
     } while (0)
 
+// Bumped by every device allocation / free of the engine: free_device_bytes() caches
+// cudaMemGetInfo only while this is unchanged.
+std::atomic<uint64_t> g_alloc_epoch{0};
+
 struct DevBuf {
     void* p = nullptr;
     size_t bytes = 0;
@@ -48,7 +54,10 @@ struct DevBuf {
     DevBuf& operator=(const DevBuf&) = delete;
     ~DevBuf() { release(); }
     void release() {
-        if (p) cudaFree(p);
+        if (p) {
+            cudaFree(p);
+            g_alloc_epoch.fetch_add(1, std::memory_order_relaxed);
+        }
         p = nullptr;
         bytes = 0;
     }
@@ -58,6 +67,7 @@ struct DevBuf {
         if (n == 0) n = 16;
         cudaError_t e = cudaMalloc(&p, n);
         if (e == cudaSuccess) bytes = n;
+        g_alloc_epoch.fetch_add(1, std::memory_order_relaxed);
         return e;
     }
     template <typename T>
@@ -166,6 +176,13 @@ struct msv_ctx {
     std::vector<Dist> dists;
     std::vector<Plan> plans;
     std::vector<Routing> routings;
+    // Multi-device context (msv_create_multi): this context is member 0 (device_ids[0]);
+    // `peers` are members 1..n-1, each a full context on its own device. Uploads go to
+    // this context and are mirrored into the peers before a sharded call
+    // (upload_serial / mirrored_serial); `share` = members on this context's device.
+    std::vector<msv_ctx*> peers;
+    uint64_t upload_serial = 0, mirrored_serial = 0;
+    int share = 1;
     // concatenated profile cells / cdfs on the device
     DevBuf d_lat, d_util, d_cdf, d_pmf, d_guide, d_sizes;
     int n_cells = 0;
@@ -276,6 +293,7 @@ ClassKey class_of(int P, int sched, int seg_w, bool overloaded = false) {
 // (and two slots per lane for 16 < P <= 32) lose to it, so they are never chosen here.
 int wave_seg_width(int64_t n4, int64_t n8, int64_t n16, int sms) {
     if (segmented_mode() == 0) return 32;
+    if (const char* e = getenv("MSV_SEG_WIDTH")) return atoi(e);  // A/B experiments
     const int64_t half_slots = (int64_t)sms * 5 * msv::kSimWarpsPerBlock / 2;
     if (n4 / 8 >= half_slots) return 4;
     if (n8 / 4 >= half_slots) return 8;
@@ -339,6 +357,11 @@ struct msv_grid {
     float t_total = 0, t_trace = 0, t_sim = 0, t_tail = 0;
     int64_t queries = -1;
     std::vector<int64_t> host_n;  // replay: trace lengths
+    std::vector<double> cost;     // expected work per scenario (longest-first order, class shares)
+    // Multi-device grid: one sub-grid per context member, over contiguous scenario
+    // ranges [dev_lo[k], dev_lo[k+1]) (usage slots from dev_use_lo[k]).
+    std::vector<std::unique_ptr<msv_grid>> dev_parts;
+    std::vector<int64_t> dev_lo, dev_use_lo;
 
     ~msv_grid() {
         for (cudaEvent_t& e : ev)
@@ -449,18 +472,22 @@ struct PhaseTimer {
 };
 
 // cudaMemGetInfo costs up to ~10 ms on a busy driver; the wave budget only needs a
-// coarse figure, so it is refreshed at most once per second per thread.
+// coarse figure, so it is refreshed at most once per second per thread — and whenever
+// the engine itself allocated or freed device memory since.
 size_t free_device_bytes() {
     thread_local size_t fr = 0;
     thread_local int dev = -1;
+    thread_local uint64_t epoch = ~0ull;
     thread_local std::chrono::steady_clock::time_point at;
     int cur = 0;
     cudaGetDevice(&cur);
     const auto now = std::chrono::steady_clock::now();
-    if (cur != dev || now - at > std::chrono::seconds(1)) {
+    const uint64_t ep = g_alloc_epoch.load(std::memory_order_relaxed);
+    if (cur != dev || ep != epoch || now - at > std::chrono::seconds(1)) {
         size_t tot = 0;
         cudaMemGetInfo(&fr, &tot);
         dev = cur;
+        epoch = ep;
         at = now;
     }
     return fr;
@@ -526,21 +553,30 @@ int grid_build(msv_ctx* ctx, const msv_scenario* sc, int64_t n, const double* ta
     // batch 4 + link 4 [+ record 24] bytes per query slot).
     const size_t per_q = 16 + (records ? sizeof(msv_record) : 0);
     // Keep enough trace slots resident that a wave of 1e6-query scenarios still fills
-    // every warp slot of the simulation kernel (~4,100 on a B200).
-    size_t budget = free_device_bytes() / 10 * 7;
+    // every warp slot of the simulation kernel (~4,100 on a B200). The budget counts the
+    // trace buffers this grid will reuse (a one-shot call's scratch set is already held by
+    // the context and is not free memory).
+    const size_t held = g->B->d_arr.bytes + g->B->d_bat.bytes + g->B->d_next.bytes + g->B->d_rec.bytes;
+    size_t budget = (free_device_bytes() + held) / 10 * 7 / (size_t)std::max(1, ctx->share);
     if (budget > ((size_t)140 << 30)) budget = (size_t)140 << 30;
     const int64_t max_q = std::max<int64_t>((int64_t)(budget / per_q), 1 << 20);
-    // Long scenarios first inside each wave (work stealing balances the rest).
+    // Waves of equal query counts (a short last wave would leave most warp slots idle
+    // for one scenario's whole run): ceil(total / max_q) waves, each cut near
+    // total / n_waves. Long scenarios first inside each wave (work stealing balances the rest).
     std::vector<int64_t> order(n);
     std::iota(order.begin(), order.end(), 0);
     {
+        int64_t total_q = 0;
+        for (int64_t i = 0; i < n; ++i) total_q += g->cap[i];
+        const int64_t n_waves = std::max<int64_t>(1, (total_q + max_q - 1) / max_q);
+        const int64_t target = (total_q + n_waves - 1) / n_waves;
         int64_t s0 = 0;
         while (s0 < n) {
             msv_grid::Wave w;
             w.s0 = s0;
             int64_t q = 0;
             int64_t s1 = s0;
-            while (s1 < n && (s1 == s0 || q + g->cap[s1] <= max_q)) q += g->cap[s1++];
+            while (s1 < n && (s1 == s0 || (q + g->cap[s1] <= max_q && q < target))) q += g->cap[s1++];
             w.s1 = s1;
             g->waves.push_back(std::move(w));
             s0 = s1;
@@ -708,6 +744,7 @@ int grid_build(msv_ctx* ctx, const msv_scenario* sc, int64_t n, const double* ta
             w.chunks.push_back(std::move(ch));
         }
     }
+    g->cost = cost;
     pt.mark("cost+chunks");
     // Device buffers.
     const size_t wq = (size_t)std::max<int64_t>(g->max_wave_q, 1);
@@ -964,6 +1001,28 @@ int launch_chunk(msv_grid* g, const msv_grid::Chunk& ch, int counter_base, cudaS
         if (!ctx->cls_fork) MSV_CUDA_TRY(cudaEventCreateWithFlags(&ctx->cls_fork, cudaEventDisableTiming));
         MSV_CUDA_TRY(cudaEventRecord(ctx->cls_fork, st));
     }
+    // Optionally, concurrent classes share the device in proportion to their expected time
+    // on it (expected work / the class's relative throughput), to run side by side and end
+    // together in one tail instead of one after another.
+    // Off by default — measured slower on C5 (5.20 vs 5.85 G q/s on a B200): every class
+    // launches full-device persistent grids instead, the largest holds the SMs and the
+    // others fill its last round. MSV_CLASS_SHARES=1 turns the shares on (A/B runs).
+    static const bool class_shares = getenv("MSV_CLASS_SHARES") && atoi(getenv("MSV_CLASS_SHARES")) != 0;
+    std::vector<double> share(ncls, 1.0);
+    if (par && class_shares) {
+        double tot = 0.0;
+        for (size_t c = 0; c < ncls; ++c) {
+            const ClassKey& k = ch.classes[c].first;
+            // relative throughput of a full device of this class (B200, C5 plans: warp kernel
+            // 1 slot ~9 G q/s, 2 slots ~5.1, 4 slots ~2.5, segmented W=8 ~12, W=4 ~15)
+            const double rel = k.W == 4 ? 1.6 : k.W == 8 ? 1.33 : k.W == 16 ? 1.0 : k.S == 1 ? 1.0 : k.S == 2 ? 0.57 : 0.28;
+            double w = 0.0;
+            for (int32_t si : ch.classes[c].second) w += g->cost.empty() ? 1.0 : g->cost[si];
+            share[c] = w / rel;
+            tot += share[c];
+        }
+        for (double& v : share) v = tot > 0.0 ? v / tot : 1.0;
+    }
     for (size_t ci = 0; ci < ncls; ++ci) {
         const size_t c = corder[ci];
         cudaStream_t cs = (par && ci > 0) ? ctx->cls[(ci - 1) % 4] : st;
@@ -995,7 +1054,8 @@ int launch_chunk(msv_grid* g, const msv_grid::Chunk& ch, int counter_base, cudaS
         const int need = (nwork + segs_per_block - 1) / segs_per_block;
         int occ_used = occ;
         if (const char* e = getenv("MSV_SIM_BLOCK_SLACK")) occ_used = std::max(1, occ - atoi(e));
-        const int blocks = std::max(1, std::min(need, occ_used * ctx->sms));
+        const int dev_blocks = std::max(1, (int)std::lround(share[c] * occ_used * ctx->sms));
+        const int blocks = std::max(1, std::min(need, dev_blocks));
         MSV_CUDA_TRY(msv::launch_sim(k.W, k.S, k.sched, g->records, p, blocks, cs));
         debug_sync(cs, "sim");
         ctx->launches += 1;
@@ -1227,6 +1287,8 @@ int msv_create(int device, msv_ctx** out) {
 
 int msv_destroy(msv_ctx* ctx) {
     if (!ctx) return MSV_OK;
+    for (msv_ctx* p : ctx->peers) msv_destroy(p);
+    ctx->peers.clear();
     SetDevice sd(ctx->device);
     cudaStreamSynchronize(ctx->stream);
     for (cudaEvent_t e : ctx->ev)
@@ -1261,6 +1323,7 @@ int msv_set_log1p_variant(msv_ctx* ctx, int variant) {
     if (variant != MSV_LOG1P_GENERIC && variant != MSV_LOG1P_FMA)
         return fail(MSV_PARAM, "msv_set_log1p_variant: unknown variant");
     ctx->log1p = variant;
+    ctx->upload_serial++;
     return MSV_OK;
 }
 
@@ -1274,6 +1337,7 @@ int msv_get_log1p_variant(msv_ctx* ctx, int* variant) {
 int msv_upload_profile(msv_ctx* ctx, int n_sizes, const int32_t* sizes, int b_max, const double* latency_ms,
                        const double* utilization, int32_t* handle) {
     if (!ctx || !handle) return fail(MSV_PARAM, "null argument");
+    ctx->upload_serial++;
     if (n_sizes <= 0) return fail(MSV_PARAM, "profile: empty size set");
     if (b_max < 1) return fail(MSV_PARAM, "profile: b_max must be >= 1");
     Profile p;
@@ -1313,6 +1377,7 @@ int msv_upload_profile(msv_ctx* ctx, int n_sizes, const int32_t* sizes, int b_ma
 // BatchDistribution(weights) (workload.hpp:25-38).
 int msv_upload_dist(msv_ctx* ctx, int b_max, const double* weights, int32_t* handle) {
     if (!ctx || !handle) return fail(MSV_PARAM, "null argument");
+    ctx->upload_serial++;
     if (b_max <= 0) return fail(MSV_PARAM, "batch distribution: empty support");
     Dist d;
     d.pmf.assign(weights, weights + b_max);
@@ -1338,6 +1403,7 @@ int msv_upload_dist(msv_ctx* ctx, int b_max, const double* weights, int32_t* han
 
 int msv_upload_cdf(msv_ctx* ctx, int b_max, const double* cdf, int32_t* handle) {
     if (!ctx || !handle || !cdf) return fail(MSV_PARAM, "null argument");
+    ctx->upload_serial++;
     if (b_max <= 0) return fail(MSV_PARAM, "batch distribution: empty support");
     Dist d;
     d.cdf.assign(cdf, cdf + b_max);
@@ -1358,6 +1424,7 @@ int msv_upload_cdf(msv_ctx* ctx, int b_max, const double* cdf, int32_t* handle) 
 int msv_upload_plan(msv_ctx* ctx, int num_gpus, int gpcs_per_gpu, const int32_t* n_per_gpu,
                     const int32_t* sizes_flat, int32_t* handle) {
     if (!ctx || !handle) return fail(MSV_PARAM, "null argument");
+    ctx->upload_serial++;
     Plan p;
     p.num_gpus = num_gpus;
     p.gpcs_per_gpu = gpcs_per_gpu;
@@ -1394,6 +1461,7 @@ int msv_upload_plan(msv_ctx* ctx, int num_gpus, int gpcs_per_gpu, const int32_t*
 int msv_upload_routing(msv_ctx* ctx, int n_segments, const int32_t* k, const int32_t* first,
                        const int32_t* last, int32_t* handle) {
     if (!ctx || !handle) return fail(MSV_PARAM, "null argument");
+    ctx->upload_serial++;
     if (n_segments < 0) return fail(MSV_PARAM, "routing: negative segment count");
     Routing r;
     r.k.assign(k, k + n_segments);
@@ -1404,8 +1472,8 @@ int msv_upload_routing(msv_ctx* ctx, int n_segments, const int32_t* k, const int
     return MSV_OK;
 }
 
-int msv_grid_create(msv_ctx* ctx, const msv_scenario* scenarios, int64_t n, const double* tail_p, int n_tails,
-                    msv_grid** out) {
+static int grid_create_dev(msv_ctx* ctx, const msv_scenario* scenarios, int64_t n, const double* tail_p, int n_tails,
+                           msv_grid** out) {
     if (!ctx || !out || (n > 0 && !scenarios)) return fail(MSV_PARAM, "null argument");
     SetDevice sd(ctx->device);
     std::vector<std::vector<int64_t>> groups;
@@ -1441,7 +1509,7 @@ int msv_grid_create(msv_ctx* ctx, const msv_scenario* scenarios, int64_t n, cons
     return MSV_OK;
 }
 
-int msv_grid_launch(msv_grid* grid) {
+static int grid_launch_dev(msv_grid* grid) {
     if (!grid) return fail(MSV_PARAM, "null grid");
     SetDevice sd(grid->ctx->device);
     if (grid->parts.empty()) return grid_launch(grid);
@@ -1457,7 +1525,7 @@ int msv_grid_launch(msv_grid* grid) {
     return MSV_OK;
 }
 
-int msv_grid_results(msv_grid* grid, msv_result* results, msv_usage* usage) {
+static int grid_results_dev(msv_grid* grid, msv_result* results, msv_usage* usage) {
     if (!grid || (grid->n > 0 && !results)) return fail(MSV_PARAM, "null argument");
     SetDevice sd(grid->ctx->device);
     if (grid->parts.empty()) return grid_results(grid, results, usage, nullptr, nullptr);
@@ -1478,15 +1546,7 @@ int msv_grid_results(msv_grid* grid, msv_result* results, msv_usage* usage) {
     return MSV_OK;
 }
 
-int msv_grid_destroy(msv_grid* grid) {
-    if (!grid) return MSV_OK;
-    SetDevice sd(grid->ctx->device);
-    cudaStreamSynchronize(grid->ctx->stream);
-    delete grid;
-    return MSV_OK;
-}
-
-int msv_grid_timing(msv_grid* g, float* total_ms, float* trace_ms, float* sim_ms, float* tail_ms) {
+static int grid_timing_dev(msv_grid* g, float* total_ms, float* trace_ms, float* sim_ms, float* tail_ms) {
     if (!g) return fail(MSV_PARAM, "null grid");
     SetDevice sd(g->ctx->device);
     if (g->t_total == -2.0f) {  // overlapped chunks: only the total is defined
@@ -1519,13 +1579,13 @@ int msv_grid_set_overlap(msv_grid* g, int on) {
     return MSV_OK;
 }
 
-int64_t msv_grid_queries(msv_grid* g) {
+static int64_t grid_queries_dev(msv_grid* g) {
     if (!g) return -1;
     SetDevice sd(g->ctx->device);
     if (!g->parts.empty()) {
         int64_t t = 0;
         for (std::unique_ptr<msv_grid>& part : g->parts) {
-            const int64_t q = msv_grid_queries(part.get());
+            const int64_t q = grid_queries_dev(part.get());
             if (q < 0) return -1;
             t += q;
         }
@@ -1541,15 +1601,30 @@ int64_t msv_grid_queries(msv_grid* g) {
 
 int msv_synchronize(msv_ctx* ctx) {
     if (!ctx) return fail(MSV_PARAM, "null context");
+    for (msv_ctx* p : ctx->peers) {
+        const int rc = msv_synchronize(p);
+        if (rc) return rc;
+    }
     SetDevice sd(ctx->device);
     MSV_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
     return MSV_OK;
 }
 
-int64_t msv_kernel_launches(msv_ctx* ctx) { return ctx ? ctx->launches : -1; }
+int64_t msv_kernel_launches(msv_ctx* ctx) {
+    if (!ctx) return -1;
+    int64_t n = ctx->launches;
+    for (msv_ctx* p : ctx->peers) n += p->launches;
+    return n;
+}
 
+// Events on every member's stream; elapsed = the max over the members (multi-device
+// timings are the slowest device's, never a host clock).
 int msv_event_record(msv_ctx* ctx, int slot) {
     if (!ctx || slot < 0 || slot >= 8) return fail(MSV_PARAM, "msv_event_record: bad slot");
+    for (msv_ctx* p : ctx->peers) {
+        const int rc = msv_event_record(p, slot);
+        if (rc) return rc;
+    }
     SetDevice sd(ctx->device);
     if (!ctx->ev[slot]) MSV_CUDA_TRY(cudaEventCreate(&ctx->ev[slot]));
     MSV_CUDA_TRY(cudaEventRecord(ctx->ev[slot], ctx->stream));
@@ -1560,16 +1635,29 @@ int msv_event_record(msv_ctx* ctx, int slot) {
 int msv_event_elapsed(msv_ctx* ctx, int a, int b, float* ms) {
     if (!ctx || !ms || a < 0 || a >= 8 || b < 0 || b >= 8 || !ctx->ev[a] || !ctx->ev[b])
         return fail(MSV_PARAM, "msv_event_elapsed: bad slot");
+    float worst = 0.0f;
+    for (msv_ctx* p : ctx->peers) {
+        float t = 0.0f;
+        const int rc = msv_event_elapsed(p, a, b, &t);
+        if (rc) return rc;
+        worst = std::max(worst, t);
+    }
     SetDevice sd(ctx->device);
     MSV_CUDA_TRY(cudaEventSynchronize(ctx->ev[b]));
     MSV_CUDA_TRY(cudaEventElapsedTime(ms, ctx->ev[a], ctx->ev[b]));
+    *ms = std::max(*ms, worst);
     return MSV_OK;
 }
 
 int msv_transfer_bytes(msv_ctx* ctx, int64_t* h2d, int64_t* d2h) {
     if (!ctx) return fail(MSV_PARAM, "null context");
-    if (h2d) *h2d = ctx->h2d;
-    if (d2h) *d2h = ctx->d2h;
+    int64_t a = ctx->h2d, b = ctx->d2h;
+    for (msv_ctx* p : ctx->peers) {
+        a += p->h2d;
+        b += p->d2h;
+    }
+    if (h2d) *h2d = a;
+    if (d2h) *d2h = b;
     return MSV_OK;
 }
 
@@ -1584,8 +1672,8 @@ int run_grid_core(msv_ctx* ctx, const msv_scenario* scenarios, int64_t n, const 
 
 extern "C" {
 
-int msv_run_grid(msv_ctx* ctx, const msv_scenario* scenarios, int64_t n, const double* tail_p, int n_tails,
-                 msv_result* results, msv_usage* usage) {
+static int run_grid_dev(msv_ctx* ctx, const msv_scenario* scenarios, int64_t n, const double* tail_p, int n_tails,
+                        msv_result* results, msv_usage* usage) {
     if (!ctx || (n > 0 && (!scenarios || !results))) return fail(MSV_PARAM, "null argument");
     SetDevice sd(ctx->device);
     std::vector<std::vector<int64_t>> groups;
@@ -1699,9 +1787,9 @@ int run_grid_core(msv_ctx* ctx, const msv_scenario* scenarios, int64_t n, const 
 
 extern "C" {
 
-int msv_run_replay(msv_ctx* ctx, const msv_scenario* scenarios, int64_t n, const int64_t* offsets,
-                   const double* arrival_ms, const int32_t* batch, const double* tail_p, int n_tails,
-                   msv_result* results, msv_usage* usage, msv_record* records) {
+static int run_replay_dev(msv_ctx* ctx, const msv_scenario* scenarios, int64_t n, const int64_t* offsets,
+                          const double* arrival_ms, const int32_t* batch, const double* tail_p, int n_tails,
+                          msv_result* results, msv_usage* usage, msv_record* records) {
     if (!ctx || (n > 0 && (!scenarios || !results || !offsets))) return fail(MSV_PARAM, "null argument");
     SetDevice sd(ctx->device);
     std::vector<std::vector<int64_t>> groups;
@@ -1732,7 +1820,7 @@ int msv_run_replay(msv_ctx* ctx, const msv_scenario* scenarios, int64_t n, const
             std::vector<msv_result> sub_res(sub.size());
             std::vector<msv_usage> sub_use(std::max<int64_t>(nu, 1));
             std::vector<msv_record> sub_rec(std::max<size_t>(arr.size(), 1));
-            const int rc = msv_run_replay(ctx, sub.data(), (int64_t)sub.size(), off.data(), arr.data(), bat.data(), tail_p,
+            const int rc = run_replay_dev(ctx, sub.data(), (int64_t)sub.size(), off.data(), arr.data(), bat.data(), tail_p,
                                           n_tails, sub_res.data(), usage ? sub_use.data() : nullptr,
                                           records ? sub_rec.data() : nullptr);
             if (rc) return rc;
@@ -2149,3 +2237,256 @@ int msv_quotient_check(msv_ctx* ctx, uint64_t seed, int64_t n, int64_t* counts) 
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------------------------
+// Multi-device contexts (msv_create_multi). Scenarios are independent,
+// so a grid is cut into contiguous, cost-balanced shards — one per member context, each
+// on its own GPU — run concurrently (one host thread per member, no device-to-device
+// traffic), and the fixed-size per-scenario results are gathered into the caller's
+// arrays in scenario order. The reference fans best_homogeneous out the same way with
+// std::async (metrics.hpp:183-209); here every batch entry point does.
+// ---------------------------------------------------------------------------------
+namespace {
+
+std::vector<msv_ctx*> members(msv_ctx* ctx) {
+    std::vector<msv_ctx*> m{ctx};
+    m.insert(m.end(), ctx->peers.begin(), ctx->peers.end());
+    return m;
+}
+
+// Mirror the primary's uploads (host copies; device tables re-synced lazily).
+void sync_peers(msv_ctx* ctx) {
+    if (ctx->mirrored_serial == ctx->upload_serial) return;
+    for (msv_ctx* p : ctx->peers) {
+        p->profiles = ctx->profiles;
+        p->dists = ctx->dists;
+        p->plans = ctx->plans;
+        p->routings = ctx->routings;
+        p->log1p = ctx->log1p;
+        p->tables_dirty = true;
+    }
+    ctx->mirrored_serial = ctx->upload_serial;
+}
+
+// Contiguous shards of [0, n) with about equal cost (expected queries x (P + 1)); the
+// same cut distributed.shard makes for one-process-per-GPU runs.
+std::vector<int64_t> shard_cuts(const msv_ctx* ctx, const msv_scenario* sc, int64_t n, const int64_t* offsets,
+                                int parts) {
+    std::vector<double> cum(n + 1, 0.0);
+    for (int64_t i = 0; i < n; ++i) {
+        const msv_scenario& s = sc[i];
+        const double q = offsets ? (double)(offsets[i + 1] - offsets[i]) : s.rate_qps * s.duration_ms / 1000.0;
+        const double P = (s.plan >= 0 && s.plan < (int)ctx->plans.size()) ? (double)ctx->plans[s.plan].flat.size() : 1.0;
+        cum[i + 1] = cum[i] + (q > 0.0 ? q : 0.0) * (P + 1.0) + 1e-9;
+    }
+    std::vector<int64_t> cut(parts + 1, 0);
+    cut[parts] = n;
+    for (int k = 1; k < parts; ++k) {
+        const double target = cum[n] * k / parts;
+        cut[k] = std::upper_bound(cum.begin(), cum.end(), target) - cum.begin() - 1;
+        cut[k] = std::max(cut[k], cut[k - 1]);
+    }
+    return cut;
+}
+
+// Run fn(member k, shard k) for every member concurrently (member 0 on this thread);
+// returns the first failing member's status with its message.
+template <typename Fn>
+int fan_out(const std::vector<msv_ctx*>& m, Fn fn) {
+    std::vector<int> rc(m.size(), MSV_OK);
+    std::vector<std::string> err(m.size());
+    std::vector<std::thread> th;
+    for (size_t k = 1; k < m.size(); ++k)
+        th.emplace_back([&, k] {
+            rc[k] = fn(k);
+            if (rc[k]) err[k] = g_err;
+        });
+    rc[0] = fn(0);
+    if (rc[0]) err[0] = g_err;
+    for (std::thread& t : th) t.join();
+    for (size_t k = 0; k < m.size(); ++k)
+        if (rc[k]) return fail(rc[k], "device " + std::to_string(m[k]->device) + " (member " + std::to_string(k) +
+                                          "): " + err[k]);
+    return MSV_OK;
+}
+
+// Usage slots before scenario i (Σ P over earlier scenarios).
+std::vector<int64_t> usage_prefix(const msv_ctx* ctx, const msv_scenario* sc, int64_t n) {
+    std::vector<int64_t> u(n + 1, 0);
+    for (int64_t i = 0; i < n; ++i) {
+        const int p = sc[i].plan;
+        u[i + 1] = u[i] + ((p >= 0 && p < (int)ctx->plans.size()) ? (int64_t)ctx->plans[p].flat.size() : 0);
+    }
+    return u;
+}
+
+}  // namespace
+
+extern "C" {
+
+int msv_create_multi(const int* device_ids, int n_devices, msv_ctx** out) {
+    if (!out || !device_ids || n_devices < 1) return fail(MSV_PARAM, "msv_create_multi: need >= 1 device");
+    *out = nullptr;
+    msv_ctx* primary = nullptr;
+    int rc = msv_create(device_ids[0], &primary);
+    if (rc) return rc;
+    std::unique_ptr<msv_ctx, int (*)(msv_ctx*)> guard(primary, msv_destroy);
+    for (int k = 1; k < n_devices; ++k) {
+        msv_ctx* p = nullptr;
+        rc = msv_create(device_ids[k], &p);
+        if (rc) return rc;
+        primary->peers.push_back(p);
+    }
+    for (msv_ctx* a : members(primary)) {
+        a->share = 0;
+        for (msv_ctx* b : members(primary)) a->share += a->device == b->device;
+    }
+    *out = guard.release();
+    return MSV_OK;
+}
+
+int msv_context_devices(msv_ctx* ctx, int* device_ids, int cap) {
+    if (!ctx) return fail(MSV_PARAM, "null context");
+    const std::vector<msv_ctx*> m = members(ctx);
+    for (int k = 0; k < (int)m.size() && k < cap; ++k) device_ids[k] = m[k]->device;
+    return (int)m.size();
+}
+
+int msv_run_grid(msv_ctx* ctx, const msv_scenario* scenarios, int64_t n, const double* tail_p, int n_tails,
+                 msv_result* results, msv_usage* usage) {
+    if (!ctx || (n > 0 && (!scenarios || !results))) return fail(MSV_PARAM, "null argument");
+    if (ctx->peers.empty()) return run_grid_dev(ctx, scenarios, n, tail_p, n_tails, results, usage);
+    sync_peers(ctx);
+    const std::vector<msv_ctx*> m = members(ctx);
+    const std::vector<int64_t> cut = shard_cuts(ctx, scenarios, n, nullptr, (int)m.size());
+    const std::vector<int64_t> uo = usage_prefix(ctx, scenarios, n);
+    return fan_out(m, [&](size_t k) {
+        const int64_t lo = cut[k], hi = cut[k + 1];
+        if (hi <= lo) return (int)MSV_OK;
+        return run_grid_dev(m[k], scenarios + lo, hi - lo, tail_p, n_tails, results + lo,
+                            usage ? usage + uo[lo] : nullptr);
+    });
+}
+
+int msv_run_replay(msv_ctx* ctx, const msv_scenario* scenarios, int64_t n, const int64_t* offsets,
+                   const double* arrival_ms, const int32_t* batch, const double* tail_p, int n_tails,
+                   msv_result* results, msv_usage* usage, msv_record* records) {
+    if (!ctx || (n > 0 && (!scenarios || !results || !offsets))) return fail(MSV_PARAM, "null argument");
+    if (ctx->peers.empty())
+        return run_replay_dev(ctx, scenarios, n, offsets, arrival_ms, batch, tail_p, n_tails, results, usage, records);
+    sync_peers(ctx);
+    const std::vector<msv_ctx*> m = members(ctx);
+    const std::vector<int64_t> cut = shard_cuts(ctx, scenarios, n, offsets, (int)m.size());
+    const std::vector<int64_t> uo = usage_prefix(ctx, scenarios, n);
+    return fan_out(m, [&](size_t k) {
+        const int64_t lo = cut[k], hi = cut[k + 1];
+        if (hi <= lo) return (int)MSV_OK;
+        std::vector<int64_t> off(offsets + lo, offsets + hi + 1);  // rebased: the shard's traces start at 0
+        const int64_t q0 = off[0];
+        for (int64_t& o : off) o -= q0;
+        return run_replay_dev(m[k], scenarios + lo, hi - lo, off.data(), arrival_ms + q0, batch + q0, tail_p, n_tails,
+                              results + lo, usage ? usage + uo[lo] : nullptr, records ? records + q0 : nullptr);
+    });
+}
+
+int msv_grid_create(msv_ctx* ctx, const msv_scenario* scenarios, int64_t n, const double* tail_p, int n_tails,
+                    msv_grid** out) {
+    if (!ctx || !out || (n > 0 && !scenarios)) return fail(MSV_PARAM, "null argument");
+    if (ctx->peers.empty()) return grid_create_dev(ctx, scenarios, n, tail_p, n_tails, out);
+    sync_peers(ctx);
+    const std::vector<msv_ctx*> m = members(ctx);
+    std::unique_ptr<msv_grid> top(new msv_grid);
+    top->ctx = ctx;
+    top->n = n;
+    top->tail_p.assign(tail_p, tail_p + std::max(n_tails, 0));
+    top->dev_lo = shard_cuts(ctx, scenarios, n, nullptr, (int)m.size());
+    const std::vector<int64_t> uo = usage_prefix(ctx, scenarios, n);
+    for (size_t k = 0; k < m.size(); ++k) top->dev_use_lo.push_back(uo[top->dev_lo[k]]);
+    top->usage_total = uo[n];
+    top->dev_parts.resize(m.size());
+    const int rc = fan_out(m, [&](size_t k) {
+        msv_grid* g = nullptr;
+        const int64_t lo = top->dev_lo[k], hi = top->dev_lo[k + 1];
+        const int r = grid_create_dev(m[k], scenarios + lo, hi - lo, tail_p, n_tails, &g);
+        top->dev_parts[k].reset(g);
+        return r;
+    });
+    if (rc) {
+        for (size_t k = 0; k < m.size(); ++k) {
+            SetDevice sd(m[k]->device);
+            top->dev_parts[k].reset();
+        }
+        return rc;
+    }
+    *out = top.release();
+    return MSV_OK;
+}
+
+int msv_grid_launch(msv_grid* grid) {
+    if (!grid) return fail(MSV_PARAM, "null grid");
+    if (grid->dev_parts.empty()) return grid_launch_dev(grid);
+    for (std::unique_ptr<msv_grid>& p : grid->dev_parts) {  // asynchronous: every device runs at once
+        p->usage = grid->usage;
+        p->overlap = grid->overlap;
+        const int rc = grid_launch_dev(p.get());
+        if (rc) return rc;
+    }
+    return MSV_OK;
+}
+
+int msv_grid_results(msv_grid* grid, msv_result* results, msv_usage* usage) {
+    if (!grid || (grid->n > 0 && !results)) return fail(MSV_PARAM, "null argument");
+    if (grid->dev_parts.empty()) return grid_results_dev(grid, results, usage);
+    for (size_t k = 0; k < grid->dev_parts.size(); ++k) {
+        const int rc = grid_results_dev(grid->dev_parts[k].get(), results + grid->dev_lo[k],
+                                        usage ? usage + grid->dev_use_lo[k] : nullptr);
+        if (rc) return rc;
+    }
+    return MSV_OK;
+}
+
+int msv_grid_destroy(msv_grid* grid) {
+    if (!grid) return MSV_OK;
+    for (std::unique_ptr<msv_grid>& p : grid->dev_parts) {
+        SetDevice sd(p->ctx->device);
+        cudaStreamSynchronize(p->ctx->stream);
+        p.reset();
+    }
+    SetDevice sd(grid->ctx->device);
+    cudaStreamSynchronize(grid->ctx->stream);
+    delete grid;
+    return MSV_OK;
+}
+
+// Multi-device grids: each stage is the max over the devices (they run concurrently).
+int msv_grid_timing(msv_grid* g, float* total_ms, float* trace_ms, float* sim_ms, float* tail_ms) {
+    if (!g) return fail(MSV_PARAM, "null grid");
+    if (g->dev_parts.empty()) return grid_timing_dev(g, total_ms, trace_ms, sim_ms, tail_ms);
+    float t[4] = {0, 0, 0, 0};
+    for (std::unique_ptr<msv_grid>& p : g->dev_parts) {
+        float v[4] = {0, 0, 0, 0};
+        const int rc = grid_timing_dev(p.get(), &v[0], &v[1], &v[2], &v[3]);
+        if (rc) return rc;
+        for (int j = 0; j < 4; ++j) t[j] = std::max(t[j], v[j]);
+    }
+    if (total_ms) *total_ms = t[0];
+    if (trace_ms) *trace_ms = t[1];
+    if (sim_ms) *sim_ms = t[2];
+    if (tail_ms) *tail_ms = t[3];
+    return MSV_OK;
+}
+
+int64_t msv_grid_queries(msv_grid* g) {
+    if (!g) return -1;
+    if (g->dev_parts.empty()) return grid_queries_dev(g);
+    int64_t t = 0;
+    for (std::unique_ptr<msv_grid>& p : g->dev_parts) {
+        const int64_t q = grid_queries_dev(p.get());
+        if (q < 0) return -1;
+        t += q;
+    }
+    return t;
+}
+
+}  // extern "C"
+

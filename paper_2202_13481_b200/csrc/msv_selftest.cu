@@ -57,10 +57,9 @@ __global__ void quotient_check_kernel(uint64_t seed, int64_t n, unsigned long lo
         const double r = ldexp(1.0 + (double)(z >> 12) * 0x1.0p-52, e);
         const double q = gap_quotient(l, r, 1.0 / r);
         bad += msv_dbits(q) != msv_dbits(__ddiv_rn(l, r));
-        // the candidate before certification, to report how often the fallback runs
-        const double q0 = l * (1.0 / r);
-        const double c = __fma_rn(__fma_rn(-r, q0, l), 1.0 / r, q0);
-        fb += msv_dbits(c) != msv_dbits(q) || (msv_dbits(q) & 0x000FFFFFFFFFFFFFull) == 0;
+        bool ok;  // how often the certificate sends the quotient to the division
+        (void)gap_quotient_candidate(l, r, 1.0 / r, ok);
+        fb += ok ? 0 : 1;
     }
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) {

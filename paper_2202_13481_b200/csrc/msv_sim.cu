@@ -89,8 +89,9 @@ __global__ void __launch_bounds__(kSimWarpsPerBlock * 32, (SegCfg<W, S>::min_blo
     bool unit = true, check_wait = false;
     int bmax = 0;
     // ---- per-lane partition slots ----
-    // c_* = the query running at the last arrival; tail = finish of the query placed last
-    bool act[S], busy[S];
+    // c_* = the query running at the last arrival; tail = finish of the query placed last.
+    // An idle slot holds c_start = -inf, c_est = 0, c_comp = +inf (msv_sim_warp.cu).
+    bool act[S];
     int32_t row[S], pk[S], qh[S], qn[S];
     uint32_t gn[S], nq[S];
     double c_start[S], c_est[S], c_comp[S], tail[S], fold[S], bms[S], wbms[S];
@@ -99,10 +100,13 @@ __global__ void __launch_bounds__(kSimWarpsPerBlock * 32, (SegCfg<W, S>::min_blo
     double wdiff = 0.0;
 #pragma unroll
     for (int s = 0; s < S; ++s) {
-        act[s] = busy[s] = false;
+        act[s] = false;
         row[s] = pk[s] = qh[s] = qn[s] = 0;
         gn[s] = nq[s] = 0;
-        c_start[s] = c_est[s] = c_comp[s] = tail[s] = fold[s] = bms[s] = wbms[s] = 0.0;
+        c_start[s] = -INFINITY;
+        c_est[s] = 0.0;
+        c_comp[s] = INFINITY;
+        tail[s] = fold[s] = bms[s] = wbms[s] = 0.0;
     }
 
     // Async copy of arrivals [from, from+32) into the segment's window buffer b.
@@ -175,10 +179,12 @@ __global__ void __launch_bounds__(kSimWarpsPerBlock * 32, (SegCfg<W, S>::min_blo
                         pk[s] = dp.pid | (dp.k << 8);
                         row[s] = dp.row;
                     }
-                    busy[s] = false;
                     qh[s] = qn[s] = 0;
                     gn[s] = nq[s] = 0;
-                    c_start[s] = c_est[s] = c_comp[s] = tail[s] = 0.0;
+                    c_start[s] = -INFINITY;
+                    c_est[s] = 0.0;
+                    c_comp[s] = INFINITY;
+                    tail[s] = 0.0;
                     fold[s] = bms[s] = wbms[s] = 0.0;
                 }
                 viol = mviol = 0;
@@ -226,7 +232,7 @@ __global__ void __launch_bounds__(kSimWarpsPerBlock * 32, (SegCfg<W, S>::min_blo
         // ---- 1. advance to t, lane-local, in chain order (engine.hpp:167-187) ----
 #pragma unroll
         for (int s = 0; s < S; ++s) {
-            while (busy[s] && c_comp[s] <= t) {
+            while (c_comp[s] <= t) {  // (idle: +inf, never)
                 if (qn[s] > 0) {  // start the queue head at the finish (engine.hpp:181-185)
                     const int h = qh[s];
                     const double est = M.q_est[s][h][lane];
@@ -243,8 +249,10 @@ __global__ void __launch_bounds__(kSimWarpsPerBlock * 32, (SegCfg<W, S>::min_blo
                     c_est[s] = est;
                     c_comp[s] = c_start[s] + est;  // the placement computed the same sum
                     if (kFold) fold[s] = refold(s);
-                } else {
-                    busy[s] = false;
+                } else {  // idle
+                    c_start[s] = -INFINITY;
+                    c_est[s] = 0.0;
+                    c_comp[s] = INFINITY;
                     fold[s] = 0.0;
                 }
             }
@@ -262,7 +270,7 @@ __global__ void __launch_bounds__(kSimWarpsPerBlock * 32, (SegCfg<W, S>::min_blo
         for (int s = 0; s < S; ++s) {
             cand[s] = go && act[s];
             const double x = c_est[s] - (t - c_start[s]);
-            wv[s] = fold[s] + ((busy[s] && 0.0 < x) ? x : 0.0);  // Eq. 1 (sched.hpp:77-85)
+            wv[s] = fold[s] + pos_part(x);  // Eq. 1 (sched.hpp:77-85); idle: x = -inf
             bad[s] = false;
         }
         int bad_o = 1 << 30;  // segment order index of the first candidate whose size is missing
@@ -291,7 +299,7 @@ __global__ void __launch_bounds__(kSimWarpsPerBlock * 32, (SegCfg<W, S>::min_blo
                 for (int s = 0; s < S; ++s) {
                     if (!cand[s] || bad[s]) continue;
                     const double y = c_comp[s] - t;
-                    const double gw = fold[s] + ((busy[s] && 0.0 < y) ? y : 0.0);
+                    const double gw = fold[s] + ((c_comp[s] < INFINITY && 0.0 < y) ? y : 0.0);
                     const double dd = fabs(gw - wv[s]);
                     wdiff = (wdiff < dd) ? dd : wdiff;
                 }
@@ -340,7 +348,7 @@ __global__ void __launch_bounds__(kSimWarpsPerBlock * 32, (SegCfg<W, S>::min_blo
             uint32_t li = ~0u, lq = ~0u;
 #pragma unroll
             for (int s = 0; s < S; ++s) {
-                ki[s] = (cand[s] && !busy[s]) ? (((0x7FFFu - ((uint32_t)pk[s] >> 8)) << 16) | ((uint32_t)pk[s] & 0xffu))
+                ki[s] = (cand[s] && c_comp[s] == INFINITY) ? (((0x7FFFu - ((uint32_t)pk[s] >> 8)) << 16) | ((uint32_t)pk[s] & 0xffu))
                                               : ~0u;
                 const uint32_t len = (uint32_t)qn[s] + gn[s];
                 kq[s] = cand[s] ? (((len < 0xFFFFFFu ? len : 0xFFFFFFu) << 8) | ((uint32_t)pk[s] & 0xffu)) : ~0u;
@@ -376,8 +384,7 @@ __global__ void __launch_bounds__(kSimWarpsPerBlock * 32, (SegCfg<W, S>::min_blo
             if (go && s * W + sl == ch) {
                 const double est = est_n[s];
                 double st, fin;
-                if (!busy[s]) {
-                    busy[s] = true;
+                if (c_comp[s] == INFINITY) {  // idle: starts now
                     st = t;
                     fin = t + est;
                     c_start[s] = t;

@@ -131,8 +131,11 @@ __global__ void __launch_bounds__(kSimWarpsPerBlock * 32, WarpCfg<S>::min_blocks
 
         // ---- lane slots ----
         // c_* = the query running at the last arrival; tail = finish of the query placed
-        // last (== c_comp while the FIFO is empty): the start of the next one queued
-        bool act[S], busy[S];
+        // last (== c_comp while the FIFO is empty): the start of the next one queued.
+        // An idle slot holds c_start = -inf, c_est = 0, c_comp = +inf: its Eq. 1 term
+        // est - (now - start) is -inf (no max(0, .) select on a busy flag), it never
+        // completes, and "idle" is c_comp == +inf (latencies are finite).
+        bool act[S];
         int32_t row[S], pk[S], qh[S], qn[S];  // pk = partition id | k << 8
         uint32_t gn[S], nq[S];
         double c_start[S], c_est[S], c_comp[S], tail[S], fold[S], bms[S], wbms[S];
@@ -147,10 +150,12 @@ __global__ void __launch_bounds__(kSimWarpsPerBlock * 32, WarpCfg<S>::min_blocks
                 pk[s] = dp.pid | (dp.k << 8);
                 row[s] = dp.row;
             }
-            busy[s] = false;
             qh[s] = qn[s] = 0;
             gn[s] = nq[s] = 0;
-            c_start[s] = c_est[s] = c_comp[s] = tail[s] = 0.0;
+            c_start[s] = -INFINITY;
+            c_est[s] = 0.0;
+            c_comp[s] = INFINITY;
+            tail[s] = 0.0;
             fold[s] = 0.0;
             bms[s] = wbms[s] = 0.0;
         }
@@ -183,25 +188,29 @@ __global__ void __launch_bounds__(kSimWarpsPerBlock * 32, WarpCfg<S>::min_blocks
         auto drain = [&](double t) {
 #pragma unroll
             for (int s = 0; s < S; ++s) {
-                while (busy[s] && c_comp[s] <= t) {
-                    if (qn[s] > 0) {
-                        const int h = qh[s];
-                        const double est = W.q_est[s][h][lane];
-                        qh[s] = (h + 1) & (QC - 1);
-                        qn[s] -= 1;
-                        const bool spilled = gn[s] > 0;  // overflow mode before this pop
-                        if (gn[s] > 0) {  // refill the ring from the overflow list
-                            const uint32_t g = W.g_head[s][lane];
-                            W.g_head[s][lane] = g_next[g];
-                            gn[s] -= 1;
-                            const int e2 = (qh[s] + qn[s]) & (QC - 1);
-                            W.q_est[s][e2][lane] = s_lat[row[s] + g_bat[g] - 1];
-                            qn[s] += 1;
+                // pops: the queue head starts at the running query's finish (idle: +inf, never)
+                while (c_comp[s] <= t && qn[s] > 0) {
+                    const int h = qh[s];
+                    const double est = W.q_est[s][h][lane];
+                    qh[s] = (h + 1) & (QC - 1);
+                    qn[s] -= 1;
+                    c_start[s] = c_comp[s];
+                    c_est[s] = est;
+                    c_comp[s] = c_start[s] + est;  // the placement computed the same sum
+                    if (gn[s] == 0) {
+                        if (kFold) {  // the queue fits the ring: exact left fold from 0.0 (0 + e == e)
+                            double acc = 0.0;
+#pragma unroll 1
+                            for (int k = 0; k < qn[s]; ++k) acc = acc + W.q_est[s][(qh[s] + k) & (QC - 1)][lane];
+                            fold[s] = acc;
                         }
-                        c_start[s] = c_comp[s];
-                        c_est[s] = est;
-                        c_comp[s] = c_start[s] + est;  // the placement computed the same sum
-                        if (kLazy && spilled && gn[s] > 0) {  // still spilled: drop the head from the sum
+                    } else {  // spilled: refill the ring from the overflow list
+                        const uint32_t g = W.g_head[s][lane];
+                        W.g_head[s][lane] = g_next[g];
+                        gn[s] -= 1;
+                        W.q_est[s][(qh[s] + qn[s]) & (QC - 1)][lane] = s_lat[row[s] + g_bat[g] - 1];
+                        qn[s] += 1;
+                        if (kLazy && gn[s] > 0) {  // still spilled: drop the head from the sum
                             double hi = W.dd_hi[s][lane], lo = W.dd_lo[s][lane];
                             dd_add(hi, lo, -est);
                             W.dd_hi[s][lane] = hi;
@@ -213,13 +222,15 @@ __global__ void __launch_bounds__(kSimWarpsPerBlock * 32, WarpCfg<S>::min_blocks
                                 pk[s] |= kFv;
                             }
                         } else if (kFold) {
-                            fold[s] = refold(s);  // the queue fits the ring: cheap exact fold
+                            fold[s] = refold(s);
                         }
-                    } else {
-                        busy[s] = false;
-                        fold[s] = 0.0;
                     }
                 }
+                // nothing queued behind a finished query: idle (c_est stays finite, so
+                // est - (now - start) = -inf; the fold of an empty queue is already 0)
+                const bool idle = c_comp[s] <= t;
+                c_start[s] = sel_f64(idle, -INFINITY, c_start[s]);
+                c_comp[s] = sel_f64(idle, INFINITY, c_comp[s]);
             }
         };
 
@@ -279,7 +290,7 @@ __global__ void __launch_bounds__(kSimWarpsPerBlock * 32, WarpCfg<S>::min_blocks
                         // plain multi-slot ELSA evaluates it slot by slot below, FIFS never
                         if constexpr (FULL || (SCHED == MSV_ELSA && S == 1)) {
                             const double x = c_est[s] - (t - c_start[s]);
-                            wv[s] = fold[s] + ((busy[s] && 0.0 < x) ? x : 0.0);
+                            wv[s] = fold[s] + pos_part(x);
                         }
                     }
                     int bad_o = 1 << 30;  // order index of the first candidate whose size is missing
@@ -308,7 +319,7 @@ __global__ void __launch_bounds__(kSimWarpsPerBlock * 32, WarpCfg<S>::min_blocks
                             for (int s = 0; s < S; ++s) {
                                 if (!cand[s] || row[s] < 0) continue;
                                 const double y = c_comp[s] - t;
-                                const double gw = fold[s] + ((busy[s] && 0.0 < y) ? y : 0.0);
+                                const double gw = fold[s] + ((c_comp[s] < INFINITY && 0.0 < y) ? y : 0.0);
                                 const double dd = fabs(gw - wv[s]);
                                 wdiff = (wdiff < dd) ? dd : wdiff;
                             }
@@ -333,7 +344,7 @@ __global__ void __launch_bounds__(kSimWarpsPerBlock * 32, WarpCfg<S>::min_blocks
 #pragma unroll
                         for (int s = 0; s < S; ++s) {
                             const double x = c_est[s] - (t - c_start[s]);
-                            const double xp = (busy[s] && 0.0 < x) ? x : 0.0;
+                            const double xp = pos_part(x);
                             stl[s] = gn[s] > 0 && !(pk[s] & kFv);
                             double flo = fold[s], fhi = fold[s];
                             if (stl[s]) {  // |left fold - exact sum| <= (n-1) 2^-53 sum; slack x2
@@ -351,7 +362,7 @@ __global__ void __launch_bounds__(kSimWarpsPerBlock * 32, WarpCfg<S>::min_blocks
                             pk[s] |= kFv;
                             stl[s] = false;
                             const double x = c_est[s] - (t - c_start[s]);
-                            vlo[s] = vhi[s] = (fold[s] + ((busy[s] && 0.0 < x) ? x : 0.0)) + est_n[s];
+                            vlo[s] = vhi[s] = (fold[s] + pos_part(x)) + est_n[s];
                         };
 #pragma unroll
                         for (int s = 0; s < S; ++s) {  // Step A (sched.hpp:125-130), slots in order
@@ -362,7 +373,7 @@ __global__ void __launch_bounds__(kSimWarpsPerBlock * 32, WarpCfg<S>::min_blocks
                             } else {
                                 if (act[s] && stl[s]) exact(s);
                                 const double x = c_est[s] - (t - c_start[s]);
-                                const double w = fold[s] + ((busy[s] && 0.0 < x) ? x : 0.0);
+                                const double w = fold[s] + pos_part(x);
                                 pred = act[s] && (sla > alpha * (w + beta * est_n[s]));
                             }
                             const unsigned bA = __ballot_sync(kFull, pred);
@@ -434,7 +445,7 @@ __global__ void __launch_bounds__(kSimWarpsPerBlock * 32, WarpCfg<S>::min_blocks
 #pragma unroll
                         for (int s = 0; s < S; ++s) {
                             const double x = c_est[s] - (t - c_start[s]);
-                            wv[s] = fold[s] + ((busy[s] && 0.0 < x) ? x : 0.0);
+                            wv[s] = fold[s] + pos_part(x);
                             s_eval = s + 1;
                             bool pred;
                             if constexpr (UNIT) pred = act[s] && (sla > wv[s] + est_n[s]);
@@ -502,7 +513,7 @@ __global__ void __launch_bounds__(kSimWarpsPerBlock * 32, WarpCfg<S>::min_blocks
                         uint32_t mi = ~0u;
 #pragma unroll
                         for (int s = 0; s < S; ++s) {
-                            key[s] = (cand[s] && !busy[s])
+                            key[s] = (cand[s] && c_comp[s] == INFINITY)
                                          ? (((0x7FFFu - ((uint32_t)pk[s] >> 8)) << 16) | ((uint32_t)pk[s] & 0xffu))
                                          : ~0u;
                             mi = key[s] < mi ? key[s] : mi;
@@ -544,47 +555,48 @@ __global__ void __launch_bounds__(kSimWarpsPerBlock * 32, WarpCfg<S>::min_blocks
                     // ---- start or enqueue on the chosen partition (engine.hpp:225-230) ----
 #pragma unroll
                     for (int s = 0; s < S; ++s) {
-                        if (mine[s]) {
-                            const double est = est_n[s];
-                            double st, fin;
-                            if (!busy[s]) {
-                                busy[s] = true;
-                                st = t;
-                                fin = t + est;
-                                c_start[s] = t;
-                                c_est[s] = est;
-                                c_comp[s] = fin;
+                        // Straight-line and predicated on `mine`: every lane executes the same
+                        // instructions (no divergent region), only the chosen one changes state.
+                        const bool m = mine[s];
+                        const double est = est_n[s];
+                        const bool busy = c_comp[s] != INFINITY;
+                        const double st = sel_f64(busy, tail[s], t);  // queued: starts when the last placed finishes
+                        const double fin = st + est;
+                        const bool now = m && !busy;  // idle: starts at its arrival
+                        const bool push = m && busy;
+                        tail[s] = sel_f64(m, fin, tail[s]);
+                        c_start[s] = sel_f64(now, t, c_start[s]);
+                        c_est[s] = sel_f64(now, est, c_est[s]);
+                        c_comp[s] = sel_f64(now, fin, c_comp[s]);
+                        // appending extends the left fold exactly (a stale fold stays stale)
+                        fold[s] = sel_f64(push, fold[s] + est, fold[s]);
+                        if (push) {
+                            if (gn[s] == 0 && qn[s] < QC) {
+                                W.q_est[s][(qh[s] + qn[s]) & (QC - 1)][lane] = est;
+                                qn[s] += 1;
                             } else {
-                                st = tail[s];  // starts when the query placed before it finishes
-                                fin = st + est;
-                                if (gn[s] == 0 && qn[s] < QC) {
-                                    W.q_est[s][(qh[s] + qn[s]) & (QC - 1)][lane] = est;
-                                    qn[s] += 1;
-                                } else {
-                                    if (kLazy) {  // overflow mode: keep the double-double sum
-                                        double hi = 0.0, lo = 0.0;
-                                        if (gn[s] == 0) {  // entering it: sum the ring, the fold is exact
+                                if (kLazy) {  // overflow mode: keep the double-double sum
+                                    double hi = 0.0, lo = 0.0;
+                                    if (gn[s] == 0) {  // entering it: sum the ring, the fold is exact
 #pragma unroll 1
-                                            for (int k = 0; k < qn[s]; ++k)
-                                                dd_add(hi, lo, W.q_est[s][(qh[s] + k) & (QC - 1)][lane]);
-                                            pk[s] |= kFv;
-                                        } else {
-                                            hi = W.dd_hi[s][lane];
-                                            lo = W.dd_lo[s][lane];
-                                        }
-                                        dd_add(hi, lo, est);
-                                        W.dd_hi[s][lane] = hi;
-                                        W.dd_lo[s][lane] = lo;
+                                        for (int k = 0; k < qn[s]; ++k)
+                                            dd_add(hi, lo, W.q_est[s][(qh[s] + k) & (QC - 1)][lane]);
+                                        pk[s] |= kFv;
+                                    } else {
+                                        hi = W.dd_hi[s][lane];
+                                        lo = W.dd_lo[s][lane];
                                     }
-                                    if (gn[s] == 0) W.g_head[s][lane] = (uint32_t)i;
-                                    else g_next[W.g_tail[s][lane]] = (uint32_t)i;
-                                    W.g_tail[s][lane] = (uint32_t)i;
-                                    gn[s] += 1;
+                                    dd_add(hi, lo, est);
+                                    W.dd_hi[s][lane] = hi;
+                                    W.dd_lo[s][lane] = lo;
                                 }
-                                // appending extends the left fold exactly (a stale fold stays stale)
-                                fold[s] = fold[s] + est;
+                                if (gn[s] == 0) W.g_head[s][lane] = (uint32_t)i;
+                                else g_next[W.g_tail[s][lane]] = (uint32_t)i;
+                                W.g_tail[s][lane] = (uint32_t)i;
+                                gn[s] += 1;
                             }
-                            tail[s] = fin;
+                        }
+                        if (m) {
                             W.win_s[j] = st;
                             W.win_f[j] = fin;
                             W.win_p[j] = (pk[s] & 0xff) | (kind << 8);

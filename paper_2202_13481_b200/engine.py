@@ -285,12 +285,21 @@ class PreparedGrid:
 
 
 class Engine:
-    """One msv_ctx: a CUDA device, its memory and stream."""
+    """One msv_ctx: a CUDA device, its memory and stream — or, given a list of devices,
+    a multi-device context (msv_create_multi): grids are cut into cost-balanced
+    contiguous shards, one per device, run concurrently and gathered in scenario order."""
 
-    def __init__(self, device: int = 0, log1p_variant: int | None = None):
+    def __init__(self, device: int | Sequence[int] = 0, log1p_variant: int | None = None):
         self._lib = N.lib()
         h = C.c_void_p()
-        check(self._lib.msv_create(device, C.byref(h)), "msv_create")
+        if isinstance(device, (list, tuple)):
+            ids = _arr(list(device), np.int32)
+            check(self._lib.msv_create_multi(_ptr(ids, C.c_int32), len(ids), C.byref(h)), "msv_create_multi")
+            self.devices = [int(x) for x in ids]
+            device = self.devices[0]
+        else:
+            check(self._lib.msv_create(device, C.byref(h)), "msv_create")
+            self.devices = [device]
         self._h = h
         self.device = device
         if log1p_variant is not None:

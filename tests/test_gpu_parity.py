@@ -395,6 +395,22 @@ def test_reference_unit_tests_against_device_engine():
     assert "42 test cases" in summary, summary
     assert failed == [], summary + "\n" + r.stdout[-2000:]
 
+@pytest.mark.parametrize("devices", ["0,0", "0,0,0"])
+def test_reference_suite_on_multi_device_context(devices):
+    """The reference's unmodified Catch2 suite through the drop-in headers with a
+    multi-device context (MSV_DEVICES; several members on this B200): run_grid, LBT and
+    GPU(max) shard every grid over the members and gather — same 42/42."""
+    exe = ROOT / "oracle" / "_ref" / "dropin_unit_tests"
+    if not exe.exists():
+        pytest.skip("dropin_unit_tests not built (needs /root/reference at build time)")
+    env = dict(__import__("os").environ, MSV_DEVICES=devices)
+    r = subprocess.run([str(exe)], capture_output=True, text=True, timeout=900, env=env)
+    lines = r.stdout.strip().splitlines()
+    summary = lines[-1] if lines else r.stderr
+    failed = [l for l in lines[:-1] if l.startswith("FAILED:")]
+    assert "42 test cases" in summary, summary
+    assert failed == [], summary + "\n" + r.stdout[-2000:]
+
 
 def test_segmented_kernel_classes_subprocess():
     """The segmented kernel (32/W scenarios per warp, W = 4/8/16) is opt-in
