@@ -287,6 +287,17 @@ int msv_lognormal_pdf(double mu, double sigma, int b_max, double* pmf, double* c
  * the input stream of msv_run_noise. */
 int msv_noise_multipliers(uint64_t seed, double sigma, int64_t n, double* out);
 
+/* A grid of noisy scenarios (EngineOptions::noise_sigma / noise_seed per scenario,
+ * engine.hpp:140-145): sample_trace -> run with execution noise -> tail_latency for every
+ * scenario, like msv_run_grid. Traces are generated on the device (K1); each scenario's
+ * multiplier stream exp(sigma*z_j - sigma^2/2), z_j = Rng(noise_seed).normal()
+ * (rng.hpp:27-32), is drawn on the host with the reference's libm (one thread per core);
+ * K5 runs one warp per scenario in the reference's global event order; K3 selects the
+ * tails. P <= 64 per scenario (ParamError otherwise); noise_sigma must be > 0. */
+int msv_run_grid_noise(msv_ctx* ctx, const msv_scenario* scenarios, int64_t n, const double* noise_sigma,
+                       const uint64_t* noise_seed, const double* tail_p, int n_tails, msv_result* results,
+                       msv_usage* usage);
+
 /* Arithmetic self-checks (test support; no reference analogue). The parity tests
  * compare these with the host's libm directly (rng.hpp:20):
  *   msv_log1p_digest   per chunk of `chunk` inputs k in [0, n) of seed's stream

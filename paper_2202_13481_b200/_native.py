@@ -116,6 +116,8 @@ _SIGNATURES = {
     "msv_run_noise": (C.c_int, [_P, C.POINTER(Scenario), C.c_int64, _f64p, _i32p, _f64p, C.POINTER(Result),
                                 C.POINTER(Usage), C.POINTER(Record)]),
     "msv_noise_multipliers": (C.c_int, [C.c_uint64, C.c_double, C.c_int64, _f64p]),
+    "msv_run_grid_noise": (C.c_int, [_P, C.POINTER(Scenario), C.c_int64, _f64p, C.POINTER(C.c_uint64), _f64p, C.c_int,
+                                     C.POINTER(Result), C.POINTER(Usage)]),
     "msv_sample_trace": (C.c_int, [_P, C.c_int32, C.c_double, C.c_double, C.c_uint64, C.c_int64, _f64p, _i32p,
                                    _i64p]),
     "msv_tail_latency": (C.c_int, [_P, _f64p, C.c_int64, _f64p, C.c_int, _f64p]),

@@ -62,6 +62,18 @@ __device__ __forceinline__ double pos_part(double x) {
     return r;
 }
 
+// Eq. 1's current-query term (sched.hpp:82-83): max(0, est - (now - start)) if the
+// partition is running a query at `now` (its finish > now; a finish <= now has
+// completed, completions precede arrivals), else 0 — two compares, one 64-bit select.
+__device__ __forceinline__ double running_part(double finish, double now, double x) {
+    double r;
+    asm("{\n\t.reg .pred p;\n\tsetp.gt.f64 p, %1, %2;\n\tsetp.gt.and.f64 p, %3, 0d0000000000000000, p;"
+        "\n\tselp.f64 %0, %3, 0d0000000000000000, p;\n\t}"
+        : "=d"(r)
+        : "d"(finish), "d"(now), "d"(x));
+    return r;
+}
+
 // c ? a : b on doubles as one predicated 64-bit select.
 __device__ __forceinline__ double sel_f64(bool c, double a, double b) {
     double r;

@@ -158,6 +158,9 @@ static void append_guide(const std::vector<double>& cdf, std::vector<int16_t>& g
 struct msv_ctx {
     int device = 0;
     GridBufs scratch;  // reused by one-shot grids (msv_run_grid / msv_run_replay)
+    // reused by noisy grids (msv_run_grid_noise): multipliers and K5 jobs
+    DevBuf d_mult, d_njobs;
+    std::vector<double> h_mult;
     int sms = 148;
     cudaStream_t stream = nullptr;
     int log1p = MSV_LOG1P_FMA;
@@ -167,6 +170,7 @@ struct msv_ctx {
     cudaStream_t aux[4] = {};    // chunk streams of overlapped grid launches
     cudaEvent_t aux_ev[4] = {};
     cudaEvent_t fork_ev = nullptr;
+    cudaEvent_t region_ev[2] = {};  // a multi-wave grid's buffer region is free again
     uint64_t grid_serial = 0;       // grids created on this context
     uint64_t last_launch_grid = 0;  // serial of the grid launched last
     cudaStream_t cls[4] = {};    // extra class streams: a chunk's kernel classes run concurrently
@@ -343,7 +347,8 @@ struct msv_grid {
     bool overlap = true;                // chunks on concurrent streams
     bool usage = true;                  // accumulate per-partition usage (msv_grid_set_usage)
     std::vector<Wave> waves;
-    int64_t max_wave_q = 0;
+    int64_t max_wave_q = 0;             // query slots of the largest wave (one buffer region)
+    int n_regions = 1;                  // buffer regions the waves alternate between
     GridBufs own;            // buffers of a persistent grid (msv_grid_create)
     GridBufs* B = &own;      // -> own, or the context's scratch set for one-shot calls
     int n_cells = 0;
@@ -561,14 +566,23 @@ int grid_build(msv_ctx* ctx, const msv_scenario* sc, int64_t n, const double* ta
     if (budget > ((size_t)140 << 30)) budget = (size_t)140 << 30;
     const int64_t max_q = std::max<int64_t>((int64_t)(budget / per_q), 1 << 20);
     // Waves of equal query counts (a short last wave would leave most warp slots idle
-    // for one scenario's whole run): ceil(total / max_q) waves, each cut near
-    // total / n_waves. Long scenarios first inside each wave (work stealing balances the rest).
+    // for one scenario's whole run). A grid that fits runs as one wave. A larger
+    // generated grid is cut into waves of at most half the budget that alternate between
+    // two buffer regions: wave w + 1 runs while wave w drains (its K1 and K2 blocks take
+    // the SMs wave w's finished scenarios free), and wave w + 2 waits only for wave w.
+    // Long scenarios first inside each wave (work stealing balances the rest).
     std::vector<int64_t> order(n);
     std::iota(order.begin(), order.end(), 0);
+    std::vector<int64_t> wave_q;
     {
         int64_t total_q = 0;
         for (int64_t i = 0; i < n; ++i) total_q += g->cap[i];
-        const int64_t n_waves = std::max<int64_t>(1, (total_q + max_q - 1) / max_q);
+        int64_t cap_w = max_q;
+        int64_t n_waves = std::max<int64_t>(1, (total_q + max_q - 1) / max_q);
+        if (n_waves > 1 && g->generated) {
+            cap_w = std::max<int64_t>(max_q / 2, 1);
+            n_waves = (total_q + cap_w - 1) / cap_w;
+        }
         const int64_t target = (total_q + n_waves - 1) / n_waves;
         int64_t s0 = 0;
         while (s0 < n) {
@@ -576,11 +590,14 @@ int grid_build(msv_ctx* ctx, const msv_scenario* sc, int64_t n, const double* ta
             w.s0 = s0;
             int64_t q = 0;
             int64_t s1 = s0;
-            while (s1 < n && (s1 == s0 || (q + g->cap[s1] <= max_q && q < target))) q += g->cap[s1++];
+            while (s1 < n && (s1 == s0 || (q + g->cap[s1] <= cap_w && q < target))) q += g->cap[s1++];
             w.s1 = s1;
             g->waves.push_back(std::move(w));
+            wave_q.push_back(q);
             s0 = s1;
         }
+        g->n_regions = g->waves.size() > 1 ? 2 : 1;
+        for (int64_t q : wave_q) g->max_wave_q = std::max(g->max_wave_q, q);
     }
     pt.mark("waves");
     // Expected work per scenario for longest-first scheduling: queries x (1 + 4 rho^2),
@@ -624,17 +641,15 @@ int grid_build(msv_ctx* ctx, const msv_scenario* sc, int64_t n, const double* ta
     static const int group_first = getenv("MSV_TRACE_GROUP_FIRST")
                                        ? std::max(1, std::min(msv::kTraceGroupMax, atoi(getenv("MSV_TRACE_GROUP_FIRST"))))
                                        : 2;
-    int64_t qoff_global = 0;
-    for (msv_grid::Wave& w : g->waves) {
-        w.q0 = qoff_global;
-        int64_t q = 0;
+    for (size_t wi = 0; wi < g->waves.size(); ++wi) {
+        msv_grid::Wave& w = g->waves[wi];
+        w.q0 = (int64_t)(wi % g->n_regions) * g->max_wave_q;  // the wave's buffer region
+        int64_t q = w.q0;
         for (int64_t i = w.s0; i < w.s1; ++i) {
-            g->toff[i] = q;  // offset inside the wave buffers
+            g->toff[i] = q;  // offset inside the trace buffers
             q += g->cap[i];
         }
-        w.q1 = w.q0 + q;
-        qoff_global += q;
-        g->max_wave_q = std::max(g->max_wave_q, q);
+        w.q1 = q;
         // Deal the wave's scenarios, most expensive first, round-robin into chunks.
         std::vector<int32_t> ord;
         for (int64_t i = w.s0; i < w.s1; ++i) ord.push_back((int32_t)i);
@@ -747,7 +762,7 @@ int grid_build(msv_ctx* ctx, const msv_scenario* sc, int64_t n, const double* ta
     g->cost = cost;
     pt.mark("cost+chunks");
     // Device buffers.
-    const size_t wq = (size_t)std::max<int64_t>(g->max_wave_q, 1);
+    const size_t wq = (size_t)std::max<int64_t>(g->max_wave_q * g->n_regions, 1);
     MSV_CUDA_TRY(g->B->d_arr.ensure(wq * 8));
     MSV_CUDA_TRY(g->B->d_bat.ensure(wq * 4));
     MSV_CUDA_TRY(g->B->d_next.ensure(wq * 4));
@@ -1110,23 +1125,37 @@ int grid_launch(msv_grid* g) {
     }
     int counter_base = 0;
     float tr = 0, si = 0, ta = 0;
+    if (overlap && g->n_regions > 1)
+        for (int r = 0; r < 2; ++r)
+            if (!ctx->region_ev[r]) MSV_CUDA_TRY(cudaEventCreateWithFlags(&ctx->region_ev[r], cudaEventDisableTiming));
+    size_t chunk_seq = 0;  // chunks of consecutive waves go to different aux streams
     for (size_t wi = 0; wi < g->waves.size(); ++wi) {
         const msv_grid::Wave& w = g->waves[wi];
         if (overlap) {
-            // fork: every aux stream starts after everything queued on the main stream
-            if (!pipelined) MSV_CUDA_TRY(cudaEventRecord(ctx->fork_ev, st));
+            // fork: the first waves start after everything queued on the main stream; a
+            // wave that reuses a buffer region waits only for the wave that used it last
+            // (the two regions' waves overlap: one drains while the next fills the SMs)
+            if (!pipelined && wi == 0) MSV_CUDA_TRY(cudaEventRecord(ctx->fork_ev, st));
+            std::vector<char> used(kAuxStreams, 0);
             for (size_t c = 0; c < w.chunks.size(); ++c) {
-                cudaStream_t sc = ctx->aux[c % kAuxStreams];
-                if (!pipelined) MSV_CUDA_TRY(cudaStreamWaitEvent(sc, ctx->fork_ev, 0));
+                const int a = (int)((chunk_seq++) % kAuxStreams);
+                cudaStream_t sc = ctx->aux[a];
+                used[a] = 1;
+                if (!pipelined && wi < (size_t)g->n_regions) MSV_CUDA_TRY(cudaStreamWaitEvent(sc, ctx->fork_ev, 0));
+                if (wi >= (size_t)g->n_regions)
+                    MSV_CUDA_TRY(cudaStreamWaitEvent(sc, ctx->region_ev[wi % g->n_regions], 0));
                 if ((rc = zero_counters(counter_base, w.chunks[c].classes.size(), sc))) return rc;
                 if ((rc = launch_chunk(g, w.chunks[c], counter_base, sc, nullptr, nullptr))) return rc;
                 counter_base += (int)w.chunks[c].classes.size();
             }
-            // join: the main stream continues after every chunk of this wave
-            for (size_t a = 0; a < std::min<size_t>(w.chunks.size(), kAuxStreams); ++a) {
+            // join: the main stream continues after every chunk of this wave, and the
+            // wave's region is free again from here
+            for (int a = 0; a < kAuxStreams; ++a) {
+                if (!used[a]) continue;
                 MSV_CUDA_TRY(cudaEventRecord(ctx->aux_ev[a], ctx->aux[a]));
                 MSV_CUDA_TRY(cudaStreamWaitEvent(st, ctx->aux_ev[a], 0));
             }
+            if (g->n_regions > 1) MSV_CUDA_TRY(cudaEventRecord(ctx->region_ev[wi % g->n_regions], st));
         } else {
             for (const msv_grid::Chunk& ch : w.chunks) {
                 cudaEvent_t e0 = g->ev[0], e1 = g->ev[1], e2 = g->ev[2], e3 = g->ev[3];
@@ -1301,6 +1330,8 @@ int msv_destroy(msv_ctx* ctx) {
         if (ctx->aux_ev[a]) cudaEventDestroy(ctx->aux_ev[a]);
     }
     if (ctx->fork_ev) cudaEventDestroy(ctx->fork_ev);
+    for (cudaEvent_t e : ctx->region_ev)
+        if (e) cudaEventDestroy(e);
     for (int a = 0; a < 4; ++a) {
         if (ctx->cls[a]) {
             cudaStreamSynchronize(ctx->cls[a]);
@@ -1858,6 +1889,9 @@ int msv_run_noise(msv_ctx* ctx, const msv_scenario* scenario, int64_t n, const d
     int rc = validate_scenario(ctx, sc, false, &P);
     if (rc) return rc;
     if (P > 64) return fail(MSV_PARAM, "run: execution noise on the device supports at most 64 partitions");
+    if ((int64_t)ctx->profiles[sc.profile].lat.size() > msv::kMaxSmemCells)
+        return fail(MSV_PARAM, "run: profile has more than " + std::to_string(msv::kMaxSmemCells) +
+                                   " (size, batch) cells, the device table limit");
     for (int64_t i = 1; i < n; ++i)
         if (arrival_ms[i] < arrival_ms[i - 1]) return fail(MSV_PARAM, "run: trace must be sorted by arrival");
     const Profile& prof = ctx->profiles[sc.profile];
@@ -1913,7 +1947,13 @@ int msv_run_noise(msv_ctx* ctx, const msv_scenario* scenario, int64_t n, const d
     np.records = d_rec.as<msv_record>();
     np.usage = d_use.as<msv_usage>();
     np.out = d_out.as<DevOut>();
-    MSV_CUDA_TRY(msv::launch_noise(np, st));
+    np.n_ptr = nullptr;
+    np.samples = nullptr;
+    np.duration_ms = sc.duration_ms;
+    DevBuf d_job;
+    MSV_CUDA_TRY(d_job.ensure(sizeof(msv::NoiseParams)));
+    MSV_CUDA_TRY(cudaMemcpyAsync(d_job.p, &np, sizeof np, cudaMemcpyHostToDevice, st));
+    MSV_CUDA_TRY(msv::launch_noise(d_job.as<msv::NoiseParams>(), 1, np.n_cells, st));
     ctx->launches += 1;
     DevOut o{};
     MSV_CUDA_TRY(cudaMemcpyAsync(&o, d_out.p, sizeof(DevOut), cudaMemcpyDeviceToHost, st));
@@ -2486,6 +2526,261 @@ int64_t msv_grid_queries(msv_grid* g) {
         t += q;
     }
     return t;
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------------------------
+// Noisy grids (execution noise at grid scale, engine.hpp:140-145): K1 generates every
+// scenario's trace on the device, the host draws each scenario's multiplier stream with
+// the reference's Rng and libm (rng.hpp:27-32; msv_noise_multipliers, one host thread per
+// core), K5 runs one warp per scenario in global (time, seq) event order, K3 selects the
+// tails from the measured latencies K5 leaves over the arrivals. Buffers are the
+// context's, reused across calls.
+// ---------------------------------------------------------------------------------
+extern "C" int msv_noise_multipliers(uint64_t seed, double sigma, int64_t n, double* out);
+
+namespace {
+
+int run_grid_noise_dev(msv_ctx* ctx, const msv_scenario* sc, int64_t n, const double* sigma, const uint64_t* nseed,
+                       const double* tail_p, int n_tails, msv_result* results, msv_usage* usage,
+                       const int64_t* cap_override) {
+    if (n_tails < 0 || n_tails > 4) return fail(MSV_PARAM, "grid: between 0 and 4 tail percentiles");
+    for (int j = 0; j < n_tails; ++j)
+        if (!(tail_p[j] > 0.0) || !(tail_p[j] < 1.0))
+            return fail(MSV_PARAM, "tail_latency: percentile must be in (0,1)");
+    SetDevice sd(ctx->device);
+    int rc = ctx->sync_tables();
+    if (rc) return rc;
+    std::vector<int32_t> P(n);
+    std::vector<int64_t> cap(n), toff(n + 1, 0), uoff(n + 1, 0);
+    int max_cells = 0;
+    for (int64_t i = 0; i < n; ++i) {
+        rc = validate_scenario(ctx, sc[i], true, &P[i]);
+        if (rc) {
+            g_err = "scenario " + std::to_string(i) + ": " + g_err;
+            return rc;
+        }
+        if (P[i] > 64)
+            return fail(MSV_PARAM, "scenario " + std::to_string(i) +
+                                       ": run: execution noise on the device supports at most 64 partitions");
+        if (!(sigma[i] > 0.0)) return fail(MSV_PARAM, "scenario " + std::to_string(i) + ": noise_sigma must be > 0");
+        const int cells = (int)ctx->profiles[sc[i].profile].lat.size();
+        if (cells > msv::kMaxSmemCells) return fail(MSV_PARAM, "run: profile exceeds the device table limit");
+        max_cells = std::max(max_cells, cells);
+        cap[i] = cap_override ? cap_override[i] : trace_capacity(sc[i].rate_qps, sc[i].duration_ms);
+        if (cap[i] < 0) return fail(MSV_PARAM, "sample_trace: expected trace too long");
+        toff[i + 1] = toff[i] + cap[i];
+        uoff[i + 1] = uoff[i] + P[i];
+    }
+    const int64_t total = toff[n];
+    GridBufs& B = ctx->scratch;
+    const size_t tq = (size_t)std::max<int64_t>(total, 1);
+    MSV_CUDA_TRY(B.d_arr.ensure(tq * 8));
+    MSV_CUDA_TRY(B.d_bat.ensure(tq * 4));
+    MSV_CUDA_TRY(B.d_next.ensure(tq * 4));
+    MSV_CUDA_TRY(ctx->d_mult.ensure(tq * 8));
+    MSV_CUDA_TRY(B.d_out.ensure(std::max<int64_t>(n, 1) * sizeof(DevOut)));
+    MSV_CUDA_TRY(B.d_nq.ensure(std::max<int64_t>(n, 1) * 8));
+    MSV_CUDA_TRY(B.d_tovf.ensure(std::max<int64_t>(n, 1) * 4));
+    MSV_CUDA_TRY(B.d_tjobs.ensure(std::max<int64_t>(n, 1) * sizeof(msv::TraceJob)));
+    MSV_CUDA_TRY(B.d_tailjobs.ensure(std::max<int64_t>(n, 1) * sizeof(msv::TailJob)));
+    MSV_CUDA_TRY(B.d_tails.ensure(std::max<int64_t>(n, 1) * 4 * sizeof(double)));
+    MSV_CUDA_TRY(B.d_p.ensure(4 * sizeof(double)));
+    MSV_CUDA_TRY(B.d_usage.ensure(std::max<int64_t>(uoff[n], 1) * sizeof(msv_usage)));
+    MSV_CUDA_TRY(ctx->d_njobs.ensure(std::max<int64_t>(n, 1) * sizeof(msv::NoiseParams)));
+    // partition tables (rows relative to each scenario's own profile) and routing masks
+    std::vector<DevPart> parts_h;
+    std::vector<uint64_t> masks_h;
+    std::vector<size_t> poff(n), moff(n, (size_t)-1);
+    for (int64_t i = 0; i < n; ++i) {
+        const Profile& prof = ctx->profiles[sc[i].profile];
+        const std::vector<DevPart> parts = plan_parts(ctx->plans[sc[i].plan], prof, 0);
+        poff[i] = parts_h.size();
+        parts_h.insert(parts_h.end(), parts.begin(), parts.end());
+        if (sc[i].routing >= 0) {
+            const std::vector<uint64_t> m = route_masks(parts, ctx->routings[sc[i].routing], prof.b_max);
+            moff[i] = masks_h.size();
+            masks_h.insert(masks_h.end(), m.begin(), m.end());
+        }
+    }
+    MSV_CUDA_TRY(B.d_parts.ensure(std::max<size_t>(parts_h.size(), 1) * sizeof(DevPart)));
+    MSV_CUDA_TRY(B.d_masks.ensure(std::max<size_t>(masks_h.size(), 1) * 8));
+    // multiplier streams on the host, one thread per core (scenario-parallel)
+    ctx->h_mult.resize(tq);
+    {
+        const int nt = std::max(1, std::min<int>((int)std::thread::hardware_concurrency(), (int)std::max<int64_t>(n, 1)));
+        std::atomic<int64_t> next_i{0};
+        std::vector<std::thread> th;
+        for (int t = 0; t < nt; ++t)
+            th.emplace_back([&] {
+                for (int64_t i; (i = next_i.fetch_add(1)) < n;)
+                    msv_noise_multipliers(nseed[i], sigma[i], cap[i], ctx->h_mult.data() + toff[i]);
+            });
+        for (std::thread& t : th) t.join();
+    }
+    std::vector<msv::TraceJob> tj(n);
+    std::vector<msv::NoiseParams> nj(n);
+    std::vector<msv::TailJob> lj(n);
+    for (int64_t i = 0; i < n; ++i) {
+        const msv_scenario& s = sc[i];
+        const Profile& prof = ctx->profiles[s.profile];
+        const Dist& ds = ctx->dists[s.dist];
+        double* arr = B.d_arr.as<double>() + toff[i];
+        int32_t* bat = B.d_bat.as<int32_t>() + toff[i];
+        msv::TraceJob& t = tj[i];
+        t.seed = s.seed;
+        t.rate_per_ms = s.rate_qps / 1000.0;  // workload.hpp:103
+        t.duration_ms = s.duration_ms;
+        t.cdf = ctx->d_cdf.as<double>() + ds.dev_off;
+        t.guide = ctx->d_guide.as<int16_t>() + ds.guide_off;
+        t.b_max = (int32_t)ds.cdf.size();
+        t.pad = 0;
+        t.arrival = arr;
+        t.batch = bat;
+        t.cap = cap[i];
+        t.n_out = B.d_nq.as<int64_t>() + i;
+        t.overflow = B.d_tovf.as<int32_t>() + i;
+        msv::NoiseParams& q = nj[i];
+        q = msv::NoiseParams{};
+        q.arrival = arr;
+        q.batch = bat;
+        q.n = 0;
+        q.n_ptr = B.d_nq.as<int64_t>() + i;
+        q.samples = arr;
+        q.duration_ms = s.duration_ms;
+        q.mult = ctx->d_mult.as<double>() + toff[i];
+        q.lat = ctx->d_lat.as<double>() + prof.cell_off;
+        q.util = ctx->d_util.as<double>() + prof.cell_off;
+        q.parts = B.d_parts.as<DevPart>() + poff[i];
+        q.route_mask = moff[i] == (size_t)-1 ? nullptr : B.d_masks.as<uint64_t>() + moff[i];
+        q.P = P[i];
+        q.b_max = prof.b_max;
+        q.sched = s.scheduler;
+        q.n_cells = (int32_t)prof.lat.size();
+        q.sla = s.sla_ms;
+        q.alpha = s.alpha;
+        q.beta = s.beta;
+        q.warmup_ms = s.warmup_fraction * s.duration_ms;  // engine.hpp:236
+        q.next = B.d_next.as<uint32_t>() + toff[i];
+        q.records = nullptr;
+        q.usage = B.d_usage.as<msv_usage>() + uoff[i];
+        q.out = B.d_out.as<DevOut>() + i;
+        msv::TailJob& l = lj[i];
+        l.samples = arr;
+        l.src = B.d_out.as<DevOut>() + i;
+        l.out = B.d_tails.as<double>() + 4 * i;
+    }
+    cudaStream_t st = ctx->stream;
+    if (!parts_h.empty())
+        MSV_CUDA_TRY(cudaMemcpyAsync(B.d_parts.p, parts_h.data(), parts_h.size() * sizeof(DevPart), cudaMemcpyHostToDevice, st));
+    if (!masks_h.empty())
+        MSV_CUDA_TRY(cudaMemcpyAsync(B.d_masks.p, masks_h.data(), masks_h.size() * 8, cudaMemcpyHostToDevice, st));
+    if (n) {
+        MSV_CUDA_TRY(cudaMemcpyAsync(B.d_tjobs.p, tj.data(), n * sizeof(msv::TraceJob), cudaMemcpyHostToDevice, st));
+        MSV_CUDA_TRY(cudaMemcpyAsync(ctx->d_njobs.p, nj.data(), n * sizeof(msv::NoiseParams), cudaMemcpyHostToDevice, st));
+        MSV_CUDA_TRY(cudaMemcpyAsync(B.d_tailjobs.p, lj.data(), n * sizeof(msv::TailJob), cudaMemcpyHostToDevice, st));
+        MSV_CUDA_TRY(cudaMemcpyAsync(ctx->d_mult.p, ctx->h_mult.data(), total * 8, cudaMemcpyHostToDevice, st));
+        MSV_CUDA_TRY(cudaMemsetAsync(B.d_tovf.p, 0, n * 4, st));
+    }
+    if (n_tails) MSV_CUDA_TRY(cudaMemcpyAsync(B.d_p.p, tail_p, n_tails * sizeof(double), cudaMemcpyHostToDevice, st));
+    ctx->h2d += total * 8 + (int64_t)(n * (sizeof(msv::TraceJob) + sizeof(msv::NoiseParams) + sizeof(msv::TailJob)) +
+                                      parts_h.size() * sizeof(DevPart) + masks_h.size() * 8);
+    if (n) {
+        MSV_CUDA_TRY(msv::launch_trace_gen(B.d_tjobs.as<msv::TraceJob>(), (int)n, ctx->log1p, st));
+        MSV_CUDA_TRY(msv::launch_noise(ctx->d_njobs.as<msv::NoiseParams>(), (int)n, max_cells, st));
+        ctx->launches += 2;
+        if (n_tails) {
+            MSV_CUDA_TRY(msv::launch_tail(B.d_tailjobs.as<msv::TailJob>(), (int)n, B.d_p.as<double>(), n_tails, st));
+            ctx->launches += 1;
+        }
+    }
+    std::vector<DevOut> outs(n);
+    std::vector<double> tails(4 * n);
+    std::vector<int64_t> nq(n);
+    std::vector<int32_t> ovf(n);
+    if (n) {
+        MSV_CUDA_TRY(cudaMemcpyAsync(outs.data(), B.d_out.p, n * sizeof(DevOut), cudaMemcpyDeviceToHost, st));
+        MSV_CUDA_TRY(cudaMemcpyAsync(tails.data(), B.d_tails.p, n * 4 * sizeof(double), cudaMemcpyDeviceToHost, st));
+        MSV_CUDA_TRY(cudaMemcpyAsync(nq.data(), B.d_nq.p, n * 8, cudaMemcpyDeviceToHost, st));
+        MSV_CUDA_TRY(cudaMemcpyAsync(ovf.data(), B.d_tovf.p, n * 4, cudaMemcpyDeviceToHost, st));
+        if (usage)
+            MSV_CUDA_TRY(cudaMemcpyAsync(usage, B.d_usage.p, uoff[n] * sizeof(msv_usage), cudaMemcpyDeviceToHost, st));
+    }
+    MSV_CUDA_TRY(cudaStreamSynchronize(st));
+    ctx->d2h += n * (int64_t)(sizeof(DevOut) + 4 * sizeof(double) + 12) + (usage ? uoff[n] * (int64_t)sizeof(msv_usage) : 0);
+    std::vector<int64_t> retry;
+    for (int64_t i = 0; i < n; ++i) {
+        if (ovf[i]) {
+            retry.push_back(i);
+            continue;
+        }
+        const DevOut& o = outs[i];
+        msv_result& r = results[i];
+        r = msv_result{};
+        r.total = nq[i];
+        r.violations = o.violations;
+        r.measured = o.measured;
+        r.measured_violations = o.measured_violations;
+        for (int j = 0; j < 4; ++j) r.tail[j] = j < n_tails ? tails[4 * i + j] : std::numeric_limits<double>::quiet_NaN();
+        r.horizon_ms = o.horizon_ms;
+        r.warmup_ms = sc[i].warmup_fraction * sc[i].duration_ms;
+        r.max_wait_estimate_diff = 0.0;  // the reference skips the check under noise (engine.hpp:208)
+        r.duration_ms = sc[i].duration_ms;
+        r.placement_hash = o.hash;
+        r.status = o.status;
+        r.n_partitions = P[i];
+    }
+    // traces longer than their Poisson-tail capacity: rerun those with 4x the capacity
+    if (!retry.empty()) {
+        std::vector<msv_scenario> sub;
+        std::vector<double> ssig;
+        std::vector<uint64_t> sseed;
+        std::vector<int64_t> scap;
+        int64_t nu = 0;
+        for (int64_t i : retry) {
+            sub.push_back(sc[i]);
+            ssig.push_back(sigma[i]);
+            sseed.push_back(nseed[i]);
+            scap.push_back(cap[i] * 4);
+            nu += P[i];
+        }
+        std::vector<msv_result> sres(sub.size());
+        std::vector<msv_usage> suse(std::max<int64_t>(nu, 1));
+        rc = run_grid_noise_dev(ctx, sub.data(), (int64_t)sub.size(), ssig.data(), sseed.data(), tail_p, n_tails,
+                                sres.data(), usage ? suse.data() : nullptr, scap.data());
+        if (rc) return rc;
+        int64_t u = 0;
+        for (size_t k = 0; k < retry.size(); ++k) {
+            results[retry[k]] = sres[k];
+            if (usage)
+                for (int32_t q = 0; q < P[retry[k]]; ++q) usage[uoff[retry[k]] + q] = suse[u++];
+        }
+    }
+    return MSV_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int msv_run_grid_noise(msv_ctx* ctx, const msv_scenario* scenarios, int64_t n, const double* noise_sigma,
+                       const uint64_t* noise_seed, const double* tail_p, int n_tails, msv_result* results,
+                       msv_usage* usage) {
+    if (!ctx || (n > 0 && (!scenarios || !results || !noise_sigma || !noise_seed)))
+        return fail(MSV_PARAM, "null argument");
+    if (ctx->peers.empty())
+        return run_grid_noise_dev(ctx, scenarios, n, noise_sigma, noise_seed, tail_p, n_tails, results, usage, nullptr);
+    sync_peers(ctx);
+    const std::vector<msv_ctx*> m = members(ctx);
+    const std::vector<int64_t> cut = shard_cuts(ctx, scenarios, n, nullptr, (int)m.size());
+    const std::vector<int64_t> uo = usage_prefix(ctx, scenarios, n);
+    return fan_out(m, [&](size_t k) {
+        const int64_t lo = cut[k], hi = cut[k + 1];
+        if (hi <= lo) return (int)MSV_OK;
+        return run_grid_noise_dev(m[k], scenarios + lo, hi - lo, noise_sigma + lo, noise_seed + lo, tail_p, n_tails,
+                                  results + lo, usage ? usage + uo[lo] : nullptr, nullptr);
+    });
 }
 
 }  // extern "C"

@@ -168,11 +168,14 @@ struct ParisParams {
     int32_t* remaining;  // scratch: num_gpus ints per job at gpu_off
 };
 
-// K5: one run() with execution noise (msv_noise.cu), one warp, P <= 64.
+// K5: run() with execution noise (msv_noise.cu), one warp (one block) per job, P <= 64.
 struct NoiseParams {
     const double* arrival;      // sorted trace (device)
     const int32_t* batch;
     int64_t n;
+    const int64_t* n_ptr;       // trace length on the device (K1's count), or null: use n
+    double* samples;            // measured latencies out at samples[q] (the arrival buffer), or null
+    double duration_ms;         // horizon = max(duration, last finish) (engine.hpp:235)
     const double* mult;         // n noise multipliers exp(sigma*z_j - sigma^2/2), start order
     const double* lat;          // this profile's cells, row-major [size_idx][batch-1]
     const double* util;
@@ -181,13 +184,14 @@ struct NoiseParams {
     int32_t P, b_max, sched, n_cells;  // n_cells: entries of lat (and util)
     double sla, alpha, beta, warmup_ms;
     uint32_t* next;             // n: FIFO links through query indices
-    msv_record* records;        // n
+    msv_record* records;        // n, or null (grids keep only the aggregates and samples)
     msv_usage* usage;           // P, by partition id
-    DevOut* out;                // violations, measured, measured_violations, hash, horizon (last finish), status
+    DevOut* out;                // violations, measured(+samples, m0), hash, horizon, status
 };
 
 // Kernel launchers (msv_kernels.cu). Return cudaGetLastError().
-cudaError_t launch_noise(const NoiseParams& p, cudaStream_t stream);
+// One block (one warp) per job; max_cells = the largest job's profile cells.
+cudaError_t launch_noise(const NoiseParams* d_jobs, int n_jobs, int max_cells, cudaStream_t stream);
 cudaError_t launch_paris(const ParisParams& p, cudaStream_t stream);
 // K1 over groups: group g covers jobs [first, first + count) (count <= kTraceGroupMax, one
 // seed and distribution per group).

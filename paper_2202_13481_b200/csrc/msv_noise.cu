@@ -30,8 +30,9 @@ namespace {
 constexpr int kNoiseSlots = 2;  // P <= 64
 constexpr int kRing = 64;       // queued estimates per slot cached in shared memory (ELSA)
 
-__global__ void __launch_bounds__(32, 1) sim_noise_kernel(const NoiseParams p) {
+__global__ void __launch_bounds__(32, 1) sim_noise_kernel(const NoiseParams* __restrict__ jobs) {
     constexpr int S = kNoiseSlots;
+    const NoiseParams& p = jobs[blockIdx.x];
     const int lane = threadIdx.x & 31;
     const double* __restrict__ arr = p.arrival;
     const int32_t* __restrict__ bat = p.batch;
@@ -44,7 +45,7 @@ __global__ void __launch_bounds__(32, 1) sim_noise_kernel(const NoiseParams p) {
     __syncwarp();
     const double* lat = s_tab;
     const double* util = s_tab + p.n_cells;
-    const int64_t n = p.n;
+    const int64_t n = p.n_ptr ? *p.n_ptr : p.n;
     const double sla = p.sla, alpha = p.alpha, beta = p.beta, warmup = p.warmup_ms;
     const bool route = p.route_mask != nullptr;
     const bool elsa = p.sched == MSV_ELSA;  // Eq. 1's fold is needed by ELSA only
@@ -97,7 +98,7 @@ __global__ void __launch_bounds__(32, 1) sim_noise_kernel(const NoiseParams p) {
             __syncwarp();
         }
     };
-    int64_t viol = 0, meas = 0, mviol = 0;
+    int64_t viol = 0, meas = 0, mviol = 0, m0 = -1;
     uint64_t hash = 0;
     double last_finish = 0.0;
     int status = 0;
@@ -169,10 +170,11 @@ __global__ void __launch_bounds__(32, 1) sim_noise_kernel(const NoiseParams p) {
                     if (a >= warmup) {
                         meas += 1;
                         mviol += met ? 0 : 1;
+                        if (p.samples) p.samples[q] = l;  // over its own (dead) arrival
                     }
                     last_finish = last_finish < now ? now : last_finish;
                     hash += msv_query_digest((uint64_t)q, pid[s], c_start[s], now);
-                    p.records[q].finish_ms = now;
+                    if (p.records) p.records[q].finish_ms = now;
                     if (qn[s] > 0) {  // start the queue head now (engine.hpp:181-185)
                         const int64_t h = qh[s];
                         qh[s] = p.next[h];
@@ -195,7 +197,7 @@ __global__ void __launch_bounds__(32, 1) sim_noise_kernel(const NoiseParams p) {
                         c_comp[s] = now + est * mw[j - mj];
                         c_seq[s] = seq;
                         cq[s] = h;
-                        p.records[h].start_ms = now;
+                        if (p.records) p.records[h].start_ms = now;
                         if (elsa) fold[s] = refold(s);
                         started = 1;
                     } else {
@@ -224,6 +226,7 @@ __global__ void __launch_bounds__(32, 1) sim_noise_kernel(const NoiseParams p) {
         }
         const double t = __shfl_sync(kFull, w_t, (int)(i & 31));
         const int b = __shfl_sync(kFull, w_b, (int)(i & 31));
+        if (m0 < 0 && t >= warmup) m0 = i;  // the measured suffix (arrivals are sorted)
         drain(t);  // completions at <= t precede the arrival (engine.hpp:101-107)
         stage_mult();
         if (b < 1 || b > p.b_max) {  // every lookup of this query fails (profile.hpp:123-132)
@@ -364,8 +367,10 @@ __global__ void __launch_bounds__(32, 1) sim_noise_kernel(const NoiseParams p) {
                     continue;
                 }
                 const double est = lat[row[s] + b - 1];
-                p.records[i].partition = pid[s];
-                p.records[i].kind = kind;
+                if (p.records) {
+                    p.records[i].partition = pid[s];
+                    p.records[i].kind = kind;
+                }
                 if (busy[s]) {
                     if (elsa) {
                         if (qn[s] < kRing) ring[s][(rh[s] + (int)qn[s]) & (kRing - 1)][lane] = est;
@@ -389,7 +394,7 @@ __global__ void __launch_bounds__(32, 1) sim_noise_kernel(const NoiseParams p) {
                     c_arr[s] = t;
                     c_b[s] = b;
                     fold[s] = 0.0;
-                    p.records[i].start_ms = t;
+                    if (p.records) p.records[i].start_ms = t;
                     started = 1;
                 }
             }
@@ -427,21 +432,26 @@ __global__ void __launch_bounds__(32, 1) sim_noise_kernel(const NoiseParams p) {
         p.out->measured = meas;
         p.out->measured_violations = mviol;
         p.out->hash = hash;
-        p.out->horizon_ms = last_finish;  // the host takes max(duration, last_finish)
+        p.out->horizon_ms = (p.duration_ms < last_finish) ? last_finish : p.duration_ms;  // engine.hpp:235
         p.out->status = status;
+        p.out->n_samples = meas;
+        p.out->m0 = m0 >= 0 ? (int32_t)m0 : 0;
+        p.out->lat_min_bits = ~0ull;  // min > max: K3 derives the key range from the samples
+        p.out->lat_max_bits = 0;
     }
 }
 
 }  // namespace
 
-cudaError_t launch_noise(const NoiseParams& p, cudaStream_t stream) {
-    const size_t smem = (size_t)2 * p.n_cells * sizeof(double);
-    if (smem > 48 * 1024) {
-        const cudaError_t e =
-            cudaFuncSetAttribute(sim_noise_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess) return e;
-    }
-    sim_noise_kernel<<<1, 32, smem, stream>>>(p);
+cudaError_t launch_noise(const NoiseParams* d_jobs, int n_jobs, int max_cells, cudaStream_t stream) {
+    // Always opt in: the kernel's ~33 KB of static shared memory (ring, multiplier
+    // window) already eats most of the default 48 KB, so the default dynamic limit is
+    // only ~15 KB (profiles of ~1,000 cells failed to launch).
+    const size_t smem = (size_t)2 * max_cells * sizeof(double);
+    const cudaError_t e = cudaFuncSetAttribute(sim_noise_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    if (n_jobs <= 0) return cudaSuccess;
+    sim_noise_kernel<<<n_jobs, 32, smem, stream>>>(d_jobs);
     return cudaGetLastError();
 }
 

@@ -89,8 +89,8 @@ __global__ void __launch_bounds__(kSimWarpsPerBlock * 32, (SegCfg<W, S>::min_blo
     bool unit = true, check_wait = false;
     int bmax = 0;
     // ---- per-lane partition slots ----
-    // c_* = the query running at the last arrival; tail = finish of the query placed last.
-    // An idle slot holds c_start = -inf, c_est = 0, c_comp = +inf (msv_sim_warp.cu).
+    // c_* = the query placed last to start; tail = finish of the query placed last; the
+    // slot is busy at t iff c_comp > t (msv_sim_warp.cu).
     bool act[S];
     int32_t row[S], pk[S], qh[S], qn[S];
     uint32_t gn[S], nq[S];
@@ -103,9 +103,8 @@ __global__ void __launch_bounds__(kSimWarpsPerBlock * 32, (SegCfg<W, S>::min_blo
         act[s] = false;
         row[s] = pk[s] = qh[s] = qn[s] = 0;
         gn[s] = nq[s] = 0;
-        c_start[s] = -INFINITY;
-        c_est[s] = 0.0;
-        c_comp[s] = INFINITY;
+        c_start[s] = c_est[s] = 0.0;
+        c_comp[s] = -INFINITY;  // idle: busy at t iff c_comp > t
         tail[s] = fold[s] = bms[s] = wbms[s] = 0.0;
     }
 
@@ -181,9 +180,8 @@ __global__ void __launch_bounds__(kSimWarpsPerBlock * 32, (SegCfg<W, S>::min_blo
                     }
                     qh[s] = qn[s] = 0;
                     gn[s] = nq[s] = 0;
-                    c_start[s] = -INFINITY;
-                    c_est[s] = 0.0;
-                    c_comp[s] = INFINITY;
+                    c_start[s] = c_est[s] = 0.0;
+                    c_comp[s] = -INFINITY;
                     tail[s] = 0.0;
                     fold[s] = bms[s] = wbms[s] = 0.0;
                 }
@@ -232,8 +230,8 @@ __global__ void __launch_bounds__(kSimWarpsPerBlock * 32, (SegCfg<W, S>::min_blo
         // ---- 1. advance to t, lane-local, in chain order (engine.hpp:167-187) ----
 #pragma unroll
         for (int s = 0; s < S; ++s) {
-            while (c_comp[s] <= t) {  // (idle: +inf, never)
-                if (qn[s] > 0) {  // start the queue head at the finish (engine.hpp:181-185)
+            while (c_comp[s] <= t && qn[s] > 0) {  // a finished query with nothing queued: idle
+                {  // start the queue head at the finish (engine.hpp:181-185)
                     const int h = qh[s];
                     const double est = M.q_est[s][h][lane];
                     qh[s] = (h + 1) & (QC - 1);
@@ -249,11 +247,6 @@ __global__ void __launch_bounds__(kSimWarpsPerBlock * 32, (SegCfg<W, S>::min_blo
                     c_est[s] = est;
                     c_comp[s] = c_start[s] + est;  // the placement computed the same sum
                     if (kFold) fold[s] = refold(s);
-                } else {  // idle
-                    c_start[s] = -INFINITY;
-                    c_est[s] = 0.0;
-                    c_comp[s] = INFINITY;
-                    fold[s] = 0.0;
                 }
             }
         }
@@ -270,7 +263,7 @@ __global__ void __launch_bounds__(kSimWarpsPerBlock * 32, (SegCfg<W, S>::min_blo
         for (int s = 0; s < S; ++s) {
             cand[s] = go && act[s];
             const double x = c_est[s] - (t - c_start[s]);
-            wv[s] = fold[s] + pos_part(x);  // Eq. 1 (sched.hpp:77-85); idle: x = -inf
+            wv[s] = fold[s] + running_part(c_comp[s], t, x);  // Eq. 1 (sched.hpp:77-85)
             bad[s] = false;
         }
         int bad_o = 1 << 30;  // segment order index of the first candidate whose size is missing
@@ -299,7 +292,7 @@ __global__ void __launch_bounds__(kSimWarpsPerBlock * 32, (SegCfg<W, S>::min_blo
                 for (int s = 0; s < S; ++s) {
                     if (!cand[s] || bad[s]) continue;
                     const double y = c_comp[s] - t;
-                    const double gw = fold[s] + ((c_comp[s] < INFINITY && 0.0 < y) ? y : 0.0);
+                    const double gw = fold[s] + pos_part(y);  // y > 0 iff running
                     const double dd = fabs(gw - wv[s]);
                     wdiff = (wdiff < dd) ? dd : wdiff;
                 }
@@ -348,7 +341,7 @@ __global__ void __launch_bounds__(kSimWarpsPerBlock * 32, (SegCfg<W, S>::min_blo
             uint32_t li = ~0u, lq = ~0u;
 #pragma unroll
             for (int s = 0; s < S; ++s) {
-                ki[s] = (cand[s] && c_comp[s] == INFINITY) ? (((0x7FFFu - ((uint32_t)pk[s] >> 8)) << 16) | ((uint32_t)pk[s] & 0xffu))
+                ki[s] = (cand[s] && !(c_comp[s] > t)) ? (((0x7FFFu - ((uint32_t)pk[s] >> 8)) << 16) | ((uint32_t)pk[s] & 0xffu))
                                               : ~0u;
                 const uint32_t len = (uint32_t)qn[s] + gn[s];
                 kq[s] = cand[s] ? (((len < 0xFFFFFFu ? len : 0xFFFFFFu) << 8) | ((uint32_t)pk[s] & 0xffu)) : ~0u;
@@ -384,7 +377,7 @@ __global__ void __launch_bounds__(kSimWarpsPerBlock * 32, (SegCfg<W, S>::min_blo
             if (go && s * W + sl == ch) {
                 const double est = est_n[s];
                 double st, fin;
-                if (c_comp[s] == INFINITY) {  // idle: starts now
+                if (!(c_comp[s] > t)) {  // idle: starts now
                     st = t;
                     fin = t + est;
                     c_start[s] = t;

@@ -130,11 +130,11 @@ __global__ void __launch_bounds__(kSimWarpsPerBlock * 32, WarpCfg<S>::min_blocks
         if (FULL && route_mask) __builtin_assume(__isGlobal(route_mask));
 
         // ---- lane slots ----
-        // c_* = the query running at the last arrival; tail = finish of the query placed
-        // last (== c_comp while the FIFO is empty): the start of the next one queued.
-        // An idle slot holds c_start = -inf, c_est = 0, c_comp = +inf: its Eq. 1 term
-        // est - (now - start) is -inf (no max(0, .) select on a busy flag), it never
-        // completes, and "idle" is c_comp == +inf (latencies are finite).
+        // c_* = the query placed last to start on the slot; tail = finish of the query
+        // placed last (== c_comp while the FIFO is empty): the start of the next one
+        // queued. The slot is busy at time t iff c_comp > t (after the drain below, a
+        // finished query has nothing queued behind it): no busy flag is kept, and an idle
+        // slot keeps its last query's (finished) values, c_comp = -inf before the first.
         bool act[S];
         int32_t row[S], pk[S], qh[S], qn[S];  // pk = partition id | k << 8
         uint32_t gn[S], nq[S];
@@ -152,9 +152,8 @@ __global__ void __launch_bounds__(kSimWarpsPerBlock * 32, WarpCfg<S>::min_blocks
             }
             qh[s] = qn[s] = 0;
             gn[s] = nq[s] = 0;
-            c_start[s] = -INFINITY;
-            c_est[s] = 0.0;
-            c_comp[s] = INFINITY;
+            c_start[s] = c_est[s] = 0.0;
+            c_comp[s] = -INFINITY;
             tail[s] = 0.0;
             fold[s] = 0.0;
             bms[s] = wbms[s] = 0.0;
@@ -188,7 +187,7 @@ __global__ void __launch_bounds__(kSimWarpsPerBlock * 32, WarpCfg<S>::min_blocks
         auto drain = [&](double t) {
 #pragma unroll
             for (int s = 0; s < S; ++s) {
-                // pops: the queue head starts at the running query's finish (idle: +inf, never)
+                // pops: the queue head starts at the running query's finish
                 while (c_comp[s] <= t && qn[s] > 0) {
                     const int h = qh[s];
                     const double est = W.q_est[s][h][lane];
@@ -226,11 +225,8 @@ __global__ void __launch_bounds__(kSimWarpsPerBlock * 32, WarpCfg<S>::min_blocks
                         }
                     }
                 }
-                // nothing queued behind a finished query: idle (c_est stays finite, so
-                // est - (now - start) = -inf; the fold of an empty queue is already 0)
-                const bool idle = c_comp[s] <= t;
-                c_start[s] = sel_f64(idle, -INFINITY, c_start[s]);
-                c_comp[s] = sel_f64(idle, INFINITY, c_comp[s]);
+                // (a finished query with nothing queued behind it leaves the slot idle:
+                // c_comp <= t, and the fold of the empty queue is already 0)
             }
         };
 
@@ -290,7 +286,7 @@ __global__ void __launch_bounds__(kSimWarpsPerBlock * 32, WarpCfg<S>::min_blocks
                         // plain multi-slot ELSA evaluates it slot by slot below, FIFS never
                         if constexpr (FULL || (SCHED == MSV_ELSA && S == 1)) {
                             const double x = c_est[s] - (t - c_start[s]);
-                            wv[s] = fold[s] + pos_part(x);
+                            wv[s] = fold[s] + running_part(c_comp[s], t, x);
                         }
                     }
                     int bad_o = 1 << 30;  // order index of the first candidate whose size is missing
@@ -319,7 +315,7 @@ __global__ void __launch_bounds__(kSimWarpsPerBlock * 32, WarpCfg<S>::min_blocks
                             for (int s = 0; s < S; ++s) {
                                 if (!cand[s] || row[s] < 0) continue;
                                 const double y = c_comp[s] - t;
-                                const double gw = fold[s] + ((c_comp[s] < INFINITY && 0.0 < y) ? y : 0.0);
+                                const double gw = fold[s] + pos_part(y);  // y > 0 iff running
                                 const double dd = fabs(gw - wv[s]);
                                 wdiff = (wdiff < dd) ? dd : wdiff;
                             }
@@ -344,7 +340,7 @@ __global__ void __launch_bounds__(kSimWarpsPerBlock * 32, WarpCfg<S>::min_blocks
 #pragma unroll
                         for (int s = 0; s < S; ++s) {
                             const double x = c_est[s] - (t - c_start[s]);
-                            const double xp = pos_part(x);
+                            const double xp = running_part(c_comp[s], t, x);
                             stl[s] = gn[s] > 0 && !(pk[s] & kFv);
                             double flo = fold[s], fhi = fold[s];
                             if (stl[s]) {  // |left fold - exact sum| <= (n-1) 2^-53 sum; slack x2
@@ -362,7 +358,7 @@ __global__ void __launch_bounds__(kSimWarpsPerBlock * 32, WarpCfg<S>::min_blocks
                             pk[s] |= kFv;
                             stl[s] = false;
                             const double x = c_est[s] - (t - c_start[s]);
-                            vlo[s] = vhi[s] = (fold[s] + pos_part(x)) + est_n[s];
+                            vlo[s] = vhi[s] = (fold[s] + running_part(c_comp[s], t, x)) + est_n[s];
                         };
 #pragma unroll
                         for (int s = 0; s < S; ++s) {  // Step A (sched.hpp:125-130), slots in order
@@ -373,7 +369,7 @@ __global__ void __launch_bounds__(kSimWarpsPerBlock * 32, WarpCfg<S>::min_blocks
                             } else {
                                 if (act[s] && stl[s]) exact(s);
                                 const double x = c_est[s] - (t - c_start[s]);
-                                const double w = fold[s] + pos_part(x);
+                                const double w = fold[s] + running_part(c_comp[s], t, x);
                                 pred = act[s] && (sla > alpha * (w + beta * est_n[s]));
                             }
                             const unsigned bA = __ballot_sync(kFull, pred);
@@ -445,7 +441,7 @@ __global__ void __launch_bounds__(kSimWarpsPerBlock * 32, WarpCfg<S>::min_blocks
 #pragma unroll
                         for (int s = 0; s < S; ++s) {
                             const double x = c_est[s] - (t - c_start[s]);
-                            wv[s] = fold[s] + pos_part(x);
+                            wv[s] = fold[s] + running_part(c_comp[s], t, x);
                             s_eval = s + 1;
                             bool pred;
                             if constexpr (UNIT) pred = act[s] && (sla > wv[s] + est_n[s]);
@@ -513,7 +509,7 @@ __global__ void __launch_bounds__(kSimWarpsPerBlock * 32, WarpCfg<S>::min_blocks
                         uint32_t mi = ~0u;
 #pragma unroll
                         for (int s = 0; s < S; ++s) {
-                            key[s] = (cand[s] && c_comp[s] == INFINITY)
+                            key[s] = (cand[s] && !(c_comp[s] > t))
                                          ? (((0x7FFFu - ((uint32_t)pk[s] >> 8)) << 16) | ((uint32_t)pk[s] & 0xffu))
                                          : ~0u;
                             mi = key[s] < mi ? key[s] : mi;
@@ -555,11 +551,13 @@ __global__ void __launch_bounds__(kSimWarpsPerBlock * 32, WarpCfg<S>::min_blocks
                     // ---- start or enqueue on the chosen partition (engine.hpp:225-230) ----
 #pragma unroll
                     for (int s = 0; s < S; ++s) {
-                        // Straight-line and predicated on `mine`: every lane executes the same
-                        // instructions (no divergent region), only the chosen one changes state.
+                        // One slot per lane: straight-line and predicated on `mine` — every lane
+                        // executes the same instructions (no divergent region), only the chosen
+                        // one changes state. Several slots: only the chosen slot's lane runs it.
                         const bool m = mine[s];
+                        if (!(S == 1 || m)) continue;
                         const double est = est_n[s];
-                        const bool busy = c_comp[s] != INFINITY;
+                        const bool busy = c_comp[s] > t;
                         const double st = sel_f64(busy, tail[s], t);  // queued: starts when the last placed finishes
                         const double fin = st + est;
                         const bool now = m && !busy;  // idle: starts at its arrival

@@ -429,6 +429,24 @@ class Engine:
         check(self._lib.msv_run_grid(self._h, sc, n, _ptr(ps, C.c_double), len(tail_p), res, use), "run_grid")
         return results_to_numpy(res, n, len(tail_p), use, n_use)
 
+    def run_grid_noise(self, specs, noise_sigma, noise_seed, tail_p: Sequence[float] = (0.95, 0.99),
+                       usage: bool = False) -> dict:
+        """One msv_run_grid_noise call: every scenario with execution noise
+        (EngineOptions::noise_sigma / noise_seed, engine.hpp:140-145) — sample_trace ->
+        run -> tail_latency, batched on the device (K1, K5 one warp per scenario, K3).
+        `noise_sigma` / `noise_seed`: one value, or one per scenario."""
+        n = len(specs)
+        sig = np.broadcast_to(np.asarray(noise_sigma, np.float64), (n,)).copy()
+        seed = np.broadcast_to(np.asarray(noise_seed, np.uint64), (n,)).copy()
+        sc = self.scenarios(specs)
+        ps = _arr(list(tail_p) or [0.5], np.float64)
+        res = (N.Result * max(n, 1))()
+        n_use = sum(s.plan.total_instances() for s in specs)
+        use = (N.Usage * max(n_use, 1))() if usage else None
+        check(self._lib.msv_run_grid_noise(self._h, sc, n, _ptr(sig, C.c_double), seed.ctypes.data_as(
+            C.POINTER(C.c_uint64)), _ptr(ps, C.c_double), len(tail_p), res, use), "run_grid_noise")
+        return results_to_numpy(res, n, len(tail_p), use, n_use)
+
     def run(self, plan: PartitionPlan, scheduler: str, arrival, batch, duration_ms: float, table: ProfileTable,
             sla: SlaConfig, warmup_fraction: float = 0.1, routing=None, check_wait: bool = False,
             tail_p: Sequence[float] = (), noise_sigma: float = 0.0, noise_seed: int = 1) -> dict:
@@ -480,12 +498,22 @@ class Engine:
         return r
 
     def run_many(self, items, tail_p: Sequence[float] = ()) -> list[dict]:
-        specs, arrs, bats = [], [], []
+        """run() on many host traces in one device grid. Traces need not be sorted: like the
+        reference's event heap, which serves arrivals by (time, trace index)
+        (engine.hpp:101-107), an unsorted trace is stable-sorted for the device and its
+        per-query records are mapped back to trace order."""
+        specs, arrs, bats, perms = [], [], [], []
         for plan, scheduler, arrival, batch, duration_ms, table, sla, warm, routing, cw in items:
             specs.append(GridSpec(plan, table, _REPLAY_DIST, sla, 1.0, duration_ms, 0, scheduler, warm, routing,
                                   cw))
-            arrs.append(_arr(arrival, np.float64))
-            bats.append(_arr(batch, np.int32))
+            a, b = _arr(arrival, np.float64), _arr(batch, np.int32)
+            perm = None
+            if len(a) > 1 and np.any(a[1:] < a[:-1]):
+                perm = np.argsort(a, kind="stable")
+                a, b = np.ascontiguousarray(a[perm]), np.ascontiguousarray(b[perm])
+            arrs.append(a)
+            bats.append(b)
+            perms.append(perm)
         sc = self.scenarios(specs)
         n = len(specs)
         offs = np.zeros(n + 1, np.int64)
@@ -508,10 +536,14 @@ class Engine:
             P = s.plan.total_instances()
             r = {k: (v[i] if isinstance(v, np.ndarray) and k != "usage" else v) for k, v in agg.items() if k != "usage"}
             rr = recs[offs[i]:offs[i + 1]]
-            r["partition"] = np.array(rr["partition"], np.int32)
-            r["start_ms"] = np.array(rr["start_ms"])
-            r["finish_ms"] = np.array(rr["finish_ms"])
-            r["kind"] = np.array(rr["kind"], np.int32)
+            inv = slice(None)
+            if perms[i] is not None:
+                inv = np.empty(len(perms[i]), np.int64)
+                inv[perms[i]] = np.arange(len(perms[i]))
+            r["partition"] = np.array(rr["partition"], np.int32)[inv]
+            r["start_ms"] = np.array(rr["start_ms"])[inv]
+            r["finish_ms"] = np.array(rr["finish_ms"])[inv]
+            r["kind"] = np.array(rr["kind"], np.int32)[inv]
             r["busy_ms"] = agg["usage"]["busy_ms"][uo:uo + P]
             r["weighted_busy_ms"] = agg["usage"]["weighted_busy_ms"][uo:uo + P]
             r["queries"] = agg["usage"]["queries"][uo:uo + P]

@@ -695,3 +695,78 @@ def test_run_noise_long_queues(eng, ref):
             a, st = arr[part == pid], start[part == pid]
             depth = max(depth, int(np.tril(st[None, :] > a[:, None], -1).sum(axis=1).max()))
         assert depth > 64, (m, depth)
+
+
+def test_run_unsorted_trace_matches_reference(eng, ref):
+    """run() on an unsorted host trace (noise off) — the reference's heap serves
+    arrivals by (time, trace index); the device stable-sorts and maps records back."""
+    rng = np.random.default_rng(11)
+    m = W.model("bert_base")
+    plan = W.paris(m, 8)
+    arr, bat = ref.sample_trace(m.dist, 0.8 * W.capacity_qps(m, plan), 3000.0, 5)
+    arr = arr.copy()
+    arr[100:110] = arr[100]  # simultaneous arrivals keep trace-index order
+    perm = rng.permutation(len(arr))
+    a, b = arr[perm], bat[perm]
+    for sched in ("elsa", "fifs"):
+        got = eng.run(plan, sched, a, b, 3000.0, m.table, m.sla)
+        want = ref.run(plan, sched, a, b, 3000.0, m.table, m.sla)
+        for k in ("partition", "kind", "start_ms", "finish_ms", "busy_ms", "weighted_busy_ms", "queries"):
+            assert same(got[k], want[k]), (sched, k)
+        for k in ("total", "violations", "measured", "measured_violations", "horizon_ms"):
+            assert got[k] == want[k], (sched, k)
+
+
+def _digest_sum(part, start, finish):
+    """Σ msv_query_digest(i, partition, start, finish) mod 2^64 (csrc/msv_math.h), numpy."""
+    i = np.arange(len(part), dtype=np.uint64)
+    sb = np.asarray(start, np.float64).view(np.uint64)
+    fb = np.asarray(finish, np.float64).view(np.uint64)
+    m32 = np.uint64(0xFFFFFFFF)
+    c = (i * np.uint64(0x9E3779B1) + np.asarray(part, np.uint64)) & m32
+    a = (((sb & m32) ^ (fb >> np.uint64(32)) ^ c) * np.uint64(0x85EBCA6B)) & m32
+    b = ((((sb >> np.uint64(32)) ^ (fb & m32) ^ c) * np.uint64(0x27D4EB2F)) + c) & m32
+    with np.errstate(over="ignore"):
+        return int(((a << np.uint64(32)) | b).sum(dtype=np.uint64))
+
+
+def test_noise_grid_matches_reference(eng, ref):
+    """noisy scenarios at grid scale (msv_run_grid_noise: K1 traces, host
+    multiplier streams, K5 one warp per scenario, K3 tails) against the reference's
+    sample_trace -> run(noise) -> tail_latency per scenario: counts, placement digest,
+    horizon and tails bit-identical."""
+    if ref.kind != "reference":
+        pytest.skip("noise parity needs oracle/_ref")
+    rng = np.random.default_rng(3)
+    specs, sig, seeds = [], [], []
+    for name, gpus in (("mobilenet", 8), ("bert_base", 8), ("resnet50", 1), ("bert_base", 2)):
+        m = W.model(name)
+        plan = W.paris(m, gpus)
+        for load in (0.4, 0.8, 1.1):
+            for sched in ("elsa", "fifs"):
+                specs.append(GridSpec(plan, m.table, m.dist, m.sla, load * W.capacity_qps(m, plan),
+                                      float(rng.choice([300.0, 900.0])), int(rng.integers(1, 1000)), sched,
+                                      float(rng.choice([0.0, 0.1, 0.3]))))
+                sig.append(float(rng.choice([0.05, 0.3, 0.8])))
+                seeds.append(int(rng.integers(0, 2**63)))
+    got = eng.run_grid_noise(specs, sig, seeds, (0.95, 0.99), usage=True)
+    uo = 0
+    for k, s in enumerate(specs):
+        arr, bat = ref.sample_trace(s.dist, s.rate_qps, s.duration_ms, s.seed)
+        want = ref.run_noise(s.plan, s.scheduler, arr, bat, s.duration_ms, s.table, s.sla, s.warmup_fraction, None,
+                             sig[k], seeds[k])
+        assert got["status"][k] == 0
+        assert got["total"][k] == len(arr)
+        for f in ("violations", "measured", "measured_violations"):
+            assert got[f][k] == want[f], (k, f)
+        assert got["horizon_ms"][k] == want["horizon_ms"], k
+        assert int(got["placement_hash"][k]) == _digest_sum(want["partition"], want["start_ms"], want["finish_ms"]), k
+        P = s.plan.total_instances()
+        for f in ("busy_ms", "weighted_busy_ms", "queries"):
+            assert same(got["usage"][f][uo:uo + P], want[f]), (k, f)
+        uo += P
+        lat = want["finish_ms"] - arr
+        meas = lat[arr >= want["warmup_ms"]]
+        for j, p in enumerate((0.95, 0.99)):
+            w = ref.tail_latency(meas, p) if len(meas) else float("nan")
+            assert same(got["tail"][k, j], w), (k, p)

@@ -1,6 +1,6 @@
 set -x
 mkdir -p gpurun_out/r02/ab
-T=v2d
+T=v2e
 timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/r02/gpu_tests_$T.log 2>&1
 tail -n 3 gpurun_out/r02/gpu_tests_$T.log
 timeout 600 python tools/diag_classes.py > gpurun_out/r02/ab/classes_$T.log 2>&1
