@@ -53,11 +53,11 @@ template <int S>
 struct WarpSmem {
     static constexpr int QC = WarpCfg<S>::qcap;
     double q_est[S][QC][32];  // queued latencies (ring; starts/finishes follow from them)
-    double win_t[32];
-    double win_s[32];   // start of window arrival j (written by the chosen lane)
-    double win_f[32];   // finish of window arrival j
-    int32_t win_b[32];
-    int32_t win_p[32];  // partition id | kind << 8
+    // window arrival j: (arrival, batch) staged by lane j, read by every lane with one
+    // 16-byte load; (start, finish) written by the chosen lane with one 16-byte store
+    double2 win_tb[32];  // {arrival, batch bits}
+    double2 win_sf[32];  // {start, finish}
+    int32_t win_p[32];   // partition id | kind << 8
     uint32_t g_head[S][32];  // overflow list head / tail per lane slot
     uint32_t g_tail[S][32];
     double dd_hi[S][32];     // overflow mode: double-double sum of the queued latencies
@@ -139,6 +139,7 @@ __global__ void __launch_bounds__(kSimWarpsPerBlock * 32, WarpCfg<S>::min_blocks
         int32_t row[S], pk[S], qh[S], qn[S];  // pk = partition id | k << 8
         uint32_t gn[S], nq[S];
         double c_start[S], c_est[S], c_comp[S], tail[S], fold[S], bms[S], wbms[S];
+        uint32_t row_sh[S];  // shared address of the slot's latency row, minus one cell: + b*8 = L(k, b)
 #pragma unroll
         for (int s = 0; s < S; ++s) {
             const int o = s * 32 + lane;
@@ -155,6 +156,7 @@ __global__ void __launch_bounds__(kSimWarpsPerBlock * 32, WarpCfg<S>::min_blocks
             c_start[s] = c_est[s] = 0.0;
             c_comp[s] = -INFINITY;
             tail[s] = 0.0;
+            row_sh[s] = lat_sh + (uint32_t)(row[s] - 1) * 8u;
             fold[s] = 0.0;
             bms[s] = wbms[s] = 0.0;
         }
@@ -239,8 +241,7 @@ __global__ void __launch_bounds__(kSimWarpsPerBlock * 32, WarpCfg<S>::min_blocks
             for (int base = 0; base < n; base += 32) {
                 const double cur_t = nx_t;
                 __syncwarp();
-                W.win_t[lane] = cur_t;
-                W.win_b[lane] = nx_b;
+                W.win_tb[lane] = make_double2(cur_t, __longlong_as_double((long long)nx_b));
                 __syncwarp();
                 if (base + 32 + lane < n) {  // prefetch the next window
                     nx_t = g_arr[base + 32 + lane];
@@ -252,8 +253,9 @@ __global__ void __launch_bounds__(kSimWarpsPerBlock * 32, WarpCfg<S>::min_blocks
                 }
                 const int cnt = min(32, n - base);
                 for (int j = 0; j < cnt; ++j) {
-                    const double t = W.win_t[j];
-                    const int b = W.win_b[j];
+                    const double2 tb = W.win_tb[j];
+                    const double t = tb.x;
+                    const int b = (int)__double_as_longlong(tb.y);
                     const int i = base + j;
                     // The new query's latency on each partition depends on its batch only:
                     // load it ahead of the drain (FULL: batch clamped into the table for
@@ -266,7 +268,7 @@ __global__ void __launch_bounds__(kSimWarpsPerBlock * 32, WarpCfg<S>::min_blocks
                             est_n[s] = s_lat[(row[s] < 0 ? 0 : row[s]) + bl - 1];
                             if (row[s] < 0) est_n[s] = 0.0;
                         } else {
-                            est_n[s] = lds_f64(lat_sh + (uint32_t)(row[s] + b - 1) * 8u);
+                            est_n[s] = lds_f64(row_sh[s] + (uint32_t)b * 8u);
                         }
                     }
                     drain(t);
@@ -568,11 +570,15 @@ __global__ void __launch_bounds__(kSimWarpsPerBlock * 32, WarpCfg<S>::min_blocks
                         c_comp[s] = sel_f64(now, fin, c_comp[s]);
                         // appending extends the left fold exactly (a stale fold stays stale)
                         fold[s] = sel_f64(push, fold[s] + est, fold[s]);
-                        if (push) {
-                            if (gn[s] == 0 && qn[s] < QC) {
-                                W.q_est[s][(qh[s] + qn[s]) & (QC - 1)][lane] = est;
-                                qn[s] += 1;
-                            } else {
+                        // ring append predicated (no divergent region); the overflow list behind
+                        // a full ring is the rare branch
+                        const bool ring_ok = gn[s] == 0 && qn[s] < QC;
+                        if (push && ring_ok) {
+                            W.q_est[s][(qh[s] + qn[s]) & (QC - 1)][lane] = est;
+                            qn[s] += 1;
+                        }
+                        if (push && !ring_ok) {
+                            {
                                 if (kLazy) {  // overflow mode: keep the double-double sum
                                     double hi = 0.0, lo = 0.0;
                                     if (gn[s] == 0) {  // entering it: sum the ring, the fold is exact
@@ -595,8 +601,7 @@ __global__ void __launch_bounds__(kSimWarpsPerBlock * 32, WarpCfg<S>::min_blocks
                             }
                         }
                         if (m) {
-                            W.win_s[j] = st;
-                            W.win_f[j] = fin;
+                            W.win_sf[j] = make_double2(st, fin);
                             W.win_p[j] = (pk[s] & 0xff) | (kind << 8);
                             if (FULL) {  // PartitionUsage (engine.hpp:175-177), completion order
                                 const double ran = fin - st;
@@ -611,7 +616,8 @@ __global__ void __launch_bounds__(kSimWarpsPerBlock * 32, WarpCfg<S>::min_blocks
                 __syncwarp();
                 if (lane < cnt) {
                     const int i = base + lane;
-                    const double st = W.win_s[lane], fin = W.win_f[lane];
+                    const double2 sf = W.win_sf[lane];
+                    const double st = sf.x, fin = sf.y;
                     const int pw = W.win_p[lane];
                     const double lat = fin - cur_t;  // latency = finish - arrival
                     const bool met = lat <= sla;

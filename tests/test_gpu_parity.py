@@ -770,3 +770,26 @@ def test_noise_grid_matches_reference(eng, ref):
         for j, p in enumerate((0.95, 0.99)):
             w = ref.tail_latency(meas, p) if len(meas) else float("nan")
             assert same(got["tail"][k, j], w), (k, p)
+
+
+def test_c4_all_fleets_full_parity(eng, ref):
+    """C4 at full fleet count — all 3,435 distinct 8-GPU fleets, one seed,
+    reduced duration — every scenario's placement digest, tails and counts equal to the
+    compiled reference, and the same PARIS argmin."""
+    from paper_2202_13481_b200.distributed import paris_argmin
+    specs, cands = W.c4(seeds=1, queries=2e4)
+    assert len(cands) == 3435
+    got = eng.run_grid(specs, (0.95, 0.99))
+    want = ref.run_grid(specs, (0.95, 0.99))
+    assert_grid_equal(got, want)
+    assert paris_argmin(got["tail"][:, 1], len(cands), 1)[0] == paris_argmin(want["tail"][:, 1], len(cands), 1)[0]
+
+
+def test_c5_slice_full_size_parity(eng, ref):
+    """a C5 slice at full query count — 75 scenarios (every model, plan and
+    load of the grid) x 10^6 queries — bit-identical to the compiled reference."""
+    specs = W.c5(n_scenarios=75, queries=1e6)
+    got = eng.run_grid(specs, (0.95, 0.99))
+    want = ref.run_grid(specs, (0.95, 0.99))
+    assert_grid_equal(got, want)
+    assert int(got["total"].sum()) > 7.4e7
