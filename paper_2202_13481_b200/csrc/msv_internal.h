@@ -208,6 +208,9 @@ cudaError_t launch_sim(int W, int S, int sched, bool records, const SimParams& p
                        cudaStream_t stream);
 size_t sim_smem_bytes(int W, int S, int n_cells);
 int sim_max_blocks_per_sm(int W, int S, int sched, bool records, bool full, bool lazy, int n_cells);
+// Raise a kernel's dynamic shared-memory limit on the current device (never lowers it;
+// thread-safe: contexts on several threads launch the same kernels).
+cudaError_t ensure_dyn_smem(const void* fn, size_t bytes);
 // Arithmetic self-checks (msv_selftest.cu).
 cudaError_t launch_log1p_digest(int variant, uint64_t seed, int64_t n, int64_t chunk, uint64_t* d_out,
                                 cudaStream_t stream);

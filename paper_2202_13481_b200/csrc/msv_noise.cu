@@ -448,7 +448,7 @@ cudaError_t launch_noise(const NoiseParams* d_jobs, int n_jobs, int max_cells, c
     // window) already eats most of the default 48 KB, so the default dynamic limit is
     // only ~15 KB (profiles of ~1,000 cells failed to launch).
     const size_t smem = (size_t)2 * max_cells * sizeof(double);
-    const cudaError_t e = cudaFuncSetAttribute(sim_noise_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    const cudaError_t e = ensure_dyn_smem((const void*)sim_noise_kernel, smem);
     if (e != cudaSuccess) return e;
     if (n_jobs <= 0) return cudaSuccess;
     sim_noise_kernel<<<n_jobs, 32, smem, stream>>>(d_jobs);

@@ -32,6 +32,10 @@
 // wait check / usage / records in the launch) carries none of those features' work.
 #include <cuda_pipeline.h>
 
+#include <map>
+#include <mutex>
+#include <utility>
+
 #include "msv_device.cuh"
 
 namespace msv {
@@ -505,11 +509,27 @@ static void* sim_fn_for(int W, int S, int sched, bool rec, bool full, bool lazy)
     return W == 32 ? sim_warp_fn(S, sched, rec, full, lazy) : pick_sim(W, S, sched, rec, full);
 }
 
+// Dynamic shared-memory opt-in, raised monotonically per (kernel, device) under a lock:
+// several contexts (threads) may launch the same kernel with different table sizes at
+// once, and a lower limit set by one must never invalidate another's launch in flight.
+cudaError_t ensure_dyn_smem(const void* fn, size_t bytes) {
+    static std::mutex mu;
+    static std::map<std::pair<const void*, int>, size_t> limit;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lk(mu);
+    size_t& cur = limit[{fn, dev}];
+    if (bytes <= cur) return cudaSuccess;
+    const cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    if (e == cudaSuccess) cur = bytes;
+    return e;
+}
+
 int sim_max_blocks_per_sm(int W, int S, int sched, bool records, bool full, bool lazy, int n_cells) {
     void* fn = sim_fn_for(W, S, sched, records, full, lazy);
     if (!fn) return 0;
     const size_t smem = sim_smem_bytes(W, S, n_cells);
-    if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) return 0;
+    if (ensure_dyn_smem(fn, smem) != cudaSuccess) return 0;
     int blocks = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, fn, kSimWarpsPerBlock * 32, smem) != cudaSuccess)
         return 0;
@@ -521,7 +541,7 @@ cudaError_t launch_sim(int W, int S, int sched, bool records, const SimParams& p
     void* fn = sim_fn_for(W, S, sched, records, full, p.lazy != 0);
     if (!fn) return cudaErrorInvalidValue;
     const size_t smem = sim_smem_bytes(W, S, p.n_cells);
-    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e = ensure_dyn_smem(fn, smem);
     if (e != cudaSuccess) return e;
     void* args[] = {const_cast<SimParams*>(&p)};
     return cudaLaunchKernel(fn, dim3(blocks), dim3(kSimWarpsPerBlock * 32), args, smem, stream);

@@ -272,7 +272,7 @@ cudaError_t launch_tail(const TailJob* d_jobs, int n_jobs, const double* d_p, in
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const size_t smem = sizeof(TailSmem);
-    cudaError_t e = cudaFuncSetAttribute(tail_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e = ensure_dyn_smem((const void*)tail_kernel, smem);
     if (e != cudaSuccess) return e;
     const int blocks = n_jobs < sms * 3 ? n_jobs : sms * 3;
     tail_kernel<<<blocks, kTailThreads, smem, stream>>>(d_jobs, n_jobs, d_p, n_p);
