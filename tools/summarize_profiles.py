@@ -63,6 +63,7 @@ def main():
     ap.add_argument("--bench", type=Path)
     ap.add_argument("--reference", type=Path)
     ap.add_argument("--opcodes", type=Path, default=None, help="report holding one K2 launch (source page)")
+    ap.add_argument("--note", default=None, help="what the capture is (command, grid)")
     ap.add_argument("--queries-per-step", type=float, default=None,
                     help="simulated queries of the captured step (default: from the bench line)")
     a = ap.parse_args()
@@ -81,7 +82,7 @@ def main():
     qps = a.queries_per_step
     if qps is None and bench:
         cfg = bench["config"]
-        qps = cfg["scenarios_per_gpu"] * cfg["queries_per_scenario"]
+        qps = cfg.get("scenarios", cfg.get("scenarios_per_gpu")) * cfg["queries_per_scenario"]
     ADD = ("duration_ms", "warp_instructions", "dram_read", "dram_write")
     kernels, raw = {}, collections.defaultdict(list)
     rows = ncu_csv(a.reps[0], "--page", "raw")
@@ -158,11 +159,14 @@ def main():
         s = sum(tot.values())
         shares = {k: {"launches": cnt[k], "total_ms": round(v / 1e6, 3), "share": round(v / s, 4)}
                   for k, v in tot.items()}
+    import hashlib
+    csrc = ROOT / "paper_2202_13481_b200" / "csrc"
+    sha = hashlib.sha256(b"".join(p.read_bytes() for p in (csrc / "msv_sim_warp.cu", csrc / "msv_sim.cu"))).hexdigest()
     summary = {
-        "note": "ncu --set full --clock-control none capture of every kernel of one step of `python bench.py "
-                "--no-cpu-baseline --steps 1 --warmup 3` (10,240 scenarios x 1e5 queries, four chunks) on one "
-                "B200; per kernel: its launches in the step summed, per-query figures over the step's queries. "
-                "ncu times are serialised / cold-cache: compare shares, not absolutes.",
+        "note": a.note or ("ncu --set full --clock-control none capture of every kernel of one bench step on one "
+                           "B200; per kernel: its launches in the step summed, per-query figures over the step's "
+                           "queries. ncu times are serialised / cold-cache: compare shares, not absolutes."),
+        "kernel_sources_sha256": sha,
         "queries_per_step": qps,
         "issue_peak_warp_inst_per_s": "148 SMs x 4 schedulers x SM clock (1 warp-instruction / scheduler / clk)",
         "kernels": kernels,
