@@ -118,6 +118,7 @@ __global__ void __launch_bounds__(kSimWarpsPerBlock * 32, WarpCfg<S>::min_blocks
         double* samples = d.samples;
         msv_record* rec = d.records;
         const double sla = d.sla, warmup = d.warmup_ms;
+        const double sla_act = lane < d.P ? sla : -INFINITY;  // Step A's bound, false on lanes without a partition
         const bool check_wait = FULL && p.any_check_wait && (d.flags & MSV_FLAG_CHECK_WAIT);
         const int bmax = d.b_max;
         const uint64_t* route_mask = d.route_mask;
@@ -429,7 +430,7 @@ __global__ void __launch_bounds__(kSimWarpsPerBlock * 32, WarpCfg<S>::min_blocks
                         // critical path.
                         const unsigned below = (1u << lane) - 1u;
                         bool pred;
-                        if constexpr (UNIT) pred = act[0] && (sla > wv[0] + est_n[0]);
+                        if constexpr (UNIT) pred = sla_act > wv[0] + est_n[0];  // inactive lanes: -inf
                         else pred = act[0] && (sla > alpha * (wv[0] + beta * est_n[0]));
                         const unsigned bA = __ballot_sync(kFull, pred);  // Step A (sched.hpp:125-130)
                         mine[0] = pred && (bA & below) == 0;
