@@ -90,26 +90,58 @@ def config(args, world, specs):
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    """SM clocks and throttle reasons sampled during the timed region, in process through
+    NVML (an nvidia-smi process every 200 ms measurably perturbed the timed loop); falls
+    back to nvidia-smi when NVML is unavailable."""
     Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    NAMES = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
 
-    def __init__(self, index: int):
+    def __init__(self, index: int, interval: float = 0.25):
         self.index = index
-        self.rows: list[list[str]] = []
+        self.interval = interval
+        self.rows: list[tuple[float, float, set]] = []
         self._stop = threading.Event()
         self._t = threading.Thread(target=self._run, daemon=True)
+        self._nvml = None
+        try:
+            import pynvml as nv
+            nv.nvmlInit()
+            # the process's CUDA ordinal -> NVML handle (honours CUDA_VISIBLE_DEVICES)
+            vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+            ordinal = int(vis.split(",")[index]) if vis and vis.split(",")[index].isdigit() else index
+            self._h = nv.nvmlDeviceGetHandleByIndex(ordinal)
+            self._bits = {nv.nvmlClocksEventReasonHwSlowdown: "hw_slowdown",
+                          nv.nvmlClocksEventReasonHwThermalSlowdown: "hw_thermal_slowdown",
+                          nv.nvmlClocksEventReasonSwThermalSlowdown: "sw_thermal_slowdown",
+                          nv.nvmlClocksEventReasonSwPowerCap: "sw_power_cap"}
+            self._nvml = nv
+        except Exception:
+            self._nvml = None
+
+    def _sample(self):
+        nv = self._nvml
+        if nv is not None:
+            sm = float(nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM))
+            mx = float(nv.nvmlDeviceGetMaxClockInfo(self._h, nv.NVML_CLOCK_SM))
+            r = nv.nvmlDeviceGetCurrentClocksEventReasons(self._h)
+            return [(sm, mx, {name for bit, name in self._bits.items() if r & bit})]
+        out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                              "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+        rows = []
+        for line in out.stdout.strip().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) >= 6 and f[0].replace(".", "").isdigit():
+                rows.append((float(f[0]), float(f[1]), {self.NAMES[i] for i in range(4) if f[2 + i] == "Active"}))
+        return rows
 
     def _run(self):
         while not self._stop.is_set():
             try:
-                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
-                                      "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
-                for line in out.stdout.strip().splitlines():
-                    self.rows.append([x.strip() for x in line.split(",")])
+                self.rows += self._sample()
             except Exception:
                 pass
-            self._stop.wait(0.2)
+            self._stop.wait(self.interval)
 
     def __enter__(self):
         self._t.start()
@@ -121,13 +153,10 @@ class ClockSampler:
 
     def summary(self):
         if not self.rows:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in self.rows for i in range(4) if len(r) > 2 + i and r[2 + i] == "Active"})
-        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.rows)}
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["clock sampling unavailable"]}
+        return {"sm_mhz": float(np.median([r[0] for r in self.rows])), "sm_max_mhz": max(r[1] for r in self.rows),
+                "reasons": sorted(set().union(*(r[2] for r in self.rows))), "samples": len(self.rows),
+                "source": "nvml" if self._nvml is not None else "nvidia-smi"}
 
 
 def host_cores() -> int:
