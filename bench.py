@@ -331,16 +331,25 @@ def main():
         prof, prof_src, fresh = profile_summary([csrc / "msv_sim_warp.cu", csrc / "msv_sim.cu"])
         sim_launches = max(1, round(launches / args.steps / 3))  # K1/K2/K3 once per chunk
         q_launch = queries / sim_launches
-        k2 = prof["kernels"]["K2 sim_warp_kernel"] if prof else None
-        traffic = k2["traffic_bytes_per_query"] * q_launch if (k2 and fresh) else None
+        # K2's per-query counters: the one-slot class (the bulk of the grid's queries)
+        k2 = None
+        if prof:
+            cls = prof.get("k2_classes_standalone", {})
+            one = next((v for kname, v in cls.items() if kname.startswith("one slot")), None)
+            k2 = ({"warp_instructions_per_query": one["warp_instructions_per_query"],
+                   "traffic_bytes_per_query": one["dram_bytes_per_query"]} if one
+                  else prof["kernels"].get("K2 sim_warp_kernel"))
+        traffic = k2["traffic_bytes_per_query"] * q_launch if (k2 and fresh and k2.get("traffic_bytes_per_query")) else None
         clk_mhz = clk.summary().get("sm_mhz") or 1965.0
         issue = None
-        if k2:
+        if k2 and k2.get("warp_instructions_per_query"):
             sms = torch.cuda.get_device_properties(dev).multi_processor_count
             pk = sms * 4 * clk_mhz * 1e6  # one warp-instruction per scheduler per clock
-            wi = sum(v["warp_instructions_per_query"] for kname, v in prof["kernels"].items()
-                     if "warp_instructions_per_query" in v and not kname.startswith("K4"))
-            issue = {"warp_inst_per_query_k2": k2["warp_instructions_per_query"], "step_warp_inst_per_query": wi,
+            wk2 = k2["warp_instructions_per_query"]
+            wi = wk2 + sum(v.get("warp_instructions_per_query") or 0.0 for kname, v in prof["kernels"].items()
+                           if kname.startswith(("K1", "K3")))
+            issue = {"warp_inst_per_query_k2": wk2, "k2_basis": "one-slot K2 class (P <= 32), ncu source page",
+                     "step_warp_inst_per_query": wi,
                      "step_frac": wi * total_q * args.steps / (dev_ms_max / 1000.0) / world / pk,
                      "peak_warp_inst_per_s": pk, "source": prof_src, "fresh": fresh}
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,

@@ -6,6 +6,7 @@ relative; we assert exact equality and report the max relative error on failure)
 from __future__ import annotations
 
 import subprocess
+import sys
 from pathlib import Path
 
 import numpy as np
@@ -793,3 +794,32 @@ def test_c5_slice_full_size_parity(eng, ref):
     want = ref.run_grid(specs, (0.95, 0.99))
     assert_grid_equal(got, want)
     assert int(got["total"].sum()) > 7.4e7
+
+
+def test_multi_wave_grids_subprocess():
+    """Grids larger than the memory budget run as waves alternating between two buffer
+    regions, wave w + 1 overlapping wave w (and K1 grouped in the overlapping waves). A
+    tiny budget (MSV_TEST_WAVE_MB, read once per process) forces many waves on a small
+    grid; results must equal the compiled reference."""
+    code = r'''
+import sys; sys.path.insert(0, %r)
+import numpy as np
+from paper_2202_13481_b200 import Engine
+from paper_2202_13481_b200 import workloads as W
+from tests import oracle_py as O
+specs = W.c5(n_scenarios=150, queries=4e4) + W.c2(seeds=4, queries=2e4)
+eng = Engine(0)
+g = eng.grid(specs)
+g.launch(); g.launch()
+got = g.results()
+want = O.best_oracle().run_grid(specs, (0.95, 0.99))
+for k in ("total", "violations", "measured", "measured_violations", "placement_hash", "horizon_ms"):
+    assert np.array_equal(got[k], want[k]), k
+assert np.array_equal(got["tail"], want["tail"], equal_nan=True)
+r = eng.run_grid(specs)
+assert np.array_equal(r["placement_hash"], want["placement_hash"])
+print("ok", len(specs))
+''' % str(ROOT)
+    env = dict(__import__("os").environ, MSV_TEST_WAVE_MB="60")
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=900, env=env)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stdout[-2000:] + r.stderr[-3000:]
