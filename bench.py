@@ -320,7 +320,6 @@ def main():
 
     if rank == 0:
         sim_s = stage["sim_ms"] / 1000.0
-        achieved = queries * SIM_BYTES_PER_QUERY / sim_s / 1e9
         peaks = {}
         try:
             peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text())
@@ -340,6 +339,14 @@ def main():
                    "traffic_bytes_per_query": one["dram_bytes_per_query"]} if one
                   else prof["kernels"].get("K2 sim_warp_kernel"))
         traffic = k2["traffic_bytes_per_query"] * q_launch if (k2 and fresh and k2.get("traffic_bytes_per_query")) else None
+        # K2's time in the timed (overlapped) step: its share of the launch list of this very
+        # command (ncu, fresh capture) times the measured step time; the serialised stage
+        # timing (stage_ms) is the fallback
+        share = None
+        if prof and fresh:
+            share = (prof.get("launch_shares_bench", {}).get("K2 sim_warp_kernel") or {}).get("share")
+        k2_s = (share * dev_ms_max / args.steps / 1000.0) if share else sim_s
+        achieved = queries * SIM_BYTES_PER_QUERY / k2_s / 1e9
         clk_mhz = clk.summary().get("sm_mhz") or 1965.0
         issue = None
         if k2 and k2.get("warp_instructions_per_query"):
@@ -367,6 +374,8 @@ def main():
                              "traffic_source": (prof_src if fresh else f"stale capture {prof_src}: null")
                              if prof else None,
                              "algorithmic_bytes_per_launch": SIM_BYTES_PER_QUERY * q_launch,
+                             "k2_time_s": k2_s, "k2_time_basis": ("K2 share %.4f of the ncu launch list x step time" % share)
+                             if share else "serialised stage timing",
                              "kernel": "sim_warp_kernel (K2)", "issue": issue,
                              "note": "K2 is issue-bound (dependent FP64 state machine): 'issue' is the binding "
                                      "roof; HBM fraction is small by construction (DESIGN.md §4)"},

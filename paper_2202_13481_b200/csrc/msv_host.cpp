@@ -1010,7 +1010,14 @@ int launch_chunk(msv_grid* g, const msv_grid::Chunk& ch, int counter_base, cudaS
     const bool par = class_streams && ncls > 1;
     std::vector<size_t> corder(ncls);
     for (size_t c = 0; c < ncls; ++c) corder[c] = c;
+    // Classes with the slowest scenarios (more partitions per lane) launch first, so their
+    // blocks are resident from the start instead of waiting for the largest class's
+    // persistent blocks to drain, and the slowest scenarios do not form the tail (C5:
+    // +3 % device-resident and end to end). MSV_CLASS_ORDER=count: largest class first (A/B).
+    static const bool slow_first = !(getenv("MSV_CLASS_ORDER") && std::string(getenv("MSV_CLASS_ORDER")) == "count");
     std::stable_sort(corder.begin(), corder.end(), [&](size_t a, size_t b) {
+        const ClassKey &ka = ch.classes[a].first, &kb = ch.classes[b].first;
+        if (slow_first && ka.S * 32 / ka.W != kb.S * 32 / kb.W) return ka.S * 32 / ka.W > kb.S * 32 / kb.W;
         return ch.classes[a].second.size() > ch.classes[b].second.size();
     });
     if (par) {
