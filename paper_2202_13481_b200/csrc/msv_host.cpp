@@ -1017,7 +1017,7 @@ int launch_chunk(msv_grid* g, const msv_grid::Chunk& ch, int counter_base, cudaS
     static const bool slow_first = !(getenv("MSV_CLASS_ORDER") && std::string(getenv("MSV_CLASS_ORDER")) == "count");
     std::stable_sort(corder.begin(), corder.end(), [&](size_t a, size_t b) {
         const ClassKey &ka = ch.classes[a].first, &kb = ch.classes[b].first;
-        if (slow_first && ka.S * 32 / ka.W != kb.S * 32 / kb.W) return ka.S * 32 / ka.W > kb.S * 32 / kb.W;
+        if (slow_first && ka.S != kb.S) return ka.S > kb.S;  // slots per lane: per-arrival cost
         return ch.classes[a].second.size() > ch.classes[b].second.size();
     });
     if (par) {
