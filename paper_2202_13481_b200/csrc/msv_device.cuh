@@ -146,6 +146,35 @@ __device__ __forceinline__ uint64_t seg_minm_u64(uint64_t v, unsigned mask) {
     }
     return v;
 }
+// Minimum and maximum of u32 values over a segment (segment-uniform branches).
+template <int W>
+__device__ __forceinline__ void seg_range_u32(uint32_t& lo, uint32_t& hi, unsigned mask) {
+    if constexpr (W == 32) {
+        lo = __reduce_min_sync(mask, lo);
+        hi = __reduce_max_sync(mask, hi);
+    } else {
+#pragma unroll
+        for (int off = W / 2; off > 0; off >>= 1) {
+            const uint32_t a = __shfl_xor_sync(mask, lo, off), b = __shfl_xor_sync(mask, hi, off);
+            lo = a < lo ? a : lo;
+            hi = b > hi ? b : hi;
+        }
+    }
+}
+
+// K3 key bounds from the high words of a scenario's (non-negative) latencies: every
+// latency's order key lies in [min_hi:00000000, max_hi:ffffffff]. With no latency
+// (lo > hi) the bounds come out empty (min > max) and K3 derives them itself.
+__device__ __forceinline__ void lat_key_bounds(uint32_t hmin, uint32_t hmax, uint64_t& kmin, uint64_t& kmax) {
+    if (hmin > hmax) {
+        kmin = ~0ull;
+        kmax = 0;
+        return;
+    }
+    kmin = (uint64_t)(hmin | 0x80000000u) << 32;
+    kmax = ((uint64_t)(hmax | 0x80000000u) << 32) | 0xffffffffull;
+}
+
 // std::max on doubles as the reference writes it: (a < b) ? b : a.
 template <int W>
 __device__ __forceinline__ double seg_max_f64(double v, unsigned mask) {

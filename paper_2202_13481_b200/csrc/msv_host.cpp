@@ -362,6 +362,7 @@ struct msv_grid {
     float t_total = 0, t_trace = 0, t_sim = 0, t_tail = 0;
     int64_t queries = -1;
     std::vector<int64_t> host_n;  // replay: trace lengths
+    std::vector<int64_t> user_off;  // replay: each trace's offset in the caller's arrays (from offsets[0])
     std::vector<double> cost;     // expected work per scenario (longest-first order, class shares)
     // Multi-device grid: one sub-grid per context member, over contiguous scenario
     // ranges [dev_lo[k], dev_lo[k+1]) (usage slots from dev_use_lo[k]).
@@ -449,13 +450,25 @@ std::vector<uint64_t> route_masks(const std::vector<DevPart>& parts, const Routi
     return m;
 }
 
+// K3's candidate scratch of a scenario: its overflow-link buffer (cap u32 words), dead
+// once the simulation kernel is done with the scenario, viewed as 8-byte keys.
+void tail_scratch(uint32_t* next, int64_t cap, msv::TailJob& l) {
+    const uintptr_t a = ((uintptr_t)next + 7) & ~(uintptr_t)7;
+    const int64_t bytes = cap * 4 - (int64_t)(a - (uintptr_t)next);
+    l.cand = bytes >= 8 ? reinterpret_cast<uint64_t*>(a) : nullptr;
+    l.cand_cap = bytes >= 8 ? bytes / 8 : 0;
+}
+
 int64_t trace_capacity(double rate_qps, double duration_ms) {
     const double mean = rate_qps * duration_ms / 1000.0;
     if (!(mean < 2.0e9)) return -1;  // the kernels index a trace with 32-bit ints
     // MSV_TEST_SHORT_CAP=1 (tests only): undersized capacities exercise the re-run path
     static const bool short_cap = getenv("MSV_TEST_SHORT_CAP") && atoi(getenv("MSV_TEST_SHORT_CAP")) != 0;
     if (short_cap) return (int64_t)ceil(0.5 * mean) + 1;
-    return (int64_t)ceil(mean + 10.0 * sqrt(mean) + 160.0);
+    // a multiple of 32 queries: every scenario's trace then starts on a 256-byte boundary,
+    // so the planar latency rows K3 streams are whole 128-byte lines
+    const int64_t c = (int64_t)ceil(mean + 10.0 * sqrt(mean) + 160.0);
+    return (c + 31) & ~(int64_t)31;
 }
 
 // MSV_HOST_TIMING=1: per-phase host timings of grid builds on stderr (diagnostics).
@@ -538,9 +551,12 @@ int grid_build(msv_ctx* ctx, const msv_scenario* sc, int64_t n, const double* ta
             g->cap[i] = cap_override ? cap_override[i] : trace_capacity(sc[i].rate_qps, sc[i].duration_ms);
             if (g->cap[i] < 0) return fail(MSV_PARAM, "sample_trace: expected trace too long");
         } else {
-            g->cap[i] = offsets[i + 1] - offsets[i];
-            if (g->cap[i] < 0) return fail(MSV_PARAM, "replay: offsets must be nondecreasing");
-            if (g->cap[i] >= (int64_t)0xFFFFFFFFll) return fail(MSV_PARAM, "replay: trace too long");
+            const int64_t len = offsets[i + 1] - offsets[i];
+            if (len < 0) return fail(MSV_PARAM, "replay: offsets must be nondecreasing");
+            if (len >= (int64_t)0xFFFFFFFFll - 32) return fail(MSV_PARAM, "replay: trace too long");
+            // whole 32-query blocks: the one-warp simulation kernel writes the latencies of
+            // a block (also a trace's last, partial one) over the block's 256 bytes
+            g->cap[i] = (len + 31) & ~(int64_t)31;
             const int b_max = ctx->profiles[sc[i].profile].b_max;
             for (int64_t q = offsets[i]; q < offsets[i + 1]; ++q) {
                 if (batch[q] < 1 || batch[q] > b_max)
@@ -603,6 +619,9 @@ int grid_build(msv_ctx* ctx, const msv_scenario* sc, int64_t n, const double* ta
         for (int64_t q : wave_q) g->max_wave_q = std::max(g->max_wave_q, q);
     }
     pt.mark("waves");
+    if (pt.on)
+        fprintf(stderr, "[msv] grid n=%lld: %zu wave(s), %lld slots each, budget %.1f GB (free %.1f GB)\n", (long long)n,
+                g->waves.size(), (long long)g->max_wave_q, budget / 1e9, free_device_bytes() / 1e9);
     // Expected work per scenario for longest-first scheduling: queries x (1 + 4 rho^2),
     // rho = offered load over the plan's nominal capacity sum_p 1000 / E_b[latency(k_p, b)].
     std::vector<double> cost(n);
@@ -924,6 +943,7 @@ int grid_build(msv_ctx* ctx, const msv_scenario* sc, int64_t n, const double* ta
         l.samples = d.samples;
         l.src = g->B->d_out.as<DevOut>() + i;
         l.out = g->B->d_tails.as<double>() + 4 * i;
+        tail_scratch(d.next, g->cap[i], l);
     }
     ctx->h2d += (int64_t)(n * (sizeof(DevScen) + sizeof(msv::TraceJob) + sizeof(msv::TailJob)) +
                           parts_h.size() * sizeof(DevPart) + masks_h.size() * 8 + glat.size() * 16 +
@@ -962,12 +982,23 @@ int grid_build(msv_ctx* ctx, const msv_scenario* sc, int64_t n, const double* ta
         // Host traces stay resident: replay grids are a single wave.
         if (g->waves.size() > 1) return fail(MSV_PARAM, "replay: traces exceed device memory budget");
         g->host_n.resize(n);
-        for (int64_t i = 0; i < n; ++i) g->host_n[i] = g->cap[i];
-        const int64_t q0 = offsets[0];
-        const int64_t total = n ? offsets[n] - q0 : 0;
-        if (total) {
-            MSV_CUDA_TRY(cudaMemcpy(g->B->d_arr.p, arrival + q0, total * 8, cudaMemcpyHostToDevice));
-            MSV_CUDA_TRY(cudaMemcpy(g->B->d_bat.p, batch + q0, total * 4, cudaMemcpyHostToDevice));
+        g->user_off.resize(n);
+        const int64_t q0 = n ? offsets[0] : 0;
+        int64_t slots = 0;
+        for (int64_t i = 0; i < n; ++i) {
+            g->host_n[i] = offsets[i + 1] - offsets[i];
+            g->user_off[i] = offsets[i] - q0;
+            slots = std::max(slots, g->toff[i] + g->cap[i]);
+        }
+        if (slots) {  // each trace at its (32-aligned) slot offset
+            std::vector<double> pa(slots, 0.0);
+            std::vector<int32_t> pb(slots, 1);
+            for (int64_t i = 0; i < n; ++i) {
+                std::copy(arrival + offsets[i], arrival + offsets[i + 1], pa.begin() + g->toff[i]);
+                std::copy(batch + offsets[i], batch + offsets[i + 1], pb.begin() + g->toff[i]);
+            }
+            MSV_CUDA_TRY(cudaMemcpy(g->B->d_arr.p, pa.data(), slots * 8, cudaMemcpyHostToDevice));
+            MSV_CUDA_TRY(cudaMemcpy(g->B->d_bat.p, pb.data(), slots * 4, cudaMemcpyHostToDevice));
         }
         if (n) MSV_CUDA_TRY(cudaMemcpy(g->B->d_nq.p, g->host_n.data(), n * 8, cudaMemcpyHostToDevice));
     }
@@ -1223,8 +1254,16 @@ int grid_results(msv_grid* g, msv_result* res, msv_usage* usage, msv_record* rec
     }
     if (usage && g->usage_total)
         MSV_CUDA_TRY(cudaMemcpy(usage, g->B->d_usage.p, g->usage_total * sizeof(msv_usage), cudaMemcpyDeviceToHost));
-    if (records && g->records && g->waves.size() == 1 && g->max_wave_q)
-        MSV_CUDA_TRY(cudaMemcpy(records, g->B->d_rec.p, g->max_wave_q * sizeof(msv_record), cudaMemcpyDeviceToHost));
+    if (records && g->records && g->waves.size() == 1 && g->max_wave_q) {
+        if (g->generated) {
+            MSV_CUDA_TRY(cudaMemcpy(records, g->B->d_rec.p, g->max_wave_q * sizeof(msv_record), cudaMemcpyDeviceToHost));
+        } else {  // back to the caller's layout
+            std::vector<msv_record> dev(g->max_wave_q);
+            MSV_CUDA_TRY(cudaMemcpy(dev.data(), g->B->d_rec.p, g->max_wave_q * sizeof(msv_record), cudaMemcpyDeviceToHost));
+            for (int64_t i = 0; i < n; ++i)
+                std::copy(dev.begin() + g->toff[i], dev.begin() + g->toff[i] + g->host_n[i], records + g->user_off[i]);
+        }
+    }
     int first_err = MSV_OK;
     int64_t first_i = -1;
     for (int64_t i = 0; i < n; ++i) {
@@ -2051,8 +2090,9 @@ int msv_tail_latency(msv_ctx* ctx, const double* samples, int64_t n, const doubl
     for (int j = 0; j < n_p; ++j)
         if (!(p[j] > 0.0) || !(p[j] < 1.0)) return fail(MSV_PARAM, "tail_latency: percentile must be in (0,1)");
     SetDevice sd(ctx->device);
-    DevBuf d_s, d_out, d_job, d_p, d_res;
+    DevBuf d_s, d_out, d_job, d_p, d_res, d_cand;
     MSV_CUDA_TRY(d_s.ensure(n * 8));
+    MSV_CUDA_TRY(d_cand.ensure((n / 2 + 1) * 8));
     MSV_CUDA_TRY(d_out.ensure(sizeof(DevOut)));
     MSV_CUDA_TRY(d_job.ensure(sizeof(msv::TailJob)));
     MSV_CUDA_TRY(d_p.ensure(n_p * 8));
@@ -2067,6 +2107,8 @@ int msv_tail_latency(msv_ctx* ctx, const double* samples, int64_t n, const doubl
     j.samples = d_s.as<double>();
     j.src = d_out.as<DevOut>();
     j.out = d_res.as<double>();
+    j.cand = d_cand.as<uint64_t>();
+    j.cand_cap = n / 2 + 1;
     MSV_CUDA_TRY(cudaMemcpyAsync(d_s.p, src, n * 8, cudaMemcpyHostToDevice, ctx->stream));
     MSV_CUDA_TRY(cudaMemcpyAsync(d_out.p, &o, sizeof o, cudaMemcpyHostToDevice, ctx->stream));
     MSV_CUDA_TRY(cudaMemcpyAsync(d_job.p, &j, sizeof j, cudaMemcpyHostToDevice, ctx->stream));
@@ -2682,6 +2724,7 @@ int run_grid_noise_dev(msv_ctx* ctx, const msv_scenario* sc, int64_t n, const do
         l.samples = arr;
         l.src = B.d_out.as<DevOut>() + i;
         l.out = B.d_tails.as<double>() + 4 * i;
+        tail_scratch(q.next, cap[i], l);
     }
     cudaStream_t st = ctx->stream;
     if (!parts_h.empty())

@@ -20,7 +20,7 @@ constexpr int kSimWarpsPerBlock = 4;
 constexpr int kTraceWarpsPerBlock = 4;
 constexpr int kTraceGroupMax = 16;    // traces sharing one random stream per K1 warp
 constexpr int kTraceAccStride = 34;   // padded row (double2 reads by 16 lanes: 2 wavefronts)
-constexpr int kTailThreads = 512;
+constexpr int kTailThreads = 256;
 constexpr int kTailSmemCap = 2048;  // values gathered for the final in-smem select
 // Guide table of BatchDistribution::sample: u in [j/G, (j+1)/G) starts its lower_bound at guide[j].
 constexpr int kGuide = 256;
@@ -73,7 +73,14 @@ struct DevOut {
     uint64_t lat_max_bits;
     int32_t status;
     int32_t m0;                 // first measured query: samples live at samples[m0, m0 + n_samples)
+    int32_t planar;             // sample layout: 0 doubles, 1 K2 warp blocks (kPlanar below)
+    int32_t pad;
 };
+
+// Planar sample layout (the one-warp K2 kernel): the latencies of queries 32b .. 32b + 31
+// occupy the 256 bytes of their own arrivals as 32 high words followed by 32 low words,
+// so K3's first passes read only the high halves (4 bytes per sample).
+__host__ __device__ inline int64_t planar_hi_word(int64_t q) { return ((q >> 5) << 6) + (q & 31); }
 
 struct SimParams {
     const DevScen* scen;
@@ -112,8 +119,10 @@ struct TraceJob {
 
 struct TailJob {
     const double* samples;
-    const DevOut* src;  // n_samples / lat_min_bits / lat_max_bits of the scenario
+    const DevOut* src;  // n_samples / lat_min_bits / lat_max_bits / layout of the scenario
     double* out;        // n_p tails
+    uint64_t* cand;     // candidate keys scratch (the scenario's dead overflow links), or null
+    int64_t cand_cap;   // entries of cand
 };
 
 // Single-decision dispatch trials (msv_dispatch_batch).

@@ -99,6 +99,7 @@ __global__ void __launch_bounds__(32, 1) sim_noise_kernel(const NoiseParams* __r
         }
     };
     int64_t viol = 0, meas = 0, mviol = 0, m0 = -1;
+    uint32_t hmin = 0xffffffffu, hmax = 0;  // high words of the measured latencies (K3's key bounds)
     uint64_t hash = 0;
     double last_finish = 0.0;
     int status = 0;
@@ -171,6 +172,9 @@ __global__ void __launch_bounds__(32, 1) sim_noise_kernel(const NoiseParams* __r
                         meas += 1;
                         mviol += met ? 0 : 1;
                         if (p.samples) p.samples[q] = l;  // over its own (dead) arrival
+                        const uint32_t lh = (uint32_t)(msv_dbits(l) >> 32);
+                        hmin = lh < hmin ? lh : hmin;
+                        hmax = lh > hmax ? lh : hmax;
                     }
                     last_finish = last_finish < now ? now : last_finish;
                     hash += msv_query_digest((uint64_t)q, pid[s], c_start[s], now);
@@ -427,6 +431,7 @@ __global__ void __launch_bounds__(32, 1) sim_noise_kernel(const NoiseParams* __r
         const double o = __shfl_xor_sync(kFull, last_finish, off);
         last_finish = last_finish < o ? o : last_finish;
     }
+    seg_range_u32<32>(hmin, hmax, kFull);
     if (lane == 0) {
         p.out->violations = viol;
         p.out->measured = meas;
@@ -436,8 +441,12 @@ __global__ void __launch_bounds__(32, 1) sim_noise_kernel(const NoiseParams* __r
         p.out->status = status;
         p.out->n_samples = meas;
         p.out->m0 = m0 >= 0 ? (int32_t)m0 : 0;
-        p.out->lat_min_bits = ~0ull;  // min > max: K3 derives the key range from the samples
-        p.out->lat_max_bits = 0;
+        uint64_t kmin, kmax;
+        lat_key_bounds(hmin, hmax, kmin, kmax);
+        p.out->lat_min_bits = kmin;
+        p.out->lat_max_bits = kmax;
+        p.out->planar = 0;
+        p.out->pad = 0;
     }
 }
 

@@ -451,6 +451,8 @@ __global__ void __launch_bounds__(kSimWarpsPerBlock * 32, (SegCfg<W, S>::min_blo
                 o.hash = hsum;
                 o.lat_min_bits = msv_dbits(d->lat_floor) | kSignBit;  // latencies lie in [floor, horizon]
                 o.lat_max_bits = msv_dbits(o.horizon_ms) | kSignBit;
+                o.planar = 0;
+                o.pad = 0;
                 o.status = status;
                 o.m0 = m0 >= 0 ? m0 : 0;
                 p.out[sidx] = o;

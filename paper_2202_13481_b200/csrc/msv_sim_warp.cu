@@ -115,7 +115,7 @@ __global__ void __launch_bounds__(kSimWarpsPerBlock * 32, WarpCfg<S>::min_blocks
         const double* __restrict__ g_arr = d.arrival;
         const int32_t* __restrict__ g_bat = d.batch;
         uint32_t* g_next = d.next;
-        double* samples = d.samples;
+        uint32_t* samples = reinterpret_cast<uint32_t*>(d.samples);  // planar layout (msv_internal.h)
         msv_record* rec = d.records;
         const double sla = d.sla, warmup = d.warmup_ms;
         const double sla_act = lane < d.P ? sla : -INFINITY;  // Step A's bound, false on lanes without a partition
@@ -635,9 +635,12 @@ __global__ void __launch_bounds__(kSimWarpsPerBlock * 32, WarpCfg<S>::min_blocks
                     const double lat = fin - cur_t;  // latency = finish - arrival
                     const bool met = lat <= sla;
                     viol += met ? 0u : 1u;
-                    if (cur_t >= warmup) {  // measured (engine.hpp:262): overwrite the dead arrival
+                    if (cur_t >= warmup) {  // measured (engine.hpp:262): overwrite the dead arrivals
                         mviol += met ? 0u : 1u;
-                        samples[i] = lat;
+                        const uint64_t lb = msv_dbits(lat);
+                        uint32_t* const row = samples + 2 * base;  // this window's 256 bytes
+                        row[lane] = (uint32_t)(lb >> 32);
+                        row[32 + lane] = (uint32_t)lb;
                     }
                     hash += msv_query_digest((uint64_t)i, pw & 0xff, st, fin);
                     if (REC) {
@@ -675,12 +678,12 @@ __global__ void __launch_bounds__(kSimWarpsPerBlock * 32, WarpCfg<S>::min_blocks
             o.horizon_ms = (d.duration_ms < lf) ? lf : d.duration_ms;  // engine.hpp:237
             o.max_wait_diff = wd;
             o.hash = hsum;
-            // key range of non-negative latencies: [+0.0, +inf] (K3's first pass
-            // splits on the exponent)
-            // key range of the latencies for K3: [floor, horizon] (a latency is at least the
-            // service time, and at most its finish time <= the horizon)
-            o.lat_min_bits = msv_dbits(d.lat_floor) | kSignBit;
-            o.lat_max_bits = msv_dbits(o.horizon_ms) | kSignBit;
+            // no key bounds (min > max): K3 derives them from the high words (tracking them
+            // here costs the simulation loop more than K3's extra 4-byte pass)
+            o.lat_min_bits = ~0ull;
+            o.lat_max_bits = 0;
+            o.planar = 1;
+            o.pad = 0;
             o.status = status;
             o.m0 = m0 >= 0 ? m0 : 0;
             p.out[sidx] = o;

@@ -319,6 +319,43 @@ def test_tail_latency_exact(eng, ref):
         eng.tail_latency([1.0], 1.0)
 
 
+def test_tail_latency_adversarial(eng, ref):
+    """K3's paths: shared and distinct candidate lists (several percentiles per call), a bin
+    too large for the candidate scratch (full-data fallback), ranges across every exponent
+    and sign, adjacent-ulp values, ties straddling a rank."""
+    rng = np.random.default_rng(11)
+    ps = (0.5, 0.95, 0.99, 0.999)
+    cases = []
+    x = rng.lognormal(2.0, 0.5, 1_000_000)
+    x[: 700_000] = 17.25  # one value holds p50..p99: bigger than the scratch (n / 2)
+    cases.append(x)
+    bits = rng.integers(0, 2**63 - 1, 200_000, dtype=np.int64).view(np.float64)
+    bits = bits[np.isfinite(bits)]
+    bits[::2] *= -1.0
+    cases.append(bits)  # every exponent, both signs
+    base = 3.0
+    cases.append(np.nextafter(base, 10.0 * np.ones(50_000)) * (rng.random(50_000) < 0.5) + base * 0.0 + base)
+    y = np.full(100_000, 5.0)
+    y[rng.integers(0, 100_000, 100)] = np.nextafter(5.0, 6.0)
+    cases.append(y)  # two adjacent values
+    z = np.concatenate([np.zeros(1000), -np.zeros(1000), rng.random(1000)])
+    cases.append(z)
+    w = np.repeat(rng.lognormal(1.0, 1.0, 3000), 300)  # ties everywhere
+    rng.shuffle(w)
+    cases.append(w)
+    for c in cases:
+        got = eng.tail_latency(c, ps)
+        want = [ref.tail_latency(c, p) for p in ps]
+        assert list(got) == want
+        assert list(eng.tail_latency(c, (0.99, 0.99))) == [want[2], want[2]]  # one shared list
+    # one far outlier: every requested rank lands in the lowest bins, which the candidate
+    # passes of the first percentile reuse as their digit histogram
+    v = np.concatenate([rng.lognormal(1.0, 0.3, 200_000), [1e12]])
+    rng.shuffle(v)
+    qs = (0.3, 0.5, 0.7, 0.9)
+    assert list(eng.tail_latency(v, qs)) == [ref.tail_latency(v, p) for p in qs]
+
+
 # ---------------------------------------------------------------- single dispatch decisions
 def test_dispatch_random_states(eng):
     """The reference's own randomized trial (test_sched.cpp:236-279), decisions from the
