@@ -2092,7 +2092,9 @@ int msv_tail_latency(msv_ctx* ctx, const double* samples, int64_t n, const doubl
     SetDevice sd(ctx->device);
     DevBuf d_s, d_out, d_job, d_p, d_res, d_cand;
     MSV_CUDA_TRY(d_s.ensure(n * 8));
-    MSV_CUDA_TRY(d_cand.ensure((n / 2 + 1) * 8));
+    // candidate scratch for K3's gather pass (a larger bin takes the full-data passes)
+    const int64_t cand_cap = std::min<int64_t>(n / 2 + 1, (int64_t)1 << 24);
+    MSV_CUDA_TRY(d_cand.ensure(cand_cap * 8));
     MSV_CUDA_TRY(d_out.ensure(sizeof(DevOut)));
     MSV_CUDA_TRY(d_job.ensure(sizeof(msv::TailJob)));
     MSV_CUDA_TRY(d_p.ensure(n_p * 8));
@@ -2108,7 +2110,7 @@ int msv_tail_latency(msv_ctx* ctx, const double* samples, int64_t n, const doubl
     j.src = d_out.as<DevOut>();
     j.out = d_res.as<double>();
     j.cand = d_cand.as<uint64_t>();
-    j.cand_cap = n / 2 + 1;
+    j.cand_cap = cand_cap;
     MSV_CUDA_TRY(cudaMemcpyAsync(d_s.p, src, n * 8, cudaMemcpyHostToDevice, ctx->stream));
     MSV_CUDA_TRY(cudaMemcpyAsync(d_out.p, &o, sizeof o, cudaMemcpyHostToDevice, ctx->stream));
     MSV_CUDA_TRY(cudaMemcpyAsync(d_job.p, &j, sizeof j, cudaMemcpyHostToDevice, ctx->stream));

@@ -1,2 +1,4 @@
-mkdir -p gpurun_out/r02/var
-for i in 1 2 3 4; do MSV_HOST_TIMING=1 timeout 900 python bench.py --no-cpu-baseline > gpurun_out/r02/var/bench_$i.log 2>&1; grep "wave(s)" gpurun_out/r02/var/bench_$i.log | sort | uniq -c | head -5; tail -1 gpurun_out/r02/var/bench_$i.log | cut -c1-200; done
+mkdir -p gpurun_out/r02/prof
+bash tools/profile_r02.sh > gpurun_out/r02/prof_run.log 2>&1
+tail -5 gpurun_out/r02/prof_run.log
+grep -h "^queries" gpurun_out/r02/prof/ncu_k2_*.log

@@ -1,4 +1,5 @@
-"""Launch one C2-shape (or C5 class) grid once, for an ncu capture of K2:
+"""Launch one C2-shape (or C5 class) grid once, for an ncu capture of K2 (run with
+MSV_MAX_CHUNKS=1: one K2 launch simulating every query of the grid):
     python tools/prof_k2.py [c2|MODEL PLAN] [n_scenarios]"""
 import sys
 sys.path.insert(0, "/root/repo")

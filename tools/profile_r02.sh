@@ -15,8 +15,9 @@ KR='regex:sim_warp_kernel|sim_kernel|trace_gen_kernel|trace_group_kernel|tail_ke
 MSV_CLASS_STREAMS=0 ncu --set full --clock-control none --import-source on -k "$KR" --launch-skip $((3 * N)) --launch-count $N \
     -o $P/step python bench.py --no-cpu-baseline --steps 1 --warmup 3 --scenarios 300 > $P/ncu_step.log 2>&1
 # one K2 launch of the C2-shape grid (one slot per lane) and of a P = 56 grid (two slots), source-level
-ncu --set full --clock-control none --import-source on -k regex:sim_warp_kernel --launch-count 1 \
+# (MSV_MAX_CHUNKS=1: one K2 launch simulates every query the script prints)
+MSV_MAX_CHUNKS=1 ncu --set full --clock-control none --import-source on -k regex:sim_warp_kernel --launch-count 1 \
     -o $P/k2_c2 python tools/prof_k2.py c2 > $P/ncu_k2_c2.log 2>&1
-ncu --set full --clock-control none --import-source on -k regex:sim_warp_kernel --launch-count 1 \
+MSV_MAX_CHUNKS=1 ncu --set full --clock-control none --import-source on -k regex:sim_warp_kernel --launch-count 1 \
     -o $P/k2_p56 python tools/prof_k2.py mobilenet k1 4096 > $P/ncu_k2_p56.log 2>&1
 tail -n 2 $P/ncu_step.log $P/ncu_k2_c2.log $P/ncu_k2_p56.log

@@ -66,6 +66,9 @@ def main():
     ap.add_argument("--note", default=None, help="what the capture is (command, grid)")
     ap.add_argument("--queries-per-step", type=float, default=None,
                     help="simulated queries of the captured step (default: from the bench line)")
+    ap.add_argument("--k2-class", action="append", default=[], metavar="LABEL@REPORT:QUERIES:WHAT",
+                    help="standalone capture of one K2 launch (tools/prof_k2.py, MSV_MAX_CHUNKS=1) and "
+                         "the queries it simulated")
     a = ap.parse_args()
     out = ROOT / "profiles" / a.round
     out.mkdir(parents=True, exist_ok=True)
@@ -85,7 +88,19 @@ def main():
         qps = cfg.get("scenarios", cfg.get("scenarios_per_gpu")) * cfg["queries_per_scenario"]
     ADD = ("duration_ms", "warp_instructions", "dram_read", "dram_write")
     kernels, raw = {}, collections.defaultdict(list)
-    rows = ncu_csv(a.reps[0], "--page", "raw")
+    rows, seen = [], set()
+    # the first report holds the step; a later report (e.g. one kernel captured alone, when
+    # kernel replay returned no counters for it inside the step) replaces that kernel's rows
+    for rep in reversed(a.reps):
+        rr = ncu_csv(rep, "--page", "raw")
+        h = rr[0]
+        names = {short(r[h.index("Kernel Name")]) for r in rr[2:]}
+        if not rows:
+            rows = rr[:2]
+        h0 = rows[0]
+        rows += [[r[h.index(c)] if c in h else "" for c in h0]
+                 for r in rr[2:] if short(r[h.index("Kernel Name")]) not in seen]
+        seen |= names
     head, units = rows[0], rows[1]
     for r in rows[2:]:
         name = short(r[head.index("Kernel Name")])
@@ -172,6 +187,27 @@ def main():
         "kernels": kernels,
         "launch_shares_bench": shares,
     }
+    if a.k2_class:
+        classes = {}
+        for spec in a.k2_class:
+            label, rest = spec.split("@", 1)
+            rep, queries, what = rest.split(":", 2)
+            rows = ncu_csv(Path(rep), "--page", "raw")
+            head, units = rows[0], rows[1]
+            r = rows[2]
+            val = lambda m: float(r[head.index(m)].replace(",", ""))
+            q = float(queries)
+            dram = (val(METRICS["dram_read"]) * UNIT.get(units[head.index(METRICS["dram_read"])], 1) +
+                    val(METRICS["dram_write"]) * UNIT.get(units[head.index(METRICS["dram_write"])], 1))
+            classes[label] = {"capture": what, "queries": q,
+                              "warp_instructions_per_query": val(METRICS["warp_instructions"]) / q,
+                              "threads_per_instruction": val(METRICS["threads_per_instruction"]),
+                              "dram_bytes_per_query": dram / q,
+                              "duration_ms": val(METRICS["duration_ms"]),
+                              "issue_active_pct": val(METRICS["issue_active_pct"]),
+                              "warps_active_per_sm": val(METRICS["warps_active_per_sm"]),
+                              "registers": val(METRICS["registers"])}
+        summary["k2_classes_standalone"] = classes
     (out / "summary.json").write_text(json.dumps(summary, indent=1) + "\n")
     print(json.dumps(summary, indent=1))
 
