@@ -23,6 +23,7 @@ from __future__ import annotations
 import argparse
 import hashlib
 import json
+import math
 import os
 import subprocess
 import sys
@@ -208,7 +209,18 @@ def run_reference(args):
             "data": "synthetic", "config": config(args, args.gpus, specs),
             "cpu_baseline": {**base, "value": val},
             "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-    print(json.dumps(line), flush=True)
+    print(json.dumps(finite(line), allow_nan=False), flush=True)
+
+
+def finite(x):
+    """The JSON line carries null, never NaN / inf (strict parsers reject them)."""
+    if isinstance(x, float) and not math.isfinite(x):
+        return None
+    if isinstance(x, dict):
+        return {k: finite(v) for k, v in x.items()}
+    if isinstance(x, (list, tuple)):
+        return [finite(v) for v in x]
+    return x
 
 
 def profile_summary(kernel_sources):
@@ -353,10 +365,18 @@ def main():
             sms = torch.cuda.get_device_properties(dev).multi_processor_count
             pk = sms * 4 * clk_mhz * 1e6  # one warp-instruction per scheduler per clock
             wk2 = k2["warp_instructions_per_query"]
-            wi = wk2 + sum(v.get("warp_instructions_per_query") or 0.0 for kname, v in prof["kernels"].items()
-                           if kname.startswith(("K1", "K3")))
+
+            def per_q(name):
+                v = (prof["kernels"].get(name) or {}).get("warp_instructions_per_query")
+                return v if isinstance(v, (int, float)) and math.isfinite(v) else None
+            # the whole step's mix (every K2 class, K1, K3) when the step capture has K2's counters
+            step_k2 = per_q("K2 sim_warp_kernel")
+            wi = (step_k2 if step_k2 is not None else wk2) + sum(
+                per_q(kname) or 0.0 for kname in prof["kernels"] if kname.startswith(("K1", "K3")))
             issue = {"warp_inst_per_query_k2": wk2, "k2_basis": "one-slot K2 class (P <= 32), ncu source page",
                      "step_warp_inst_per_query": wi,
+                     "step_basis": ("K1 + K2 (all classes) + K3 of the step capture" if step_k2 is not None
+                                    else "one-slot K2 class + K1 + K3"),
                      "step_frac": wi * total_q * args.steps / (dev_ms_max / 1000.0) / world / pk,
                      "peak_warp_inst_per_s": pk, "source": prof_src, "fresh": fresh}
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -393,7 +413,7 @@ def main():
                 "counts_equal": bool(all(np.array_equal(res[k][idx], ref[k]) for k in
                                          ("total", "violations", "measured", "measured_violations"))),
                 "against": b["kind"]}
-        print(json.dumps(line), flush=True)
+        print(json.dumps(finite(line), allow_nan=False), flush=True)
     if world > 1:
         td.destroy_process_group()
 

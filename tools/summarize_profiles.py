@@ -88,52 +88,48 @@ def main():
         qps = cfg.get("scenarios", cfg.get("scenarios_per_gpu")) * cfg["queries_per_scenario"]
     ADD = ("duration_ms", "warp_instructions", "dram_read", "dram_write")
     kernels, raw = {}, collections.defaultdict(list)
-    rows, seen = [], set()
     # the first report holds the step; a later report (e.g. one kernel captured alone, when
     # kernel replay returned no counters for it inside the step) replaces that kernel's rows
+    reports, seen = [], set()
     for rep in reversed(a.reps):
         rr = ncu_csv(rep, "--page", "raw")
         h = rr[0]
-        names = {short(r[h.index("Kernel Name")]) for r in rr[2:]}
-        if not rows:
-            rows = rr[:2]
-        h0 = rows[0]
-        rows += [[r[h.index(c)] if c in h else "" for c in h0]
-                 for r in rr[2:] if short(r[h.index("Kernel Name")]) not in seen]
-        seen |= names
-    head, units = rows[0], rows[1]
-    for r in rows[2:]:
-        name = short(r[head.index("Kernel Name")])
-        vals = {}
-        for key, m in METRICS.items():
-            if m not in head:
-                continue
-            i = head.index(m)
-            try:
-                v = float(r[i].replace(",", ""))
-            except ValueError:
-                continue
-            if key.startswith("dram"):
-                v *= UNIT.get(units[i], 1)
-            elif key == "duration_ms":
-                v *= UNIT.get(units[i], 1) if units[i] != "ms" else 1
-            vals[key] = v
-        raw[name].append(r)
-        k = kernels.setdefault(name, {"kernel": r[head.index("Kernel Name")], "launches": 0,
-                                      **{x: 0.0 for x in ADD}, "_w": {}})
-        k["launches"] += 1
-        for x in ADD:
-            k[x] += vals.get(x, 0.0)
-        # duration-weighted means of the rates, instruction-weighted lane occupancy
-        for x, wkey in (("issue_active_pct", "duration_ms"), ("warps_active_per_sm", "duration_ms"),
-                        ("threads_per_instruction", "warp_instructions")):
-            if x in vals:
-                acc = k["_w"].setdefault(x, [0.0, 0.0])
-                acc[0] += vals[x] * vals.get(wkey, 0.0)
-                acc[1] += vals.get(wkey, 0.0)
-        for x in ("registers", "grid"):
-            if x in vals:
-                k.setdefault(x + "_per_launch", []).append(vals[x])
+        keep = [r for r in rr[2:] if short(r[h.index("Kernel Name")]) not in seen]
+        seen |= {short(r[h.index("Kernel Name")]) for r in rr[2:]}
+        reports.append((h, rr[1], keep))
+    for head, units, body in reports:
+        for r in body:
+            name = short(r[head.index("Kernel Name")])
+            vals = {}
+            for key, m in METRICS.items():
+                if m not in head:
+                    continue
+                i = head.index(m)
+                try:
+                    v = float(r[i].replace(",", ""))
+                except ValueError:
+                    continue
+                if key.startswith("dram"):
+                    v *= UNIT.get(units[i], 1)
+                elif key == "duration_ms":
+                    v *= UNIT.get(units[i], 1) if units[i] != "ms" else 1
+                vals[key] = v
+            raw[name].append((head, units, r))
+            k = kernels.setdefault(name, {"kernel": r[head.index("Kernel Name")], "launches": 0,
+                                          **{x: 0.0 for x in ADD}, "_w": {}})
+            k["launches"] += 1
+            for x in ADD:
+                k[x] += vals.get(x, 0.0)
+            # duration-weighted means of the rates, instruction-weighted lane occupancy
+            for x, wkey in (("issue_active_pct", "duration_ms"), ("warps_active_per_sm", "duration_ms"),
+                            ("threads_per_instruction", "warp_instructions")):
+                if x in vals:
+                    acc = k["_w"].setdefault(x, [0.0, 0.0])
+                    acc[0] += vals[x] * vals.get(wkey, 0.0)
+                    acc[1] += vals.get(wkey, 0.0)
+            for x in ("registers", "grid"):
+                if x in vals:
+                    k.setdefault(x + "_per_launch", []).append(vals[x])
     for name, k in kernels.items():
         for x, (num, den) in k.pop("_w").items():
             k[x] = num / den if den else None
@@ -143,7 +139,8 @@ def main():
             k["warp_instructions_per_query"] = k["warp_instructions"] / qps
             k["traffic_bytes_per_query"] = k["traffic_bytes_per_step"] / (qps * samples)
         with open(out / f"{name.split()[0].lower()}_{name.split()[1]}_raw.csv", "w", newline="") as f:
-            csv.writer(f).writerows([head, units, *raw[name]])
+            h, u = raw[name][0][0], raw[name][0][1]
+            csv.writer(f).writerows([h, u, *[r for _, _, r in raw[name]]])
     if a.opcodes and a.opcodes.exists():
         src = ncu_csv(a.opcodes, "--page", "source", "--print-source", "cuda,sass")
         ops, tot = collections.Counter(), 0
@@ -208,6 +205,15 @@ def main():
                               "warps_active_per_sm": val(METRICS["warps_active_per_sm"]),
                               "registers": val(METRICS["registers"])}
         summary["k2_classes_standalone"] = classes
+    def finite(x):  # counters ncu could not collect are NaN: null in the JSON
+        if isinstance(x, float) and x != x:
+            return None
+        if isinstance(x, dict):
+            return {k: finite(v) for k, v in x.items()}
+        if isinstance(x, list):
+            return [finite(v) for v in x]
+        return x
+    summary = finite(summary)
     (out / "summary.json").write_text(json.dumps(summary, indent=1) + "\n")
     print(json.dumps(summary, indent=1))
 
