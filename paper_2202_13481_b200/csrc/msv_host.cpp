@@ -140,7 +140,7 @@ int set_error(int code, const char* what) { return fail(code, what ? what : "");
 // Device buffers of one grid launch sequence.
 struct GridBufs {
     DevBuf d_scen, d_out, d_tjobs, d_tgroups, d_tailjobs, d_tails, d_p, d_usage, d_nq, d_tovf, d_parts, d_masks,
-        d_work, d_counter;
+        d_work, d_counter, d_sjobs;
     DevBuf d_arr, d_bat, d_next, d_rec, d_glat, d_gutil, d_gcdf, d_gguide;
 };
 
@@ -325,6 +325,10 @@ struct msv_grid {
     std::vector<int64_t> cap, toff;   // per-scenario trace capacity and offset
     std::vector<int32_t> P, usage_off;
     std::vector<uint8_t> bad;  // plan has a size the profile lacks
+    // Streamed K1 -> K2 (msv_sim_warp.cu STREAM): a latency-bound generated grid (one wave,
+    // few scenarios, warp-kernel classes without routing / missing sizes / wait checks)
+    // generates each trace inside its simulating block; records and usage launches do not.
+    bool stream_ok = false;
     int64_t usage_total = 0;
     // A chunk is a set of scenarios launched together (K1 -> K2 per class -> K3) on one
     // stream; chunks of a wave run on different streams so one chunk's K1/K3 fill the
@@ -960,6 +964,21 @@ int grid_build(msv_ctx* ctx, const msv_scenario* sc, int64_t n, const double* ta
         MSV_CUDA_TRY(cudaMemcpy(g->B->d_tailjobs.p, lj_l.data(), n * sizeof(msv::TailJob), cudaMemcpyHostToDevice));
         MSV_CUDA_TRY(cudaMemset(g->B->d_tovf.p, 0, n * 4));
     }
+    // streamed launches: latency-bound (at most two scenarios per SM) single-wave grids
+    // MSV_STREAM=0 never streams, MSV_STREAM=1 streams every eligible grid (tests)
+    static const int stream_env = getenv("MSV_STREAM") ? atoi(getenv("MSV_STREAM")) : -1;
+    g->stream_ok = stream_env != 0 && g->generated && n > 0 && g->waves.size() == 1 &&
+                   (stream_env == 1 || n <= 2 * (int64_t)ctx->sms);
+    for (int64_t i = 0; i < n && g->stream_ok; ++i)
+        if (g->bad[i] || sc[i].routing >= 0 || (sc[i].flags & MSV_FLAG_CHECK_WAIT)) g->stream_ok = false;
+    for (const auto& w : g->waves)
+        for (const auto& ch : w.chunks)
+            for (const auto& c : ch.classes)
+                if (c.first.W != 32) g->stream_ok = false;
+    if (g->stream_ok) {  // trace jobs in scenario order (a block finds its job by scenario index)
+        MSV_CUDA_TRY(g->B->d_sjobs.ensure(n * sizeof(msv::TraceJob)));
+        MSV_CUDA_TRY(cudaMemcpy(g->B->d_sjobs.p, tj.data(), n * sizeof(msv::TraceJob), cudaMemcpyHostToDevice));
+    }
     MSV_CUDA_TRY(g->B->d_tgroups.ensure(std::max<size_t>(g->tgroups.size(), 1) * sizeof(msv::TraceGroup)));
     if (!g->tgroups.empty())
         MSV_CUDA_TRY(cudaMemcpy(g->B->d_tgroups.p, g->tgroups.data(), g->tgroups.size() * sizeof(msv::TraceGroup),
@@ -1022,7 +1041,9 @@ int launch_chunk(msv_grid* g, const msv_grid::Chunk& ch, int counter_base, cudaS
                  cudaEvent_t e2) {
     msv_ctx* ctx = g->ctx;
     const int64_t nl = ch.l1 - ch.l0;
-    if (g->generated && nl > 0) {
+    const bool stream = g->stream_ok && !g->records && !g->usage;  // K1 inside K2's blocks
+    static const bool stream_pregen = getenv("MSV_STREAM_PREGEN") != nullptr;  // A/B: K1 first anyway
+    if (g->generated && nl > 0 && (!stream || stream_pregen)) {
         if (ch.g1 - ch.g0 == nl)  // no shared streams in this chunk: one warp per trace
             MSV_CUDA_TRY(msv::launch_trace_gen(g->B->d_tjobs.as<msv::TraceJob>() + ch.l0, (int)nl, ctx->log1p, st));
         else
@@ -1106,6 +1127,9 @@ int launch_chunk(msv_grid* g, const msv_grid::Chunk& ch, int counter_base, cudaS
         }
         const bool full = g->records || p.any_routing || p.any_bad || p.any_check_wait || p.any_usage;
         p.lazy = k.lazy;
+        p.stream = stream ? (stream_pregen ? 2 : 1) : 0;
+        p.log1p_variant = ctx->log1p;
+        p.stream_jobs = stream ? g->B->d_sjobs.as<msv::TraceJob>() : nullptr;
         const int occ = msv::sim_max_blocks_per_sm(k.W, k.S, k.sched, g->records, full, k.lazy != 0, g->n_cells);
         if (occ <= 0) return fail(MSV_CUDA, "sim kernel: no occupancy for class");
         const int segs_per_block = msv::kSimWarpsPerBlock * (32 / k.W);

@@ -99,6 +99,11 @@ struct SimParams {
     int32_t any_check_wait;  // some scenario sets MSV_FLAG_CHECK_WAIT
     int32_t any_usage;       // per-partition usage (PartitionUsage) requested
     int32_t lazy;            // warp kernel: lazy folds for long queues (overloaded scenarios)
+    // Streamed launch (latency-bound generated grids): one 2-warp block per scenario, warp 0
+    // generates the trace (stream_jobs[scenario index], K1's job) while warp 1 simulates it.
+    int32_t stream;
+    int32_t log1p_variant;
+    const struct TraceJob* stream_jobs;
 };
 
 // Trace generation job (sample_trace, workload.hpp:97-113).

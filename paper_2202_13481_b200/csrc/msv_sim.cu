@@ -494,7 +494,7 @@ void* pick_sim(int W, int S, int sched, bool rec, bool full) {
 
 }  // namespace
 
-void* sim_warp_fn(int S, int sched, bool rec, bool full, bool lazy);  // msv_sim_warp.cu
+void* sim_warp_fn(int S, int sched, bool rec, bool full, bool lazy, bool stream);  // msv_sim_warp.cu
 size_t sim_warp_smem_bytes(int S, int n_cells);
 
 size_t sim_smem_bytes(int W, int S, int n_cells) {
@@ -508,7 +508,7 @@ size_t sim_smem_bytes(int W, int S, int n_cells) {
 }
 
 static void* sim_fn_for(int W, int S, int sched, bool rec, bool full, bool lazy) {
-    return W == 32 ? sim_warp_fn(S, sched, rec, full, lazy) : pick_sim(W, S, sched, rec, full);
+    return W == 32 ? sim_warp_fn(S, sched, rec, full, lazy, false) : pick_sim(W, S, sched, rec, full);
 }
 
 // Dynamic shared-memory opt-in, raised monotonically per (kernel, device) under a lock:
@@ -540,6 +540,16 @@ int sim_max_blocks_per_sm(int W, int S, int sched, bool records, bool full, bool
 
 cudaError_t launch_sim(int W, int S, int sched, bool records, const SimParams& p, int blocks, cudaStream_t stream) {
     const bool full = records || p.any_routing || p.any_bad || p.any_check_wait || p.any_usage;
+    if (p.stream) {  // one 2-warp block per scenario: trace generator + simulator
+        if (W != 32 || full) return cudaErrorInvalidValue;
+        void* fn = sim_warp_fn(S, sched, false, false, p.lazy != 0, true);
+        if (!fn) return cudaErrorInvalidValue;
+        const size_t smem = sim_smem_bytes(W, S, p.n_cells);  // (sized for 4 warps; 2 used)
+        cudaError_t e = ensure_dyn_smem(fn, smem);
+        if (e != cudaSuccess) return e;
+        void* args[] = {const_cast<SimParams*>(&p)};
+        return cudaLaunchKernel(fn, dim3(p.n_work), dim3(64), args, smem, stream);
+    }
     void* fn = sim_fn_for(W, S, sched, records, full, p.lazy != 0);
     if (!fn) return cudaErrorInvalidValue;
     const size_t smem = sim_smem_bytes(W, S, p.n_cells);

@@ -860,3 +860,45 @@ print("ok", len(specs))
     env = dict(__import__("os").environ, MSV_TEST_WAVE_MB="60")
     r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=900, env=env)
     assert r.returncode == 0 and "ok" in r.stdout, r.stdout[-2000:] + r.stderr[-3000:]
+
+
+_STREAM_CODE = r'''
+import sys; sys.path.insert(0, %r)
+import numpy as np
+from paper_2202_13481_b200 import Engine, homogeneous_plan
+from paper_2202_13481_b200 import workloads as W
+from tests import oracle_py as O
+m = W.model("mobilenet")
+big = homogeneous_plan(1, 112, 16, 7)  # P = 112: four slots per lane
+specs = (W.c1(queries=2e4) + W.c3(seeds=2, queries=3e4) + W.c5(n_scenarios=75, queries=1.5e4)
+         + [W._spec(m, big, f * W.capacity_qps(m, big), 2e4, 7 + i) for i, f in enumerate((0.5, 0.9, 1.4))])
+specs += [W._spec(m, W.paris(m, 8), 1.2 * W.capacity_qps(m, W.paris(m, 8)), 2e4, 3, "fifs")]
+eng = Engine(0)
+want = O.best_oracle().run_grid(specs, (0.5, 0.95, 0.99))
+for _ in range(2):  # one-shot call, then a device-resident grid
+    got = eng.run_grid(specs, (0.5, 0.95, 0.99))
+    for k in ("total", "violations", "measured", "measured_violations", "placement_hash", "horizon_ms", "status"):
+        assert np.array_equal(got[k], want[k]), k
+    assert np.array_equal(got["tail"], want["tail"], equal_nan=True)
+g = eng.grid(specs, (0.5, 0.95, 0.99))
+g.launch(); g.launch()
+r = g.results()
+ok = r["status"] == 0  # a device-resident grid reports overflowed traces instead of re-running them
+assert ok.all() or __import__("os").environ.get("MSV_TEST_SHORT_CAP") == "1"
+assert np.array_equal(r["placement_hash"][ok], want["placement_hash"][ok])
+assert np.array_equal(r["tail"][ok], want["tail"][ok], equal_nan=True)
+print("ok", len(specs), int(ok.sum()), eng.kernel_launches())
+'''
+
+
+@pytest.mark.parametrize("env", [{"MSV_STREAM": "1"}, {"MSV_STREAM": "1", "MSV_TEST_SHORT_CAP": "1"},
+                                 {"MSV_STREAM": "0"}], ids=["streamed", "streamed-overflow", "unstreamed"])
+def test_streamed_grids_subprocess(env):
+    """Latency-bound grids generate each trace inside the simulating block (warp 0 writes
+    the trace, warp 1 simulates behind its published count): ELSA / FIFS, one, two and four
+    slots per lane, overloaded (lazy-fold) scenarios, traces that overflow a (test-shortened)
+    capacity and are re-run — equal to the compiled reference, streamed or not (MSV_STREAM,
+    read once per process)."""
+    r = subprocess.run([sys.executable, "-c", _STREAM_CODE % str(ROOT)], capture_output=True, text=True,
+                       timeout=900, env=dict(__import__("os").environ, **env))
+    assert r.returncode == 0 and "ok" in r.stdout, r.stdout[-2000:] + r.stderr[-3000:]

@@ -1,6 +1,4 @@
-P=gpurun_out/r02/final2
+P=gpurun_out/r02/stream
 mkdir -p $P
-timeout 1500 python -m pytest tests -m gpu -x -q > $P/gpu_tests.log 2>&1; tail -2 $P/gpu_tests.log
-timeout 300 python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')" > $P/smoke.log 2>&1; tail -2 $P/smoke.log
-timeout 900 python bench.py > $P/bench.log 2>&1; tail -1 $P/bench.log | cut -c1-200
-timeout 900 python bench.py --impl reference > $P/bench_ref.log 2>&1; tail -1 $P/bench_ref.log | cut -c1-200
+timeout 1800 python -m pytest tests -m gpu -x -q > $P/gpu_tests.log 2>&1; tail -2 $P/gpu_tests.log
+timeout 1800 python tools/run_configs.py $P/configs.json > $P/configs.log 2>&1; tail -6 $P/configs.log | cut -c1-330
