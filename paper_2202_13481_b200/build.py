@@ -69,17 +69,27 @@ def build_libmsv(force: bool = False, verbose: bool = False) -> Path:
     headers = sorted(CSRC.glob("*.h")) + sorted(CSRC.glob("*.cuh")) + sorted((ROOT / "include").rglob("*.h*"))
     objs: list[Path] = []
     log: list[str] = []
+    steps = []  # independent compiles, run concurrently (the kernel files dominate the build)
     for src in sorted(CSRC.glob("*.cu")):
         obj = BUILD / (src.stem + ".o")
         if force or _stale(obj, [src, *headers]):
-            _run([NVCC, *NVCC_FLAGS, "-c", str(src), "-o", str(obj)], log)
+            steps.append([NVCC, *NVCC_FLAGS, "-c", str(src), "-o", str(obj)])
         objs.append(obj)
     for src in sorted(CSRC.glob("*.cpp")):
         obj = BUILD / (src.stem + ".o")
         if force or _stale(obj, [src, *headers]):
-            _run(["g++", *CXX_FLAGS, f"-I{CUDA_INC}", f"-I{ROOT / 'include'}", f"-I{json_include_dir()}",
-                  "-c", str(src), "-o", str(obj)], log)
+            steps.append(["g++", *CXX_FLAGS, f"-I{CUDA_INC}", f"-I{ROOT / 'include'}", f"-I{json_include_dir()}",
+                          "-c", str(src), "-o", str(obj)])
         objs.append(obj)
+    if steps:
+        from concurrent.futures import ThreadPoolExecutor
+        logs: list[list[str]] = [[] for _ in steps]
+        with ThreadPoolExecutor(max_workers=min(len(steps), os.cpu_count() or 1)) as ex:
+            futs = [ex.submit(_run, cmd, lg) for cmd, lg in zip(steps, logs)]
+            for f in futs:
+                f.result()  # re-raises a failed step
+        for lg in logs:
+            log.extend(lg)
     if force or _stale(LIB, objs):
         tmp = LIB.with_suffix(".so.tmp")
         _run([NVCC, *ARCH, "-shared", "-o", str(tmp), *map(str, objs), "-cudart", "static",
