@@ -582,8 +582,10 @@ int grid_build(msv_ctx* ctx, const msv_scenario* sc, int64_t n, const double* ta
     // trace buffers this grid will reuse (a one-shot call's scratch set is already held by
     // the context and is not free memory).
     const size_t held = g->B->d_arr.bytes + g->B->d_bat.bytes + g->B->d_next.bytes + g->B->d_rec.bytes;
-    size_t budget = (free_device_bytes() + held) / 10 * 7 / (size_t)std::max(1, ctx->share);
-    if (budget > ((size_t)140 << 30)) budget = (size_t)140 << 30;
+    static const int frac_pct = getenv("MSV_WAVE_PCT") ? atoi(getenv("MSV_WAVE_PCT")) : 70;  // (A/B)
+    static const size_t cap_bytes = (size_t)(getenv("MSV_WAVE_CAP_GIB") ? atoll(getenv("MSV_WAVE_CAP_GIB")) : 140) << 30;
+    size_t budget = (free_device_bytes() + held) / 100 * (size_t)frac_pct / (size_t)std::max(1, ctx->share);
+    if (budget > cap_bytes) budget = cap_bytes;
     // MSV_TEST_WAVE_MB (tests only): a small budget forces the multi-wave path on small grids
     static const long long test_wave_mb = getenv("MSV_TEST_WAVE_MB") ? atoll(getenv("MSV_TEST_WAVE_MB")) : 0;
     if (test_wave_mb > 0) budget = (size_t)test_wave_mb << 20;
