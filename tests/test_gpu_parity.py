@@ -902,3 +902,36 @@ def test_streamed_grids_subprocess(env):
     r = subprocess.run([sys.executable, "-c", _STREAM_CODE % str(ROOT)], capture_output=True, text=True,
                        timeout=900, env=dict(__import__("os").environ, **env))
     assert r.returncode == 0 and "ok" in r.stdout, r.stdout[-2000:] + r.stderr[-3000:]
+
+
+_CONST_CODE = r'''
+import sys; sys.path.insert(0, %r)
+import numpy as np
+from paper_2202_13481_b200 import Engine, GridSpec, BatchDistribution, homogeneous_plan
+from paper_2202_13481_b200 import workloads as W
+from tests import oracle_py as O
+m = W.model("resnet50")
+one_hot = BatchDistribution(np.eye(1, m.table.b_max, 3).ravel() + 0.0)  # batch 4 only
+specs = [GridSpec(p, m.table, one_hot, m.sla, 0.02 * W.capacity_qps(m, p), 2e5 / (0.02 * W.capacity_qps(m, p)) * 1e3,
+                 seed, "fifs") for p in (homogeneous_plan(7, 56, 8, 7), homogeneous_plan(1, 7, 1, 7)) for seed in range(1, 4)]
+got = Engine(0).run_grid(specs, (0.5, 0.95, 0.99))
+want = O.best_oracle().run_grid(specs, (0.5, 0.95, 0.99))
+for k in ("total", "violations", "measured", "placement_hash", "horizon_ms"):
+    assert np.array_equal(got[k], want[k]), k
+assert np.array_equal(got["tail"], want["tail"], equal_nan=True)
+assert (want["tail"][:, 0] == want["tail"][:, 2]).sum() >= 3  # p50 .. p99 one latency value
+print("ok")
+'''
+
+
+@pytest.mark.parametrize("env", [{}, {"MSV_STREAM": "0"}, {"MSV_STREAM": "0", "MSV_SEG_WIDTH": "8"}],
+                         ids=["streamed-planar", "planar", "segmented-plain"])
+def test_tails_of_constant_latencies(env):
+    """Every query meets an idle partition of one size, so all latencies are one value: the
+    rank's histogram bin holds every sample — more than K3's candidate scratch (half the
+    trace slots) — and the full-data digit passes settle it (min == max after one pass).
+    Planar samples (one-warp K2, streamed or not) and plain ones (segmented K2, 4 scenarios
+    per warp: MSV_SEG_WIDTH=8)."""
+    r = subprocess.run([sys.executable, "-c", _CONST_CODE % str(ROOT)], capture_output=True, text=True,
+                       timeout=900, env=dict(__import__("os").environ, **env))
+    assert r.returncode == 0 and "ok" in r.stdout, r.stdout[-2000:] + r.stderr[-3000:]
