@@ -17,6 +17,7 @@
 #include <numeric>
 #include <string>
 #include <utility>
+#include <sched.h>
 #include <thread>
 #include <vector>
 
@@ -160,7 +161,11 @@ struct msv_ctx {
     GridBufs scratch;  // reused by one-shot grids (msv_run_grid / msv_run_replay)
     // reused by noisy grids (msv_run_grid_noise): multipliers and K5 jobs
     DevBuf d_mult, d_njobs;
-    std::vector<double> h_mult;
+    // pinned staging of the multiplier streams: two buffers, alternating by chunk
+    double* pin[2] = {nullptr, nullptr};
+    size_t pin_n = 0;  // doubles per buffer
+    cudaEvent_t pin_ev[2] = {};  // the copy out of the buffer is done
+    cudaEvent_t k1_ev = nullptr;
     int sms = 148;
     cudaStream_t stream = nullptr;
     int log1p = MSV_LOG1P_FMA;
@@ -492,6 +497,13 @@ struct PhaseTimer {
         if (on && !line.empty()) fprintf(stderr, "[msv] grid_build ms:%s\n", line.c_str());
     }
 };
+
+// Host cores this process may run on (the affinity mask, not the machine's core count).
+int host_threads() {
+    cpu_set_t set;
+    if (sched_getaffinity(0, sizeof set, &set) == 0) return std::max(1, CPU_COUNT(&set));
+    return std::max(1, (int)std::thread::hardware_concurrency());
+}
 
 // cudaMemGetInfo costs up to ~10 ms on a busy driver; the wave budget only needs a
 // coarse figure, so it is refreshed at most once per second per thread — and whenever
@@ -1417,6 +1429,11 @@ int msv_destroy(msv_ctx* ctx) {
         if (ctx->cls_ev[a]) cudaEventDestroy(ctx->cls_ev[a]);
     }
     if (ctx->cls_fork) cudaEventDestroy(ctx->cls_fork);
+    for (int b = 0; b < 2; ++b) {
+        if (ctx->pin[b]) cudaFreeHost(ctx->pin[b]);
+        if (ctx->pin_ev[b]) cudaEventDestroy(ctx->pin_ev[b]);
+    }
+    if (ctx->k1_ev) cudaEventDestroy(ctx->k1_ev);
     cudaStreamDestroy(ctx->stream);
     delete ctx;
     return MSV_OK;
@@ -2632,6 +2649,7 @@ int run_grid_noise_dev(msv_ctx* ctx, const msv_scenario* sc, int64_t n, const do
         if (!(tail_p[j] > 0.0) || !(tail_p[j] < 1.0))
             return fail(MSV_PARAM, "tail_latency: percentile must be in (0,1)");
     SetDevice sd(ctx->device);
+    PhaseTimer pt;
     int rc = ctx->sync_tables();
     if (rc) return rc;
     std::vector<int32_t> P(n);
@@ -2688,19 +2706,6 @@ int run_grid_noise_dev(msv_ctx* ctx, const msv_scenario* sc, int64_t n, const do
     }
     MSV_CUDA_TRY(B.d_parts.ensure(std::max<size_t>(parts_h.size(), 1) * sizeof(DevPart)));
     MSV_CUDA_TRY(B.d_masks.ensure(std::max<size_t>(masks_h.size(), 1) * 8));
-    // multiplier streams on the host, one thread per core (scenario-parallel)
-    ctx->h_mult.resize(tq);
-    {
-        const int nt = std::max(1, std::min<int>((int)std::thread::hardware_concurrency(), (int)std::max<int64_t>(n, 1)));
-        std::atomic<int64_t> next_i{0};
-        std::vector<std::thread> th;
-        for (int t = 0; t < nt; ++t)
-            th.emplace_back([&] {
-                for (int64_t i; (i = next_i.fetch_add(1)) < n;)
-                    msv_noise_multipliers(nseed[i], sigma[i], cap[i], ctx->h_mult.data() + toff[i]);
-            });
-        for (std::thread& t : th) t.join();
-    }
     std::vector<msv::TraceJob> tj(n);
     std::vector<msv::NoiseParams> nj(n);
     std::vector<msv::TailJob> lj(n);
@@ -2763,21 +2768,75 @@ int run_grid_noise_dev(msv_ctx* ctx, const msv_scenario* sc, int64_t n, const do
         MSV_CUDA_TRY(cudaMemcpyAsync(B.d_tjobs.p, tj.data(), n * sizeof(msv::TraceJob), cudaMemcpyHostToDevice, st));
         MSV_CUDA_TRY(cudaMemcpyAsync(ctx->d_njobs.p, nj.data(), n * sizeof(msv::NoiseParams), cudaMemcpyHostToDevice, st));
         MSV_CUDA_TRY(cudaMemcpyAsync(B.d_tailjobs.p, lj.data(), n * sizeof(msv::TailJob), cudaMemcpyHostToDevice, st));
-        MSV_CUDA_TRY(cudaMemcpyAsync(ctx->d_mult.p, ctx->h_mult.data(), total * 8, cudaMemcpyHostToDevice, st));
         MSV_CUDA_TRY(cudaMemsetAsync(B.d_tovf.p, 0, n * 4, st));
     }
     if (n_tails) MSV_CUDA_TRY(cudaMemcpyAsync(B.d_p.p, tail_p, n_tails * sizeof(double), cudaMemcpyHostToDevice, st));
     ctx->h2d += total * 8 + (int64_t)(n * (sizeof(msv::TraceJob) + sizeof(msv::NoiseParams) + sizeof(msv::TailJob)) +
                                       parts_h.size() * sizeof(DevPart) + masks_h.size() * 8);
     if (n) {
+        // K1 first (the traces need no multipliers); then, chunk by chunk, the multiplier
+        // streams are drawn on the host (the reference's Rng and libm, rng.hpp:27-32, one
+        // thread per core) into pinned staging, copied, and the chunk's K5 launched on an aux
+        // stream — so the host draws chunk c + 1 while the device copies and simulates chunk c.
+        if (!ctx->k1_ev) MSV_CUDA_TRY(cudaEventCreateWithFlags(&ctx->k1_ev, cudaEventDisableTiming));
         MSV_CUDA_TRY(msv::launch_trace_gen(B.d_tjobs.as<msv::TraceJob>(), (int)n, ctx->log1p, st));
-        MSV_CUDA_TRY(msv::launch_noise(ctx->d_njobs.as<msv::NoiseParams>(), (int)n, max_cells, st));
-        ctx->launches += 2;
+        MSV_CUDA_TRY(cudaEventRecord(ctx->k1_ev, st));
+        ctx->launches += 1;
+        constexpr int64_t kChunkQ = (int64_t)8 << 20;  // multipliers per chunk (64 MB)
+        int64_t max_cap = 0;
+        for (int64_t i = 0; i < n; ++i) max_cap = std::max(max_cap, cap[i]);
+        const size_t need = (size_t)std::max<int64_t>(std::min<int64_t>(kChunkQ, total), max_cap);
+        if (ctx->pin_n < need) {
+            for (int b = 0; b < 2; ++b) {
+                if (ctx->pin_ev[b]) MSV_CUDA_TRY(cudaEventSynchronize(ctx->pin_ev[b]));
+                if (ctx->pin[b]) cudaFreeHost(ctx->pin[b]);
+                ctx->pin[b] = nullptr;
+                MSV_CUDA_TRY(cudaHostAlloc(reinterpret_cast<void**>(&ctx->pin[b]), need * 8, cudaHostAllocDefault));
+            }
+            ctx->pin_n = need;
+        }
+        for (int b = 0; b < 2; ++b)
+            if (!ctx->pin_ev[b]) MSV_CUDA_TRY(cudaEventCreateWithFlags(&ctx->pin_ev[b], cudaEventDisableTiming));
+        for (int a = 0; a < kAuxStreams; ++a) {
+            if (!ctx->aux[a]) MSV_CUDA_TRY(cudaStreamCreateWithFlags(&ctx->aux[a], cudaStreamNonBlocking));
+            if (!ctx->aux_ev[a]) MSV_CUDA_TRY(cudaEventCreateWithFlags(&ctx->aux_ev[a], cudaEventDisableTiming));
+            MSV_CUDA_TRY(cudaStreamWaitEvent(ctx->aux[a], ctx->k1_ev, 0));
+        }
+        const int nt = std::max(1, std::min(host_threads(), 64));
+        int chunk = 0;
+        for (int64_t s0 = 0; s0 < n; ++chunk) {
+            int64_t s1 = s0 + 1;
+            while (s1 < n && toff[s1 + 1] - toff[s0] <= (int64_t)ctx->pin_n) ++s1;
+            const int b = chunk & 1;
+            if (chunk >= 2) MSV_CUDA_TRY(cudaEventSynchronize(ctx->pin_ev[b]));  // its last copy is done
+            double* const stage = ctx->pin[b] - toff[s0];
+            std::atomic<int64_t> next_i{s0};
+            std::vector<std::thread> th;
+            const int nth = (int)std::min<int64_t>(nt, s1 - s0);
+            for (int t = 0; t < nth; ++t)
+                th.emplace_back([&] {
+                    for (int64_t i; (i = next_i.fetch_add(1)) < s1;)
+                        msv_noise_multipliers(nseed[i], sigma[i], cap[i], stage + toff[i]);
+                });
+            for (std::thread& t : th) t.join();
+            cudaStream_t sa = ctx->aux[chunk % kAuxStreams];
+            MSV_CUDA_TRY(cudaMemcpyAsync(ctx->d_mult.as<double>() + toff[s0], ctx->pin[b],
+                                         (size_t)(toff[s1] - toff[s0]) * 8, cudaMemcpyHostToDevice, sa));
+            MSV_CUDA_TRY(cudaEventRecord(ctx->pin_ev[b], sa));
+            MSV_CUDA_TRY(msv::launch_noise(ctx->d_njobs.as<msv::NoiseParams>() + s0, (int)(s1 - s0), max_cells, sa));
+            ctx->launches += 1;
+            s0 = s1;
+        }
+        for (int a = 0; a < kAuxStreams; ++a) {  // join
+            MSV_CUDA_TRY(cudaEventRecord(ctx->aux_ev[a], ctx->aux[a]));
+            MSV_CUDA_TRY(cudaStreamWaitEvent(st, ctx->aux_ev[a], 0));
+        }
         if (n_tails) {
             MSV_CUDA_TRY(msv::launch_tail(B.d_tailjobs.as<msv::TailJob>(), (int)n, B.d_p.as<double>(), n_tails, st));
             ctx->launches += 1;
         }
     }
+    pt.mark("jobs+enqueue");
     std::vector<DevOut> outs(n);
     std::vector<double> tails(4 * n);
     std::vector<int64_t> nq(n);
@@ -2791,6 +2850,7 @@ int run_grid_noise_dev(msv_ctx* ctx, const msv_scenario* sc, int64_t n, const do
             MSV_CUDA_TRY(cudaMemcpyAsync(usage, B.d_usage.p, uoff[n] * sizeof(msv_usage), cudaMemcpyDeviceToHost, st));
     }
     MSV_CUDA_TRY(cudaStreamSynchronize(st));
+    pt.mark("device");
     ctx->d2h += n * (int64_t)(sizeof(DevOut) + 4 * sizeof(double) + 12) + (usage ? uoff[n] * (int64_t)sizeof(msv_usage) : 0);
     std::vector<int64_t> retry;
     for (int64_t i = 0; i < n; ++i) {

@@ -1,4 +1,5 @@
-P=gpurun_out/r02/final3
+P=gpurun_out/r02/noise
 mkdir -p $P
-timeout 900 python -m pytest tests/test_gpu_parity.py -x -q -k "constant_latencies" > $P/t_const.log 2>&1; tail -2 $P/t_const.log
-timeout 1800 python -m pytest tests -m gpu -x -q > $P/gpu_tests.log 2>&1; tail -2 $P/gpu_tests.log
+timeout 900 python -m pytest tests -m gpu -x -q -k "noise" > $P/t.log 2>&1; tail -2 $P/t.log
+MSV_HOST_TIMING=1 timeout 900 python tools/noise_grid_bench.py > $P/nb.log 2>&1; grep -E "msv|device:|reference|parity" $P/nb.log | tail -5
+timeout 900 python tools/noise_grid_bench.py > $P/nb2.log 2>&1; tail -3 $P/nb2.log
