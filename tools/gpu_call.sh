@@ -1,5 +1,8 @@
-P=gpurun_out/r02/noise
-mkdir -p $P
-timeout 900 python -m pytest tests -m gpu -x -q -k "noise" > $P/t.log 2>&1; tail -2 $P/t.log
-MSV_HOST_TIMING=1 timeout 900 python tools/noise_grid_bench.py > $P/nb.log 2>&1; grep -E "msv|device:|reference|parity" $P/nb.log | tail -5
-timeout 900 python tools/noise_grid_bench.py > $P/nb2.log 2>&1; tail -3 $P/nb2.log
+mkdir -p gpurun_out/r02/prof gpurun_out/r02/prof2
+bash tools/profile_r02.sh > gpurun_out/r02/prof_run.log 2>&1
+tail -3 gpurun_out/r02/prof_run.log
+grep -h "^queries" gpurun_out/r02/prof/ncu_k2_*.log
+P2=gpurun_out/r02/prof2
+MSV_CLASS_STREAMS=0 timeout 900 ncu --set full --clock-control none --import-source on -k regex:tail_kernel --launch-skip 3 --launch-count 1 \
+    -o $P2/k3 python bench.py --no-cpu-baseline --steps 1 --warmup 3 --scenarios 300 > $P2/ncu_k3.log 2>&1; tail -1 $P2/ncu_k3.log
+timeout 900 python bench.py > $P2/bench.log 2>&1; tail -1 $P2/bench.log | cut -c1-150
