@@ -1,8 +1,3 @@
-mkdir -p gpurun_out/r02/prof gpurun_out/r02/prof2
-bash tools/profile_r02.sh > gpurun_out/r02/prof_run.log 2>&1
-tail -3 gpurun_out/r02/prof_run.log
-grep -h "^queries" gpurun_out/r02/prof/ncu_k2_*.log
-P2=gpurun_out/r02/prof2
-MSV_CLASS_STREAMS=0 timeout 900 ncu --set full --clock-control none --import-source on -k regex:tail_kernel --launch-skip 3 --launch-count 1 \
-    -o $P2/k3 python bench.py --no-cpu-baseline --steps 1 --warmup 3 --scenarios 300 > $P2/ncu_k3.log 2>&1; tail -1 $P2/ncu_k3.log
-timeout 900 python bench.py > $P2/bench.log 2>&1; tail -1 $P2/bench.log | cut -c1-150
+P=gpurun_out/r02/sort
+mkdir -p $P
+for rep in 1 2; do for m in "" 1 2; do MSV_BENCH_SORT=$m timeout 900 python bench.py --no-cpu-baseline > $P/b.log 2>&1; echo -n "sort=$m: "; tail -1 $P/b.log | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(round(d['value']/1e9,3), round(d['e2e']['value']/1e9,3), round(d['ms_per_step'],2))"; done; done
