@@ -307,6 +307,7 @@ class Engine:
         self._profiles: dict[int, int] = {}
         self._dists: dict[int, int] = {}
         self._plans: dict[tuple, int] = {}
+        self._plan_objs: dict[int, tuple] = {}  # id(plan) -> (plan, handle, contents)
         self._routings: dict[tuple, int] = {}
         self._keep: list = []
 
@@ -356,6 +357,9 @@ class Engine:
         return self._dists[key]
 
     def plan(self, p: PartitionPlan) -> int:
+        hit = self._plan_objs.get(id(p))  # the same, unchanged object again: skip the key
+        if hit is not None and hit[0] is p and hit[2] == p.gpus and hit[3] == (p.num_gpus, p.gpcs_per_gpu):
+            return hit[1]
         key = p.key()
         if key not in self._plans:
             n_per = _arr([len(g) for g in p.gpus] or [0], np.int32)
@@ -364,6 +368,8 @@ class Engine:
             check(self._lib.msv_upload_plan(self._h, p.num_gpus, p.gpcs_per_gpu, _ptr(n_per, C.c_int32),
                                             _ptr(flat, C.c_int32), C.byref(h)), "msv_upload_plan")
             self._plans[key] = h.value
+        # (holds p, so its id stays unique; a snapshot of its contents catches later edits)
+        self._plan_objs[id(p)] = (p, self._plans[key], [list(g) for g in p.gpus], (p.num_gpus, p.gpcs_per_gpu))
         return self._plans[key]
 
     def routing(self, segs: Sequence[tuple[int, int, int]]) -> int:
