@@ -172,10 +172,10 @@ struct msv_ctx {
     int64_t launches = 0;
     int64_t h2d = 0, d2h = 0;
     cudaEvent_t ev[8] = {};
-    cudaStream_t aux[4] = {};    // chunk streams of overlapped grid launches
-    cudaEvent_t aux_ev[4] = {};
+    cudaStream_t aux[8] = {};    // chunk streams of overlapped grid launches
+    cudaEvent_t aux_ev[8] = {};
     cudaEvent_t fork_ev = nullptr;
-    cudaEvent_t region_ev[2] = {};  // a multi-wave grid's buffer region is free again
+    cudaEvent_t region_ev[8] = {};  // a multi-wave grid's buffer region is free again
     uint64_t grid_serial = 0;       // grids created on this context
     uint64_t last_launch_grid = 0;  // serial of the grid launched last
     cudaStream_t cls[4] = {};    // extra class streams: a chunk's kernel classes run concurrently
@@ -265,7 +265,8 @@ struct ClassKey {
 constexpr int kMaxChunks = 8;           // chunks per wave (pipelined over kAuxStreams streams)
 constexpr int64_t kChunkScenarios = 1024;  // smallest chunk worth its own launch
 constexpr int kCounterSlots = 1024;      // work-stealing counters per launch (chunk x class)
-constexpr int kAuxStreams = 4;  // chunk c runs on aux stream c % kAuxStreams
+constexpr int kAuxStreams = 4;  // chunk c runs on aux stream c % kAuxStreams (more for more regions)
+constexpr int kMaxRegions = 8;  // buffer regions of a multi-wave grid (ctx->region_ev, ctx->aux)
 
 // Kernel class of a plan with P partitions. The one-scenario-per-warp kernel (W = 32)
 // serves every plan; the segmented kernel runs G = 32/W scenarios per warp (W lanes
@@ -616,8 +617,11 @@ int grid_build(msv_ctx* ctx, const msv_scenario* sc, int64_t n, const double* ta
         for (int64_t i = 0; i < n; ++i) total_q += g->cap[i];
         int64_t cap_w = max_q;
         int64_t n_waves = std::max<int64_t>(1, (total_q + max_q - 1) / max_q);
+        // MSV_WAVE_REGIONS (A/B): buffer regions the waves rotate through (default 2)
+        static const int regions_env = getenv("MSV_WAVE_REGIONS") ? atoi(getenv("MSV_WAVE_REGIONS")) : 2;
+        const int regions = std::max(2, std::min(kMaxRegions, regions_env));
         if (n_waves > 1 && g->generated) {
-            cap_w = std::max<int64_t>(max_q / 2, 1);
+            cap_w = std::max<int64_t>(max_q / regions, 1);
             n_waves = (total_q + cap_w - 1) / cap_w;
         }
         const int64_t target = (total_q + n_waves - 1) / n_waves;
@@ -633,7 +637,7 @@ int grid_build(msv_ctx* ctx, const msv_scenario* sc, int64_t n, const double* ta
             wave_q.push_back(q);
             s0 = s1;
         }
-        g->n_regions = g->waves.size() > 1 ? 2 : 1;
+        g->n_regions = g->waves.size() > 1 ? (int)std::min<int64_t>(regions, (int64_t)g->waves.size()) : 1;
         for (int64_t q : wave_q) g->max_wave_q = std::max(g->max_wave_q, q);
     }
     pt.mark("waves");
@@ -1049,6 +1053,36 @@ void debug_sync(cudaStream_t st, const char* what) {
     fprintf(stderr, "[msv] %s done: %s\n", what, cudaGetErrorString(e));
 }
 
+// MSV_TIMELINE=1 (diagnostics): events around every chunk's stages; grid_launch prints
+// them relative to the launch's start once it completes (synchronising: not for timing runs).
+struct TimelineMark {
+    std::string what;
+    cudaEvent_t ev;
+};
+static std::vector<TimelineMark> g_timeline;
+static bool timeline_on() {
+    static const bool on = getenv("MSV_TIMELINE") != nullptr;
+    return on;
+}
+static void timeline_mark(const std::string& what, cudaStream_t st) {
+    if (!timeline_on()) return;
+    cudaEvent_t e;
+    if (cudaEventCreate(&e) != cudaSuccess) return;
+    cudaEventRecord(e, st);
+    g_timeline.push_back({what, e});
+}
+static void timeline_print(cudaEvent_t start) {
+    if (!timeline_on() || g_timeline.empty()) return;
+    cudaDeviceSynchronize();
+    for (const TimelineMark& m : g_timeline) {
+        float ms = 0;
+        cudaEventElapsedTime(&ms, start, m.ev);
+        fprintf(stderr, "[msv] timeline %9.2f ms %s\n", ms, m.what.c_str());
+        cudaEventDestroy(m.ev);
+    }
+    g_timeline.clear();
+}
+
 // Launch one chunk's K1 -> K2 (per class) -> K3 on `st`. Stage events (optional) bracket
 // the three stages when the launch is not overlapped.
 int launch_chunk(msv_grid* g, const msv_grid::Chunk& ch, int counter_base, cudaStream_t st, cudaEvent_t e1,
@@ -1057,6 +1091,8 @@ int launch_chunk(msv_grid* g, const msv_grid::Chunk& ch, int counter_base, cudaS
     const int64_t nl = ch.l1 - ch.l0;
     const bool stream = g->stream_ok && !g->records && !g->usage;  // K1 inside K2's blocks
     static const bool stream_pregen = getenv("MSV_STREAM_PREGEN") != nullptr;  // A/B: K1 first anyway
+    const std::string tag = "chunk l" + std::to_string(ch.l0) + "-" + std::to_string(ch.l1);
+    timeline_mark(tag + " start", st);
     if (g->generated && nl > 0 && (!stream || stream_pregen)) {
         if (ch.g1 - ch.g0 == nl)  // no shared streams in this chunk: one warp per trace
             MSV_CUDA_TRY(msv::launch_trace_gen(g->B->d_tjobs.as<msv::TraceJob>() + ch.l0, (int)nl, ctx->log1p, st));
@@ -1068,6 +1104,7 @@ int launch_chunk(msv_grid* g, const msv_grid::Chunk& ch, int counter_base, cudaS
         ctx->launches += 1;
     }
     if (e1) MSV_CUDA_TRY(cudaEventRecord(e1, st));
+    timeline_mark(tag + " K1 done", st);
     // A chunk's kernel classes are independent: the largest runs on the chunk stream, the
     // others on class streams forked after K1, so their blocks fill the largest one's
     // last round instead of each class launch ending in its own tail.
@@ -1163,12 +1200,14 @@ int launch_chunk(msv_grid* g, const msv_grid::Chunk& ch, int counter_base, cudaS
         }
     }
     if (e2) MSV_CUDA_TRY(cudaEventRecord(e2, st));
+    timeline_mark(tag + " K2 done", st);
     if (!g->tail_p.empty() && nl > 0) {
         MSV_CUDA_TRY(msv::launch_tail(g->B->d_tailjobs.as<msv::TailJob>() + ch.l0, (int)nl, g->B->d_p.as<double>(),
                                       (int)g->tail_p.size(), st));
         debug_sync(st, "tail");
         ctx->launches += 1;
     }
+    timeline_mark(tag + " K3 done", st);
     return MSV_OK;
 }
 
@@ -1197,8 +1236,10 @@ int grid_launch(msv_grid* g) {
         if (n > first) MSV_CUDA_TRY(cudaMemsetAsync(g->B->d_counter.p, 0, (n - first) * sizeof(int32_t), s));
         return MSV_OK;
     };
+    // waves of a multi-region grid each need their own stream to run side by side
+    const int n_aux = std::max(kAuxStreams, std::min(8, g->n_regions));
     if (overlap) {
-        for (int a = 0; a < kAuxStreams; ++a) {
+        for (int a = 0; a < n_aux; ++a) {
             if (!ctx->aux[a]) MSV_CUDA_TRY(cudaStreamCreateWithFlags(&ctx->aux[a], cudaStreamNonBlocking));
             if (!ctx->aux_ev[a]) MSV_CUDA_TRY(cudaEventCreateWithFlags(&ctx->aux_ev[a], cudaEventDisableTiming));
         }
@@ -1207,7 +1248,7 @@ int grid_launch(msv_grid* g) {
     int counter_base = 0;
     float tr = 0, si = 0, ta = 0;
     if (overlap && g->n_regions > 1)
-        for (int r = 0; r < 2; ++r)
+        for (int r = 0; r < g->n_regions; ++r)
             if (!ctx->region_ev[r]) MSV_CUDA_TRY(cudaEventCreateWithFlags(&ctx->region_ev[r], cudaEventDisableTiming));
     size_t chunk_seq = 0;  // chunks of consecutive waves go to different aux streams
     for (size_t wi = 0; wi < g->waves.size(); ++wi) {
@@ -1217,9 +1258,9 @@ int grid_launch(msv_grid* g) {
             // wave that reuses a buffer region waits only for the wave that used it last
             // (the two regions' waves overlap: one drains while the next fills the SMs)
             if (!pipelined && wi == 0) MSV_CUDA_TRY(cudaEventRecord(ctx->fork_ev, st));
-            std::vector<char> used(kAuxStreams, 0);
+            std::vector<char> used(n_aux, 0);
             for (size_t c = 0; c < w.chunks.size(); ++c) {
-                const int a = (int)((chunk_seq++) % kAuxStreams);
+                const int a = (int)((chunk_seq++) % n_aux);
                 cudaStream_t sc = ctx->aux[a];
                 used[a] = 1;
                 if (!pipelined && wi < (size_t)g->n_regions) MSV_CUDA_TRY(cudaStreamWaitEvent(sc, ctx->fork_ev, 0));
@@ -1231,7 +1272,7 @@ int grid_launch(msv_grid* g) {
             }
             // join: the main stream continues after every chunk of this wave, and the
             // wave's region is free again from here
-            for (int a = 0; a < kAuxStreams; ++a) {
+            for (int a = 0; a < n_aux; ++a) {
                 if (!used[a]) continue;
                 MSV_CUDA_TRY(cudaEventRecord(ctx->aux_ev[a], ctx->aux[a]));
                 MSV_CUDA_TRY(cudaStreamWaitEvent(st, ctx->aux_ev[a], 0));
@@ -1268,6 +1309,10 @@ int grid_launch(msv_grid* g) {
         g->t_total = tr + si + ta;
     } else {
         g->t_total = -1;  // resolved lazily in msv_grid_timing
+    }
+    if (timeline_on()) {
+        timeline_mark("launch end", st);
+        timeline_print(g->ev[0]);
     }
     return MSV_OK;
 }
@@ -1411,7 +1456,7 @@ int msv_destroy(msv_ctx* ctx) {
     cudaStreamSynchronize(ctx->stream);
     for (cudaEvent_t e : ctx->ev)
         if (e) cudaEventDestroy(e);
-    for (int a = 0; a < 4; ++a) {
+    for (int a = 0; a < 8; ++a) {
         if (ctx->aux[a]) {
             cudaStreamSynchronize(ctx->aux[a]);
             cudaStreamDestroy(ctx->aux[a]);
