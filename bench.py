@@ -205,7 +205,7 @@ def run_reference(args):
     val = float(np.median(vals))
     line = {"impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": None, "higher_is_better": True,
-            "scaling": "strong" if args.gpus > 1 else "weak", "vs_baseline": None, "dtype": "f64",
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "config": config(args, args.gpus, specs),
             "cpu_baseline": {**base, "value": val},
             "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -381,7 +381,7 @@ def main():
                      "peak_warp_inst_per_s": pk, "source": prof_src, "fresh": fresh}
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": dev_ms_max / args.steps, "higher_is_better": True,
-                "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "f64",
+                "scaling": "strong", "vs_baseline": None, "dtype": "f64",
                 "data": "synthetic", "config": config(args, world, specs),
                 "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": (h1 - h0) // e2e_steps,
                         "d2h_bytes_per_step": (d1 - d0) // e2e_steps,
