@@ -2027,7 +2027,6 @@ int msv_run_noise(msv_ctx* ctx, const msv_scenario* scenario, int64_t n, const d
     int32_t P = 0;
     int rc = validate_scenario(ctx, sc, false, &P);
     if (rc) return rc;
-    if (P > 64) return fail(MSV_PARAM, "run: execution noise on the device supports at most 64 partitions");
     if ((int64_t)ctx->profiles[sc.profile].lat.size() > msv::kMaxSmemCells)
         return fail(MSV_PARAM, "run: profile has more than " + std::to_string(msv::kMaxSmemCells) +
                                    " (size, batch) cells, the device table limit");
@@ -2092,7 +2091,7 @@ int msv_run_noise(msv_ctx* ctx, const msv_scenario* scenario, int64_t n, const d
     DevBuf d_job;
     MSV_CUDA_TRY(d_job.ensure(sizeof(msv::NoiseParams)));
     MSV_CUDA_TRY(cudaMemcpyAsync(d_job.p, &np, sizeof np, cudaMemcpyHostToDevice, st));
-    MSV_CUDA_TRY(msv::launch_noise(d_job.as<msv::NoiseParams>(), 1, np.n_cells, st));
+    MSV_CUDA_TRY(msv::launch_noise(d_job.as<msv::NoiseParams>(), 1, np.n_cells, P, st));
     ctx->launches += 1;
     DevOut o{};
     MSV_CUDA_TRY(cudaMemcpyAsync(&o, d_out.p, sizeof(DevOut), cudaMemcpyDeviceToHost, st));
@@ -2706,9 +2705,6 @@ int run_grid_noise_dev(msv_ctx* ctx, const msv_scenario* sc, int64_t n, const do
             g_err = "scenario " + std::to_string(i) + ": " + g_err;
             return rc;
         }
-        if (P[i] > 64)
-            return fail(MSV_PARAM, "scenario " + std::to_string(i) +
-                                       ": run: execution noise on the device supports at most 64 partitions");
         if (!(sigma[i] > 0.0)) return fail(MSV_PARAM, "scenario " + std::to_string(i) + ": noise_sigma must be > 0");
         const int cells = (int)ctx->profiles[sc[i].profile].lat.size();
         if (cells > msv::kMaxSmemCells) return fail(MSV_PARAM, "run: profile exceeds the device table limit");
@@ -2868,7 +2864,9 @@ int run_grid_noise_dev(msv_ctx* ctx, const msv_scenario* sc, int64_t n, const do
             MSV_CUDA_TRY(cudaMemcpyAsync(ctx->d_mult.as<double>() + toff[s0], ctx->pin[b],
                                          (size_t)(toff[s1] - toff[s0]) * 8, cudaMemcpyHostToDevice, sa));
             MSV_CUDA_TRY(cudaEventRecord(ctx->pin_ev[b], sa));
-            MSV_CUDA_TRY(msv::launch_noise(ctx->d_njobs.as<msv::NoiseParams>() + s0, (int)(s1 - s0), max_cells, sa));
+            int max_p = 0;
+            for (int64_t i = s0; i < s1; ++i) max_p = std::max(max_p, (int)P[i]);
+            MSV_CUDA_TRY(msv::launch_noise(ctx->d_njobs.as<msv::NoiseParams>() + s0, (int)(s1 - s0), max_cells, max_p, sa));
             ctx->launches += 1;
             s0 = s1;
         }

@@ -205,7 +205,7 @@ struct NoiseParams {
 
 // Kernel launchers (msv_kernels.cu). Return cudaGetLastError().
 // One block (one warp) per job; max_cells = the largest job's profile cells.
-cudaError_t launch_noise(const NoiseParams* d_jobs, int n_jobs, int max_cells, cudaStream_t stream);
+cudaError_t launch_noise(const NoiseParams* d_jobs, int n_jobs, int max_cells, int max_parts, cudaStream_t stream);
 cudaError_t launch_paris(const ParisParams& p, cudaStream_t stream);
 // K1 over groups: group g covers jobs [first, first + count) (count <= kTraceGroupMax, one
 // seed and distribution per group).

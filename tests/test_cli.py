@@ -216,13 +216,21 @@ def test_noise_run_tree_identical_to_reference(tmp_path, cfg, extra):
 
 
 @pytest.mark.gpu
+@need_ref
 @need_dev
-def test_noise_partition_limit(tmp_path):
-    """K5 holds at most 64 partitions (two lane slots): larger plans raise ParamError."""
-    cfg = write_cfg(tmp_path, {**SMALL, "server": {"num_gpus": 10}, "engine": {"noise_sigma": 0.1},
-                               "designs": [{"plan": "gpu(1)", "scheduler": "elsa"}]})
-    r = msv(DEV, "run", cfg, "--out", tmp_path / "o")
-    assert r.returncode == 1 and "ParamError" in r.stderr and "64" in r.stderr, r.stderr
+def test_noise_four_slots_and_partition_limit(tmp_path):
+    """K5 with four lane slots: a 70-partition plan (10 GPUs of 1g) with execution noise is
+    byte-identical to the reference engine, ELSA and FIFS; plans beyond 128 partitions raise
+    ParamError (the device engine's limit, with or without noise)."""
+    cfg = write_cfg(tmp_path, {**SMALL, "server": {"num_gpus": 10}, "engine": {"noise_sigma": 0.3},
+                               "workload": {"rate_qps": 3000, "duration_ms": 800, "seeds": [1, 2]},
+                               "designs": [{"plan": "gpu(1)", "scheduler": "elsa"},
+                                           {"plan": "gpu(1)", "scheduler": "fifs"}]})
+    _both(tmp_path, "run", cfg)
+    big = write_cfg(tmp_path, {**SMALL, "server": {"num_gpus": 19}, "engine": {"noise_sigma": 0.1},
+                               "designs": [{"plan": "gpu(1)", "scheduler": "elsa"}]}, "big.json")
+    r = msv(DEV, "run", big, "--out", tmp_path / "o2")
+    assert r.returncode == 1 and "ParamError" in r.stderr and "128" in r.stderr, r.stderr
 
 
 @pytest.mark.gpu

@@ -777,9 +777,11 @@ def test_noise_grid_matches_reference(eng, ref):
         pytest.skip("noise parity needs oracle/_ref")
     rng = np.random.default_rng(3)
     specs, sig, seeds = [], [], []
-    for name, gpus in (("mobilenet", 8), ("bert_base", 8), ("resnet50", 1), ("bert_base", 2)):
+    plans = [(name, W.paris(W.model(name), gpus)) for name, gpus in
+             (("mobilenet", 8), ("bert_base", 8), ("resnet50", 1), ("bert_base", 2))]
+    plans.append(("mobilenet", homogeneous_plan(1, 112, 16, 7)))  # P = 112: four lane slots
+    for name, plan in plans:
         m = W.model(name)
-        plan = W.paris(m, gpus)
         for load in (0.4, 0.8, 1.1):
             for sched in ("elsa", "fifs"):
                 specs.append(GridSpec(plan, m.table, m.dist, m.sla, load * W.capacity_qps(m, plan),

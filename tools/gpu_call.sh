@@ -1,5 +1,4 @@
-P=gpurun_out/r02/final5
+P=gpurun_out/r02/noise4
 mkdir -p $P
+timeout 900 python -m pytest tests -m gpu -x -q -k "noise" > $P/t.log 2>&1; tail -3 $P/t.log
 timeout 1800 python -m pytest tests -m gpu -x -q > $P/gpu_tests.log 2>&1; tail -2 $P/gpu_tests.log
-timeout 300 python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')" > $P/smoke.log 2>&1; tail -1 $P/smoke.log
-timeout 900 python bench.py > $P/bench.log 2>&1; tail -1 $P/bench.log | cut -c1-200
