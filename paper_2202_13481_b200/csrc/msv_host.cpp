@@ -328,7 +328,8 @@ struct msv_grid {
     int64_t n = 0;
     std::vector<msv_scenario> scen;
     std::vector<double> tail_p;
-    std::vector<int64_t> cap, toff;   // per-scenario trace capacity and offset
+    std::vector<int64_t> cap, toff;   // per-scenario trace capacity and offset (arrival, batch)
+    std::vector<int64_t> noff;        // per-scenario offset in the overflow-link buffer
     std::vector<int32_t> P, usage_off;
     std::vector<uint8_t> bad;  // plan has a size the profile lacks
     // Streamed K1 -> K2 (msv_sim_warp.cu STREAM): a latency-bound generated grid (one wave,
@@ -358,7 +359,8 @@ struct msv_grid {
     bool usage = true;                  // accumulate per-partition usage (msv_grid_set_usage)
     std::vector<Wave> waves;
     int64_t max_wave_q = 0;             // query slots of the largest wave (one buffer region)
-    int n_regions = 1;                  // buffer regions the waves alternate between
+    int n_regions = 1;                  // buffer regions the waves alternate between (links, K2 / K3)
+    int n_in_regions = 1;               // regions of the trace inputs (arrival / latency + batch)
     GridBufs own;            // buffers of a persistent grid (msv_grid_create)
     GridBufs* B = &own;      // -> own, or the context's scratch set for one-shot calls
     int n_cells = 0;
@@ -552,6 +554,7 @@ int grid_build(msv_ctx* ctx, const msv_scenario* sc, int64_t n, const double* ta
     g->tail_p.assign(tail_p, tail_p + n_tails);
     g->cap.resize(n);
     g->toff.resize(n);
+    g->noff.resize(n);
     g->P.resize(n);
     g->usage_off.resize(n);
     for (int64_t i = 0; i < n; ++i) {
@@ -620,10 +623,16 @@ int grid_build(msv_ctx* ctx, const msv_scenario* sc, int64_t n, const double* ta
         // MSV_WAVE_REGIONS (A/B): buffer regions the waves rotate through (default 2)
         static const int regions_env = getenv("MSV_WAVE_REGIONS") ? atoi(getenv("MSV_WAVE_REGIONS")) : 2;
         const int regions = std::max(2, std::min(kMaxRegions, regions_env));
+        // MSV_INPUT_REGIONS (A/B): the trace inputs (arrival / latency 8 + batch 4 bytes per
+        // slot) rotate through more regions than the overflow links (4 bytes), so a wave's K1
+        // can run while the waves before it still hold the link regions
+        static const int in_env = getenv("MSV_INPUT_REGIONS") ? atoi(getenv("MSV_INPUT_REGIONS")) : regions;
+        const int in_regions = std::max(regions, std::min(kMaxRegions / 2, in_env));
         if (n_waves > 1 && g->generated) {
-            cap_w = std::max<int64_t>(max_q / regions, 1);
+            cap_w = std::max<int64_t>((int64_t)(budget / (size_t)(12 * in_regions + 4 * regions)), 1);
             n_waves = (total_q + cap_w - 1) / cap_w;
         }
+        g->n_in_regions = n_waves > 1 && g->generated ? (int)std::min<int64_t>(in_regions, n_waves) : 1;
         const int64_t target = (total_q + n_waves - 1) / n_waves;
         int64_t s0 = 0;
         while (s0 < n) {
@@ -638,6 +647,8 @@ int grid_build(msv_ctx* ctx, const msv_scenario* sc, int64_t n, const double* ta
             s0 = s1;
         }
         g->n_regions = g->waves.size() > 1 ? (int)std::min<int64_t>(regions, (int64_t)g->waves.size()) : 1;
+        if (g->waves.size() <= 1) g->n_in_regions = 1;
+        g->n_in_regions = std::max(g->n_in_regions, g->n_regions);
         for (int64_t q : wave_q) g->max_wave_q = std::max(g->max_wave_q, q);
     }
     pt.mark("waves");
@@ -687,10 +698,12 @@ int grid_build(msv_ctx* ctx, const msv_scenario* sc, int64_t n, const double* ta
                                        : 2;
     for (size_t wi = 0; wi < g->waves.size(); ++wi) {
         msv_grid::Wave& w = g->waves[wi];
-        w.q0 = (int64_t)(wi % g->n_regions) * g->max_wave_q;  // the wave's buffer region
+        w.q0 = (int64_t)(wi % g->n_in_regions) * g->max_wave_q;  // the wave's input region
+        const int64_t n0 = (int64_t)(wi % g->n_regions) * g->max_wave_q;  // and link region
         int64_t q = w.q0;
         for (int64_t i = w.s0; i < w.s1; ++i) {
             g->toff[i] = q;  // offset inside the trace buffers
+            g->noff[i] = n0 + (q - w.q0);
             q += g->cap[i];
         }
         w.q1 = q;
@@ -808,10 +821,11 @@ int grid_build(msv_ctx* ctx, const msv_scenario* sc, int64_t n, const double* ta
     g->cost = cost;
     pt.mark("cost+chunks");
     // Device buffers.
-    const size_t wq = (size_t)std::max<int64_t>(g->max_wave_q * g->n_regions, 1);
+    const size_t wq = (size_t)std::max<int64_t>(g->max_wave_q * g->n_in_regions, 1);
+    const size_t wn = (size_t)std::max<int64_t>(g->max_wave_q * g->n_regions, 1);
     MSV_CUDA_TRY(g->B->d_arr.ensure(wq * 8));
     MSV_CUDA_TRY(g->B->d_bat.ensure(wq * 4));
-    MSV_CUDA_TRY(g->B->d_next.ensure(wq * 4));
+    MSV_CUDA_TRY(g->B->d_next.ensure(wn * 4));
     if (records) MSV_CUDA_TRY(g->B->d_rec.ensure(wq * sizeof(msv_record)));
     MSV_CUDA_TRY(g->B->d_scen.ensure(std::max<int64_t>(n, 1) * sizeof(DevScen)));
     MSV_CUDA_TRY(g->B->d_out.ensure(std::max<int64_t>(n, 1) * sizeof(DevOut)));
@@ -939,7 +953,7 @@ int grid_build(msv_ctx* ctx, const msv_scenario* sc, int64_t n, const double* ta
         d.beta = s.beta;
         d.parts = g->B->d_parts.as<DevPart>() + sc_part[i];
         d.route_mask = (sc_mask[i] == (size_t)-1) ? nullptr : g->B->d_masks.as<uint64_t>() + sc_mask[i];
-        d.next = g->B->d_next.as<uint32_t>() + o;
+        d.next = g->B->d_next.as<uint32_t>() + g->noff[i];
         d.samples = g->B->d_arr.as<double>() + o;  // latencies overwrite their own (dead) arrivals
         d.records = records ? g->B->d_rec.as<msv_record>() + o : nullptr;
         d.P = g->P[i];
@@ -1086,7 +1100,7 @@ static void timeline_print(cudaEvent_t start) {
 // Launch one chunk's K1 -> K2 (per class) -> K3 on `st`. Stage events (optional) bracket
 // the three stages when the launch is not overlapped.
 int launch_chunk(msv_grid* g, const msv_grid::Chunk& ch, int counter_base, cudaStream_t st, cudaEvent_t e1,
-                 cudaEvent_t e2) {
+                 cudaEvent_t e2, cudaEvent_t k2_wait = nullptr) {
     msv_ctx* ctx = g->ctx;
     const int64_t nl = ch.l1 - ch.l0;
     const bool stream = g->stream_ok && !g->records && !g->usage;  // K1 inside K2's blocks
@@ -1105,6 +1119,7 @@ int launch_chunk(msv_grid* g, const msv_grid::Chunk& ch, int counter_base, cudaS
     }
     if (e1) MSV_CUDA_TRY(cudaEventRecord(e1, st));
     timeline_mark(tag + " K1 done", st);
+    if (k2_wait) MSV_CUDA_TRY(cudaStreamWaitEvent(st, k2_wait, 0));  // the link region is free
     // A chunk's kernel classes are independent: the largest runs on the chunk stream, the
     // others on class streams forked after K1, so their blocks fill the largest one's
     // last round instead of each class launch ending in its own tail.
@@ -1247,8 +1262,11 @@ int grid_launch(msv_grid* g) {
     }
     int counter_base = 0;
     float tr = 0, si = 0, ta = 0;
+    // wave w's completion: region_ev[w % kWaveRing]. Its K1 waits for wave w - n_in_regions
+    // (the input region), its K2 for wave w - n_regions (the link region).
+    constexpr int kWaveRing = 8;  // (ctx->region_ev slots: at least the largest lookback)
     if (overlap && g->n_regions > 1)
-        for (int r = 0; r < g->n_regions; ++r)
+        for (int r = 0; r < kWaveRing; ++r)
             if (!ctx->region_ev[r]) MSV_CUDA_TRY(cudaEventCreateWithFlags(&ctx->region_ev[r], cudaEventDisableTiming));
     size_t chunk_seq = 0;  // chunks of consecutive waves go to different aux streams
     for (size_t wi = 0; wi < g->waves.size(); ++wi) {
@@ -1263,11 +1281,14 @@ int grid_launch(msv_grid* g) {
                 const int a = (int)((chunk_seq++) % n_aux);
                 cudaStream_t sc = ctx->aux[a];
                 used[a] = 1;
-                if (!pipelined && wi < (size_t)g->n_regions) MSV_CUDA_TRY(cudaStreamWaitEvent(sc, ctx->fork_ev, 0));
-                if (wi >= (size_t)g->n_regions)
-                    MSV_CUDA_TRY(cudaStreamWaitEvent(sc, ctx->region_ev[wi % g->n_regions], 0));
+                if (!pipelined && wi < (size_t)g->n_in_regions) MSV_CUDA_TRY(cudaStreamWaitEvent(sc, ctx->fork_ev, 0));
+                if (wi >= (size_t)g->n_in_regions)
+                    MSV_CUDA_TRY(cudaStreamWaitEvent(sc, ctx->region_ev[(wi - g->n_in_regions) % kWaveRing], 0));
+                cudaEvent_t k2_wait = nullptr;
+                if (wi >= (size_t)g->n_regions && g->n_in_regions > g->n_regions)
+                    k2_wait = ctx->region_ev[(wi - g->n_regions) % kWaveRing];
                 if ((rc = zero_counters(counter_base, w.chunks[c].classes.size(), sc))) return rc;
-                if ((rc = launch_chunk(g, w.chunks[c], counter_base, sc, nullptr, nullptr))) return rc;
+                if ((rc = launch_chunk(g, w.chunks[c], counter_base, sc, nullptr, nullptr, k2_wait))) return rc;
                 counter_base += (int)w.chunks[c].classes.size();
             }
             // join: the main stream continues after every chunk of this wave, and the
@@ -1277,7 +1298,7 @@ int grid_launch(msv_grid* g) {
                 MSV_CUDA_TRY(cudaEventRecord(ctx->aux_ev[a], ctx->aux[a]));
                 MSV_CUDA_TRY(cudaStreamWaitEvent(st, ctx->aux_ev[a], 0));
             }
-            if (g->n_regions > 1) MSV_CUDA_TRY(cudaEventRecord(ctx->region_ev[wi % g->n_regions], st));
+            if (g->n_regions > 1) MSV_CUDA_TRY(cudaEventRecord(ctx->region_ev[wi % kWaveRing], st));
         } else {
             for (const msv_grid::Chunk& ch : w.chunks) {
                 cudaEvent_t e0 = g->ev[0], e1 = g->ev[1], e2 = g->ev[2], e3 = g->ev[3];
