@@ -182,20 +182,20 @@ __global__ void __launch_bounds__(32, 1) sim_noise_kernel(const NoiseParams* __r
                     if (qn[s] > 0) {  // start the queue head now (engine.hpp:181-185)
                         const int64_t h = qh[s];
                         qh[s] = p.next[h];
-                        if (elsa) {  // the ring drops its head and takes queue item kRing
-                            const int vac = rh[s];
-                            rh[s] = (vac + 1) & (kRing - 1);
-                            if (qn[s] > kRing) {
-                                ring[s][vac][lane] = lat[row[s] + bat[rq[s]] - 1];
-                                if (qn[s] > kRing + 1) rq[s] = p.next[rq[s]];
-                            }
+                        // the head's latency comes from the ring (cached when it was queued), so
+                        // the new finish does not wait for a global load of the head's batch
+                        const int vac = rh[s];
+                        const double est = ring[s][vac][lane];
+                        rh[s] = (vac + 1) & (kRing - 1);  // the ring drops its head, takes item kRing
+                        if (qn[s] > kRing) {
+                            ring[s][vac][lane] = lat[row[s] + bat[rq[s]] - 1];
+                            if (qn[s] > kRing + 1) rq[s] = p.next[rq[s]];
                         }
                         qn[s] -= 1;
                         if (qn[s] == 0) qt[s] = -1;
-                        const int32_t hb = bat[h];
+                        const int32_t hb = bat[h];  // needed at its completion (utilisation)
                         c_arr[s] = arr[h];
                         c_b[s] = hb;
-                        const double est = lat[row[s] + hb - 1];
                         c_start[s] = now;
                         c_est[s] = est;
                         c_comp[s] = now + est * mw[j - mj];
@@ -375,11 +375,9 @@ __global__ void __launch_bounds__(32, 1) sim_noise_kernel(const NoiseParams* __r
                     p.records[i].partition = pid[s];
                     p.records[i].kind = kind;
                 }
-                if (busy[s]) {
-                    if (elsa) {
-                        if (qn[s] < kRing) ring[s][(rh[s] + (int)qn[s]) & (kRing - 1)][lane] = est;
-                        else if (qn[s] == kRing) rq[s] = i;
-                    }
+                if (busy[s]) {  // queue it; the ring caches the first kRing latencies (both schedulers)
+                    if (qn[s] < kRing) ring[s][(rh[s] + (int)qn[s]) & (kRing - 1)][lane] = est;
+                    else if (qn[s] == kRing) rq[s] = i;
                     if (qn[s] == 0) {
                         qh[s] = i;
                     } else {

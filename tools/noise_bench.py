@@ -21,7 +21,8 @@ assert ref.kind == "reference", "needs oracle/_ref (the C port has no noise path
 qmax = float(sys.argv[1]) if len(sys.argv) > 1 else 1e6
 rows = []
 for m, gpus, sched, load, sigma in (("bert_base", 8, "elsa", 0.5, 0.1), ("bert_base", 8, "elsa", 0.9, 0.3),
-                                    ("resnet50", 8, "elsa", 0.9, 0.3), ("mobilenet", 8, "fifs", 0.9, 0.3)):
+                                    ("resnet50", 8, "elsa", 0.9, 0.3), ("mobilenet", 8, "fifs", 0.9, 0.3),
+                                    ("bert_base", 8, "elsa", 1.3, 0.3)):  # overloaded: queues grow
     mod = W.model(m)
     plan = W.paris(mod, gpus)
     rate = load * W.capacity_qps(mod, plan)
