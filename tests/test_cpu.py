@@ -205,3 +205,35 @@ def test_ref_workloads_match_product_workloads():
             assert (a.sla.sla_target_ms, a.sla.alpha, a.sla.beta) == (b.sla.sla_target_ms, b.sla.alpha, b.sla.beta)
             assert (a.rate_qps, a.duration_ms, a.seed, a.scheduler, a.warmup_fraction) == \
                    (b.rate_qps, b.duration_ms, b.seed, b.scheduler, b.warmup_fraction)
+
+
+def test_engine_plan_handle_cache_sees_edits():
+    """Engine.plan reuses the handle of the same, unchanged plan object without rebuilding its
+    by-value key, and re-keys a plan object whose contents were edited after upload (no GPU:
+    the upload call is stubbed)."""
+    import copy
+    from paper_2202_13481_b200 import engine as E
+    from paper_2202_13481_b200 import workloads as W
+
+    class Lib:
+        def __init__(self):
+            self.uploads = 0
+
+        def msv_upload_plan(self, h, num_gpus, gpcs, n_per, flat, out):
+            self.uploads += 1
+            out._obj.value = self.uploads
+            return 0
+
+    eng = E.Engine.__new__(E.Engine)  # no device context
+    eng._lib, eng._h = Lib(), None
+    eng._plans, eng._plan_objs = {}, {}
+    m = W.model("resnet50")
+    p = copy.deepcopy(W.paris(m, 8))
+    h1 = eng.plan(p)
+    assert eng.plan(p) == h1 and eng._lib.uploads == 1  # same object: cached
+    q = copy.deepcopy(p)
+    assert eng.plan(q) == h1 and eng._lib.uploads == 1  # equal contents: same handle, no upload
+    p.gpus[0] = list(reversed(p.gpus[0])) + [1] if p.gpus[0] else [1]  # edited after upload
+    h2 = eng.plan(p)
+    assert h2 != h1 and eng._lib.uploads == 2
+    assert eng.plan(p) == h2 and eng._lib.uploads == 2
