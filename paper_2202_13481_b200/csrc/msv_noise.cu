@@ -8,7 +8,7 @@
 // event order — (time asc, completion before arrival, seq asc), seq = push order
 // (engine.hpp:93-107, :134-137). This kernel keeps that order exactly:
 //   * one warp per scenario, lane slot s of lane l = by_ascending_size index s*32 + l
-//     (sched.hpp:96-104), P <= 128 (two or four slots per lane);
+//     (sched.hpp:96-104), P <= 128 (one, two or four slots per lane);
 //   * before each arrival (and after the last) the warp repeatedly takes the global
 //     minimum (completion time, seq) over the slots with completion <= t — a shuffle
 //     argmin — and retires it; a queue head started there takes the next multiplier and
@@ -27,8 +27,8 @@ namespace msv {
 
 namespace {
 
-// S slots per lane (P <= 32 * S); RING queued estimates per slot cached in shared memory
-// (ELSA): S = 2 with a 64-entry ring, S = 4 (P <= 128) with 32 entries — 32 KB either way.
+// S slots per lane (P <= 32 * S); RING queued latencies per slot cached in shared memory:
+// S = 1 (P <= 32) with a 128-entry ring, S = 2 with 64, S = 4 (P <= 128) with 32 — 32 KB each.
 template <int S, int RING>
 __global__ void __launch_bounds__(32, 1) sim_noise_kernel(const NoiseParams* __restrict__ jobs) {
     constexpr int kRing = RING;
@@ -456,12 +456,15 @@ cudaError_t launch_noise(const NoiseParams* d_jobs, int n_jobs, int max_cells, i
     // window) already eats most of the default 48 KB, so the default dynamic limit is
     // only ~15 KB (profiles of ~1,000 cells failed to launch).
     const size_t smem = (size_t)2 * max_cells * sizeof(double);
-    const void* fn = max_parts > 64 ? (const void*)sim_noise_kernel<4, 32> : (const void*)sim_noise_kernel<2, 64>;
+    const void* fn = max_parts > 64   ? (const void*)sim_noise_kernel<4, 32>
+                     : max_parts > 32 ? (const void*)sim_noise_kernel<2, 64>
+                                      : (const void*)sim_noise_kernel<1, 128>;
     const cudaError_t e = ensure_dyn_smem(fn, smem);
     if (e != cudaSuccess) return e;
     if (n_jobs <= 0) return cudaSuccess;
     if (max_parts > 64) sim_noise_kernel<4, 32><<<n_jobs, 32, smem, stream>>>(d_jobs);
-    else sim_noise_kernel<2, 64><<<n_jobs, 32, smem, stream>>>(d_jobs);
+    else if (max_parts > 32) sim_noise_kernel<2, 64><<<n_jobs, 32, smem, stream>>>(d_jobs);
+    else sim_noise_kernel<1, 128><<<n_jobs, 32, smem, stream>>>(d_jobs);
     return cudaGetLastError();
 }
 

@@ -789,12 +789,24 @@ def test_noise_grid_matches_reference(eng, ref):
                                       float(rng.choice([0.0, 0.1, 0.3]))))
                 sig.append(float(rng.choice([0.05, 0.3, 0.8])))
                 seeds.append(int(rng.integers(0, 2**63)))
+    # the whole grid (one chunk: four-slot K5 for every scenario), then the plans of <= 64 and of
+    # <= 32 partitions alone (two- and one-slot K5)
+    want_all = {}
+    for cut in (128, 64, 32):
+        idx = [k for k, s in enumerate(specs) if s.plan.total_instances() <= cut]
+        _check_noise_grid(eng, ref, [specs[k] for k in idx], [sig[k] for k in idx], [seeds[k] for k in idx],
+                          want_all, idx)
+
+
+def _check_noise_grid(eng, ref, specs, sig, seeds, cache, idx):
     got = eng.run_grid_noise(specs, sig, seeds, (0.95, 0.99), usage=True)
     uo = 0
     for k, s in enumerate(specs):
-        arr, bat = ref.sample_trace(s.dist, s.rate_qps, s.duration_ms, s.seed)
-        want = ref.run_noise(s.plan, s.scheduler, arr, bat, s.duration_ms, s.table, s.sla, s.warmup_fraction, None,
-                             sig[k], seeds[k])
+        if idx[k] not in cache:
+            arr, bat = ref.sample_trace(s.dist, s.rate_qps, s.duration_ms, s.seed)
+            cache[idx[k]] = (arr, ref.run_noise(s.plan, s.scheduler, arr, bat, s.duration_ms, s.table, s.sla,
+                                                s.warmup_fraction, None, sig[k], seeds[k]))
+        arr, want = cache[idx[k]]
         assert got["status"][k] == 0
         assert got["total"][k] == len(arr)
         for f in ("violations", "measured", "measured_violations"):
