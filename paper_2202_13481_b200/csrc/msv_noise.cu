@@ -136,23 +136,27 @@ __global__ void __launch_bounds__(32, 1) sim_noise_kernel(const NoiseParams* __r
                     bs = c_seq[s];
                     bsl = s;
                 }
-            int bl = bsl >= 0 ? lane : 32;
+            int bl;
             if (__popc(dm) == 1) {
                 bl = __ffs(dm) - 1;  // one lane has due completions: its own minimum is the global one
             } else {
-#pragma unroll
-                for (int off = 16; off > 0; off >>= 1) {
-                    const double ot = __shfl_xor_sync(kFull, bt, off);
-                    const uint64_t os = __shfl_xor_sync(kFull, bs, off);
-                    const int ol = __shfl_xor_sync(kFull, bl, off);
-                    if (ot < bt || (ot == bt && os < bs)) {
-                        bt = ot;
-                        bs = os;
-                        bl = ol;
-                    }
+                // the earliest (time, seq) over the due lanes: completion times are non-negative,
+                // so their IEEE bits order like the values — two 32-bit warp reductions find
+                // the minimum time, and only equal times fall back to the seq reduction
+                const uint64_t tb = bsl >= 0 ? msv_dbits(bt) : ~0ull;
+                const uint32_t mh = __reduce_min_sync(kFull, (uint32_t)(tb >> 32));
+                const uint32_t ml = __reduce_min_sync(kFull, (uint32_t)(tb >> 32) == mh ? (uint32_t)tb : 0xffffffffu);
+                const bool at_min = tb == (((uint64_t)mh << 32) | ml);
+                const unsigned tie = __ballot_sync(kFull, at_min);
+                if (__popc(tie) == 1) {
+                    bl = __ffs(tie) - 1;
+                } else {  // equal completion times: the smaller seq first (engine.hpp:101-107)
+                    const uint64_t sk = at_min ? bs : ~0ull;
+                    const uint32_t sh = __reduce_min_sync(kFull, (uint32_t)(sk >> 32));
+                    const uint32_t sl = __reduce_min_sync(kFull, (uint32_t)(sk >> 32) == sh ? (uint32_t)sk : 0xffffffffu);
+                    bl = __ffs(__ballot_sync(kFull, at_min && sk == (((uint64_t)sh << 32) | sl))) - 1;
                 }
             }
-            if (bl == 32) return;  // nothing due by t
             int started = 0;
             if (lane == bl) {
 #pragma unroll

@@ -1,4 +1,3 @@
-P=gpurun_out/r02/final7
-mkdir -p $P
-timeout 1800 python -m pytest tests -m gpu -x -q > $P/gpu_tests.log 2>&1; tail -2 $P/gpu_tests.log
-timeout 300 python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')" > $P/smoke.log 2>&1; tail -1 $P/smoke.log
+timeout 900 python -m pytest tests -m gpu -x -q -k "noise" 2>&1 | tail -1
+for v in base redux base redux; do echo "== $v"; MSV_LIB=_ab/$v.so timeout 600 python tools/_nb1.py; done
+MSV_LIB=_ab/redux.so timeout 900 python tools/noise_grid_bench.py 2>&1 | tail -3
