@@ -1,3 +1,3 @@
-timeout 900 python -m pytest tests -m gpu -x -q -k "noise" 2>&1 | tail -1
-for v in base redux base redux; do echo "== $v"; MSV_LIB=_ab/$v.so timeout 600 python tools/_nb1.py; done
-MSV_LIB=_ab/redux.so timeout 900 python tools/noise_grid_bench.py 2>&1 | tail -3
+mkdir -p gpurun_out/r02/extra
+timeout 1500 python tools/diag_lbt.py > gpurun_out/r02/extra/lbt.log 2>&1; cat gpurun_out/r02/extra/lbt.log | cut -c1-300
+timeout 900 python tools/noise_bench.py 1e5 > gpurun_out/r02/extra/noise_bench.log 2>&1; tail -5 gpurun_out/r02/extra/noise_bench.log | cut -c1-100
