@@ -1074,6 +1074,7 @@ struct TimelineMark {
     cudaEvent_t ev;
 };
 static std::vector<TimelineMark> g_timeline;
+static std::mutex g_timeline_mu;  // contexts on several threads may launch at once
 static bool timeline_on() {
     static const bool on = getenv("MSV_TIMELINE") != nullptr;
     return on;
@@ -1083,10 +1084,13 @@ static void timeline_mark(const std::string& what, cudaStream_t st) {
     cudaEvent_t e;
     if (cudaEventCreate(&e) != cudaSuccess) return;
     cudaEventRecord(e, st);
+    std::lock_guard<std::mutex> lk(g_timeline_mu);
     g_timeline.push_back({what, e});
 }
 static void timeline_print(cudaEvent_t start) {
-    if (!timeline_on() || g_timeline.empty()) return;
+    if (!timeline_on()) return;
+    std::lock_guard<std::mutex> lk(g_timeline_mu);
+    if (g_timeline.empty()) return;
     cudaDeviceSynchronize();
     for (const TimelineMark& m : g_timeline) {
         float ms = 0;
