@@ -1207,6 +1207,9 @@ int launch_chunk(msv_grid* g, const msv_grid::Chunk& ch, int counter_base, cudaS
         const int need = (nwork + segs_per_block - 1) / segs_per_block;
         int occ_used = occ;
         if (const char* e = getenv("MSV_SIM_BLOCK_SLACK")) occ_used = std::max(1, occ - atoi(e));
+        // MSV_MULTI_SLOT_BLOCKS (A/B): blocks per SM of the multi-slot classes' persistent grids
+        static const int ms_blocks = getenv("MSV_MULTI_SLOT_BLOCKS") ? atoi(getenv("MSV_MULTI_SLOT_BLOCKS")) : 0;
+        if (ms_blocks > 0 && k.S > 1 && k.W == 32) occ_used = std::min(occ_used, ms_blocks);
         const int dev_blocks = std::max(1, (int)std::lround(share[c] * occ_used * ctx->sms));
         const int blocks = std::max(1, std::min(need, dev_blocks));
         MSV_CUDA_TRY(msv::launch_sim(k.W, k.S, k.sched, g->records, p, blocks, cs));
