@@ -1,1 +1,5 @@
-for rep in 1 2 3; do for cfg in "MSV_MULTI_SLOT_BLOCKS=0" "MSV_MULTI_SLOT_BLOCKS=3" "MSV_MULTI_SLOT_BLOCKS=4" "MSV_MULTI_SLOT_BLOCKS=2"; do env $cfg timeout 900 python bench.py --no-cpu-baseline --steps 5 > gpurun_out/b.log 2>&1; echo -n "$cfg: "; tail -1 gpurun_out/b.log | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(round(d['value']/1e9,3), round(d['e2e']['value']/1e9,3), round(d['ms_per_step'],2))"; done; done
+P=gpurun_out/r02/final8
+mkdir -p $P
+timeout 1800 python -m pytest tests -m gpu -x -q > $P/gpu_tests.log 2>&1; tail -1 $P/gpu_tests.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')" > $P/smoke.log 2>&1; tail -1 $P/smoke.log
+timeout 900 python bench.py > $P/bench.log 2>&1; tail -1 $P/bench.log | cut -c1-120
