@@ -173,6 +173,27 @@ def test_run_records_bit_exact(eng, ref, case):
             assert got["max_wait_estimate_diff"] == want["max_wait_estimate_diff"]
 
 
+def test_full_size_records_bit_exact(eng, ref):
+    """per-query records at full size, not only a digest — four C5 cells (one-
+    and two-slot plans, ELSA and FIFS, the highest load) at 10^6 queries each: every query's
+    partition, kind, start and finish, and every partition's usage, equal to the compiled
+    reference's run() on the same trace."""
+    cells = W.c5_cells()
+    picks = [c for c in cells if c[4] == 0.9 and c[2] in ("paris", "homog1")][:4]
+    for k, (name, m, tag, plan, load) in enumerate(picks):
+        sched = "elsa" if k % 2 == 0 else "fifs"
+        rate = load * W.capacity_qps(m, plan)
+        duration = 1e6 / rate * 1000.0
+        arr, bat = ref.sample_trace(m.dist, rate, duration, 100 + k)
+        got = eng.run(plan, sched, arr, bat, duration, m.table, m.sla, 0.1)
+        want = ref.run(plan, sched, arr, bat, duration, m.table, m.sla, 0.1)
+        assert len(arr) > 9e5
+        for f in ("partition", "kind", "start_ms", "finish_ms", "busy_ms", "weighted_busy_ms", "queries"):
+            assert same(got[f], want[f]), (name, tag, f, np.nonzero(np.asarray(got[f]) != np.asarray(want[f]))[0][:5])
+        for f in ("total", "violations", "measured", "measured_violations", "horizon_ms"):
+            assert got[f] == want[f], (name, tag, f)
+
+
 def test_run_edge_cases(eng, ref):
     t = W_tables()["small_large"]
     one = PartitionPlan(1, 7, [[7]])
