@@ -162,6 +162,10 @@ struct msv_ctx {
     GridBufs scratch;  // reused by one-shot grids (msv_run_grid / msv_run_replay)
     // reused by noisy grids (msv_run_grid_noise): multipliers and K5 jobs
     DevBuf d_mult, d_njobs;
+    // reused by single noisy runs (msv_run_noise): no allocation per call
+    struct NoiseRunBufs {
+        DevBuf arr, bat, mult, lat, util, parts, masks, next, rec, use, out, job;
+    } noise1;
     // pinned staging of the multiplier streams: two buffers, alternating by chunk
     double* pin[2] = {nullptr, nullptr};
     size_t pin_n = 0;  // doubles per buffer
@@ -2066,7 +2070,10 @@ int msv_run_noise(msv_ctx* ctx, const msv_scenario* scenario, int64_t n, const d
     std::vector<uint64_t> masks;
     if (sc.routing >= 0) masks = route_masks(parts, ctx->routings[sc.routing], prof.b_max);
     const size_t nn = (size_t)std::max<int64_t>(n, 1);
-    DevBuf d_arr, d_bat, d_mult, d_lat, d_util, d_parts, d_masks, d_next, d_rec, d_use, d_out;
+    msv_ctx::NoiseRunBufs& nb = ctx->noise1;
+    DevBuf &d_arr = nb.arr, &d_bat = nb.bat, &d_mult = nb.mult, &d_lat = nb.lat, &d_util = nb.util,
+           &d_parts = nb.parts, &d_masks = nb.masks, &d_next = nb.next, &d_rec = nb.rec, &d_use = nb.use,
+           &d_out = nb.out;
     MSV_CUDA_TRY(d_arr.ensure(nn * 8));
     MSV_CUDA_TRY(d_bat.ensure(nn * 4));
     MSV_CUDA_TRY(d_mult.ensure(nn * 8));
@@ -2117,7 +2124,7 @@ int msv_run_noise(msv_ctx* ctx, const msv_scenario* scenario, int64_t n, const d
     np.n_ptr = nullptr;
     np.samples = nullptr;
     np.duration_ms = sc.duration_ms;
-    DevBuf d_job;
+    DevBuf& d_job = nb.job;
     MSV_CUDA_TRY(d_job.ensure(sizeof(msv::NoiseParams)));
     MSV_CUDA_TRY(cudaMemcpyAsync(d_job.p, &np, sizeof np, cudaMemcpyHostToDevice, st));
     MSV_CUDA_TRY(msv::launch_noise(d_job.as<msv::NoiseParams>(), 1, np.n_cells, P, st));
